@@ -1,0 +1,163 @@
+/*
+ * rsot_cuda.h -- C ABI of the B200-native RSOT dual evaluator.
+ *
+ * The drop-in boundary for rsot::evaluate_dual
+ * (/root/reference/proj/include/rsot/evaluate.hpp:79-82, implemented at
+ * proj/src/evaluate.cpp:86-174) and the target-side state of
+ * rsot::SpatialIndex (proj/include/rsot/spatial_index.hpp:15-54).  Plain C:
+ * pointers, sizes and status codes; no CUDA or torch types in signatures.
+ * Host C++ (paper_2507_23602_b200/csrc/dropin/) re-exposes it under the
+ * reference's unchanged C++ headers; Python binds it with ctypes.
+ *
+ * Layout conventions (identical to the reference's in-memory layout):
+ *   points are AoS double[3] per point, contiguous (rsot::Point =
+ *   std::array<double,3>, zero-padded for d < 3, point.hpp:10-13), i.e.
+ *   std::vector<Point>::data() can be passed as is;
+ *   masses / weights / psi / gradient are contiguous double[].
+ *
+ * Errors: every function returns RSOT_CUDA_OK (0) or a negative status;
+ * rsot_cuda_last_error() describes the last failure on the calling thread.
+ * RSOT_CUDA_INVALID_ARGUMENT corresponds to the reference's
+ * std::invalid_argument (e.g. non-finite psi, potential.hpp:42-46; empty
+ * target set, spatial_index.cpp:31-32) and is raised before any device work.
+ * There is no CPU fallback: without a usable sm_100 device every entry point
+ * that computes returns RSOT_CUDA_NO_DEVICE.
+ */
+#ifndef RSOT_CUDA_H_
+#define RSOT_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RSOT_CUDA_ABI_VERSION 1
+
+typedef enum rsot_cuda_status {
+  RSOT_CUDA_OK = 0,
+  RSOT_CUDA_INVALID_ARGUMENT = -1, /* std::invalid_argument */
+  RSOT_CUDA_RUNTIME_ERROR = -2,    /* CUDA / NCCL failure (std::runtime_error) */
+  RSOT_CUDA_NO_DEVICE = -3,        /* no usable sm_100 GPU */
+  RSOT_CUDA_UNSUPPORTED = -4       /* e.g. CostKind::SqGeodesicSphere */
+} rsot_cuda_status;
+
+typedef struct rsot_cuda_ctx rsot_cuda_ctx;         /* device, stream, comm */
+typedef struct rsot_cuda_targets rsot_cuda_targets; /* resident targets + cells */
+typedef struct rsot_cuda_atoms rsot_cuda_atoms;     /* resident atom shard */
+
+/* EvalResult scalars (evaluate.hpp:15-28).  Counters are global (summed
+ * over ranks when a communicator is attached). */
+typedef struct rsot_cuda_scalars {
+  double J;
+  double D;
+  uint64_t atoms_visited;
+  uint64_t candidate_pairs;
+  uint64_t empty_candidate_atoms;
+} rsot_cuda_scalars;
+
+int rsot_cuda_abi_version(void);
+const char* rsot_cuda_last_error(void);
+
+/* ---- context ------------------------------------------------------------
+ * One context per GPU (one process per GPU).  `device` is the CUDA ordinal.
+ * Replaces nothing in the reference (which has no device state); GPU count
+ * and selection live here, not in SolverConfig. */
+int rsot_cuda_ctx_create(int device, rsot_cuda_ctx** out);
+int rsot_cuda_ctx_destroy(rsot_cuda_ctx* ctx);
+/* Opaque cudaStream_t the context enqueues on (for event timing). */
+void* rsot_cuda_ctx_stream(rsot_cuda_ctx* ctx);
+int rsot_cuda_ctx_synchronize(rsot_cuda_ctx* ctx);
+/* Number of SMs of the context's device. */
+int rsot_cuda_ctx_num_sms(rsot_cuda_ctx* ctx);
+
+/* ---- multi-GPU (atoms sharded, targets replicated) ------------------------
+ * The gradient and scalars are combined with one ncclAllReduce(sum) per
+ * evaluation.  Rank 0 creates the id and ships its 128 bytes
+ * to the other ranks out of band (e.g. torch.distributed broadcast). */
+int rsot_cuda_comm_unique_id(unsigned char id_out[128]);
+int rsot_cuda_ctx_set_comm(rsot_cuda_ctx* ctx, int rank, int world,
+                           const unsigned char id[128]);
+/* Contiguous shard [lo, hi) of nq atoms for `rank` of `world`
+ * (same partition rule as parallel_blocks, parallel.hpp:14-31). */
+void rsot_cuda_shard_range(size_t nq, int rank, int world, size_t* lo,
+                           size_t* hi);
+
+/* ---- resident data ------------------------------------------------------- */
+/* TargetMeasure{points, weights} (measures.hpp:13-19); n >= 1 else
+ * RSOT_CUDA_INVALID_ARGUMENT ("spatial index: empty point set"). */
+int rsot_cuda_targets_create(rsot_cuda_ctx* ctx, const double* xyz,
+                             const double* nu, size_t n,
+                             rsot_cuda_targets** out);
+int rsot_cuda_targets_destroy(rsot_cuda_targets* t);
+size_t rsot_cuda_targets_size(const rsot_cuda_targets* t);
+
+/* SourceAtoms{points, masses} (measures.hpp:24-32) for this rank's shard
+ * (quad_weights and densities are not used by the evaluation). */
+int rsot_cuda_atoms_create(rsot_cuda_ctx* ctx, const double* xyz,
+                           const double* mass, size_t nq,
+                           rsot_cuda_atoms** out);
+int rsot_cuda_atoms_destroy(rsot_cuda_atoms* a);
+size_t rsot_cuda_atoms_size(const rsot_cuda_atoms* a);
+
+/* ---- evaluation ----------------------------------------------------------
+ * rsot::evaluate_dual for CostKind::SqEuclidean:
+ *   cutoff = +inf            -> dense (evaluate.cpp:119-121)
+ *   cutoff finite            -> ball query radius = sqrt(2 cutoff)
+ *                               (cost.hpp:38-42), empty sets fall back to the
+ *                               nearest target (evaluate.cpp:129-132)
+ * psi (length n) and g_out (length n) are HOST pointers; the call copies psi
+ * in, evaluates, reduces over ranks and copies g and the scalars back, then
+ * synchronises.  Non-finite psi -> RSOT_CUDA_INVALID_ARGUMENT before any
+ * device work (evaluate.cpp:91-93). */
+int rsot_cuda_eval(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
+                   rsot_cuda_targets* targets, const double* psi, double eps,
+                   double cutoff, double* g_out, rsot_cuda_scalars* out);
+
+/* Device-resident variant, asynchronous on the context stream: d_psi and
+ * d_g_out are device pointers (length n); scalars land in device memory at
+ * d_scalars as 5 doubles {J, D, atoms_visited, candidate_pairs,
+ * empty_candidate_atoms}.  Non-finite psi is reported by the next
+ * rsot_cuda_ctx_synchronize / rsot_cuda_check_status. */
+int rsot_cuda_eval_device(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
+                          rsot_cuda_targets* targets, const double* d_psi,
+                          double eps, double cutoff, double* d_g_out,
+                          double* d_scalars);
+int rsot_cuda_check_status(rsot_cuda_ctx* ctx);
+
+/* Parity/debug variant of rsot_cuda_eval that also returns, for this rank's
+ * atoms, the candidate-set size (1 for empty-fallback atoms), the wrapping
+ * sum of splitmix64(j) over the candidate set, and ln S_q.  Any of the three
+ * may be NULL. */
+int rsot_cuda_eval_debug(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
+                         rsot_cuda_targets* targets, const double* psi,
+                         double eps, double cutoff, double* g_out,
+                         rsot_cuda_scalars* out, uint32_t* cand_count,
+                         uint64_t* cand_hash, double* log_s);
+
+/* ---- spatial queries (SpatialIndex / covering_cost) ----------------------
+ * nearest target for m host points (lowest index on ties,
+ * spatial_index.cpp:70-84). */
+int rsot_cuda_nearest(rsot_cuda_ctx* ctx, rsot_cuda_targets* targets,
+                      const double* xyz, size_t m, uint64_t* out);
+/* covering_cost C0 = max_q min_j 0.5|x_q - y_j|^2 over this rank's atoms,
+ * max-reduced over ranks (spatial_index.cpp:101-121). */
+int rsot_cuda_covering_cost(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
+                            rsot_cuda_targets* targets, double* out);
+
+/* ---- measurement ----------------------------------------------------------
+ * Enables CUDA-event timing of the hot kernels inside each evaluation
+ * (events on the launching stream); rsot_cuda_last_kernel_ms returns the
+ * durations of the last evaluation's pass A and pass B launches. */
+int rsot_cuda_ctx_set_timing(rsot_cuda_ctx* ctx, int enable);
+int rsot_cuda_last_kernel_ms(rsot_cuda_ctx* ctx, double* pass_a_ms,
+                             double* pass_b_ms, double* total_ms);
+/* Measured FP64 DFMA rate of the device (lane-FMAs per second). */
+int rsot_cuda_measure_fp64_peak(rsot_cuda_ctx* ctx, double* dfma_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RSOT_CUDA_H_ */

@@ -1,0 +1,595 @@
+// capi.cu -- C ABI (include/rsot_cuda.h) over the sm_100a evaluator kernels.
+//
+// Owns the device state that the reference keeps implicitly on the host:
+// resident targets (TargetMeasure + the cell list that replaces the R*-tree
+// of spatial_index.cpp), resident atom shards (SourceAtoms), per-context
+// workspace, the stream, and the NCCL communicator for the one allreduce per
+// evaluation.  NCCL is resolved with dlopen at rsot_cuda_ctx_set_comm time so
+// the library coexists with the NCCL copy torch may already have loaded.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/rsot_cuda.h"
+#include "kernels.cuh"
+#include "truncated.cuh"
+
+using namespace rsot_cuda;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define RSOT_CK(call)                                                         \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      return fail(RSOT_CUDA_RUNTIME_ERROR,                                    \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+// ---- NCCL via dlopen -------------------------------------------------------
+struct NcclApi {
+  void* handle = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t,
+                            ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      api.handle = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (api.handle) break;
+    }
+    if (!api.handle) return;
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(api.handle, "ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(api.handle, "ncclCommInitRank"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(api.handle, "ncclAllReduce"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.handle, "ncclCommDestroy"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.handle, "ncclGetErrorString"));
+    api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy;
+  });
+  return api;
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, sizeof(T) * (n ? n : 1));
+    if (e == cudaSuccess) cap = n;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct rsot_cuda_ctx {
+  int device = 0;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  // workspace
+  DevBuf<double> psi, b2, scal, part, partS, shiftA, atomL, atomLam, atomJ,
+      atomD, partG, res, g_out, scalars_out;
+  DevBuf<int> flagged;
+  TruncWorkspace trunc;
+  double* h_pinned = nullptr;  // small pinned staging for scalars
+  bool timing = false;
+  cudaEvent_t ev[8] = {};
+  double last_ms[3] = {0, 0, 0};
+};
+
+struct rsot_cuda_targets {
+  rsot_cuda_ctx* ctx = nullptr;
+  size_t n = 0;
+  double4* y = nullptr;  // {y0, y1, y2, ln nu}
+  double* nu = nullptr;
+  TargetCells cells;     // cell list (built on demand for a radius)
+};
+
+struct rsot_cuda_atoms {
+  rsot_cuda_ctx* ctx = nullptr;
+  size_t nq = 0;
+  double4* x = nullptr;  // {x0, x1, x2, m}
+  AtomCells cells;       // cell order (built on demand)
+};
+
+namespace {
+
+int set_device(rsot_cuda_ctx* ctx) {
+  RSOT_CK(cudaSetDevice(ctx->device));
+  return RSOT_CUDA_OK;
+}
+
+int ensure_workspace(rsot_cuda_ctx* c, size_t nq, size_t n, const DenseLaunch& p) {
+  RSOT_CK(c->psi.ensure(n));
+  RSOT_CK(c->b2.ensure(n));
+  RSOT_CK(c->scal.ensure(kNumSlots));
+  RSOT_CK(c->part.ensure(4 * 1024));
+  RSOT_CK(c->partS.ensure(static_cast<size_t>(p.splitsA) * (nq ? nq : 1)));
+  RSOT_CK(c->shiftA.ensure(nq));
+  RSOT_CK(c->atomL.ensure(nq));
+  RSOT_CK(c->atomLam.ensure(nq));
+  RSOT_CK(c->atomJ.ensure(nq));
+  RSOT_CK(c->atomD.ensure(nq));
+  RSOT_CK(c->flagged.ensure(nq));
+  RSOT_CK(c->partG.ensure(static_cast<size_t>(p.splitsB) * n));
+  RSOT_CK(c->res.ensure(n + kResTail));
+  RSOT_CK(c->g_out.ensure(n));
+  RSOT_CK(c->scalars_out.ensure(kResTail));
+  return RSOT_CUDA_OK;
+}
+
+EvalBuffers buffers(rsot_cuda_ctx* c, double* g_out, double* scalars_out) {
+  EvalBuffers b;
+  b.psi = c->psi.p;
+  b.b2 = c->b2.p;
+  b.scal = c->scal.p;
+  b.part = c->part.p;
+  b.partS = c->partS.p;
+  b.shiftA = c->shiftA.p;
+  b.atomL = c->atomL.p;
+  b.atomLam = c->atomLam.p;
+  b.atomJ = c->atomJ.p;
+  b.atomD = c->atomD.p;
+  b.flagged = c->flagged.p;
+  b.partG = c->partG.p;
+  b.res = c->res.p;
+  b.g_out = g_out ? g_out : c->g_out.p;
+  b.scalars_out = scalars_out ? scalars_out : c->scalars_out.p;
+  b.timing = c->timing ? c->ev : nullptr;
+  return b;
+}
+
+// Enqueues one evaluation reading psi from b.psi (device) and leaving the
+// final gradient / scalars in b.g_out / b.scalars_out.
+int enqueue_eval(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
+                 EvalBuffers& b, double eps, double cutoff, DebugOut* dbg) {
+  const cudaStream_t s = c->stream;
+  DeviceTargets dt{t->y, t->nu, static_cast<int>(t->n)};
+  DeviceAtoms da{a->x, static_cast<int>(a->nq)};
+  if (b.timing) cudaEventRecord(b.timing[0], s);
+  launch_prologue(dt, b, eps, s);
+  if (std::isfinite(cutoff)) {
+    const int rc = run_truncated(c->trunc, da, a->cells, dt, t->cells, b, eps,
+                                 cutoff, c->num_sms, dbg, s, g_last_error);
+    if (rc != 0) return fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error);
+  } else {
+    const DenseLaunch plan = plan_dense(da.nq, dt.n, c->num_sms);
+    launch_dense(da, dt, b, plan, eps, s);
+    if (dbg) launch_dense_debug(da, dt, b, *dbg, s);
+  }
+  if (c->comm) {
+    NcclApi& api = nccl();
+    const ncclResult_t r = api.AllReduce(b.res, b.res, t->n + kResTail,
+                                         ncclDouble, ncclSum, c->comm, s);
+    if (r != ncclSuccess)
+      return fail(RSOT_CUDA_RUNTIME_ERROR,
+                  std::string("ncclAllReduce: ") + api.GetErrorString(r));
+  }
+  launch_finalize(dt, b, s);
+  if (b.timing) cudaEventRecord(b.timing[5], s);
+  RSOT_CK(cudaGetLastError());
+  return RSOT_CUDA_OK;
+}
+
+void record_timing(rsot_cuda_ctx* c) {
+  if (!c->timing) return;
+  float a = 0.f, bb = 0.f, tot = 0.f;
+  cudaEventElapsedTime(&a, c->ev[1], c->ev[2]);
+  cudaEventElapsedTime(&bb, c->ev[3], c->ev[4]);
+  cudaEventElapsedTime(&tot, c->ev[0], c->ev[5]);
+  c->last_ms[0] = a;
+  c->last_ms[1] = bb;
+  c->last_ms[2] = tot;
+}
+
+int check_ready(rsot_cuda_ctx* ctx, rsot_cuda_atoms* a, rsot_cuda_targets* t) {
+  if (!ctx || !a || !t) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null handle");
+  if (a->ctx != ctx || t->ctx != ctx)
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "handles belong to another context");
+  return set_device(ctx);
+}
+
+int finish_host_eval(rsot_cuda_ctx* c, rsot_cuda_targets* t, double* g_out,
+                     rsot_cuda_scalars* out) {
+  const cudaStream_t s = c->stream;
+  RSOT_CK(cudaMemcpyAsync(c->h_pinned, c->scalars_out.p, sizeof(double) * kResTail,
+                          cudaMemcpyDeviceToHost, s));
+  RSOT_CK(cudaMemcpyAsync(c->h_pinned + kResTail, c->scal.p + kSlotNonFinite,
+                          sizeof(double), cudaMemcpyDeviceToHost, s));
+  RSOT_CK(cudaMemcpyAsync(g_out, c->g_out.p, sizeof(double) * t->n,
+                          cudaMemcpyDeviceToHost, s));
+  RSOT_CK(cudaStreamSynchronize(s));
+  record_timing(c);
+  if (c->h_pinned[kResTail] != 0.0)
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "potential has non-finite entries");
+  out->J = c->h_pinned[kResJ];
+  out->D = c->h_pinned[kResD];
+  out->candidate_pairs = static_cast<uint64_t>(c->h_pinned[kResPairs]);
+  out->empty_candidate_atoms = static_cast<uint64_t>(c->h_pinned[kResEmpty]);
+  out->atoms_visited = static_cast<uint64_t>(c->h_pinned[kResVisited]);
+  return RSOT_CUDA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rsot_cuda_abi_version(void) { return RSOT_CUDA_ABI_VERSION; }
+
+const char* rsot_cuda_last_error(void) { return g_last_error.c_str(); }
+
+int rsot_cuda_ctx_create(int device, rsot_cuda_ctx** out) {
+  if (!out) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null output pointer");
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(RSOT_CUDA_NO_DEVICE, "no CUDA device visible");
+  }
+  if (device < 0 || device >= count)
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "device ordinal out of range");
+  cudaDeviceProp prop;
+  RSOT_CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(RSOT_CUDA_NO_DEVICE,
+                "device is not sm_100 (built for sm_100a only): " +
+                    std::string(prop.name));
+  auto* c = new (std::nothrow) rsot_cuda_ctx();
+  if (!c) return fail(RSOT_CUDA_RUNTIME_ERROR, "out of host memory");
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  RSOT_CK(cudaSetDevice(device));
+  RSOT_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  RSOT_CK(cudaMallocHost(&c->h_pinned, sizeof(double) * 64));
+  for (auto& e : c->ev) RSOT_CK(cudaEventCreate(&e));
+  *out = c;
+  return RSOT_CUDA_OK;
+}
+
+int rsot_cuda_ctx_destroy(rsot_cuda_ctx* c) {
+  if (!c) return RSOT_CUDA_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (c->comm) nccl().CommDestroy(c->comm);
+  c->psi.release(); c->b2.release(); c->scal.release(); c->part.release();
+  c->partS.release(); c->shiftA.release(); c->atomL.release();
+  c->atomLam.release(); c->atomJ.release(); c->atomD.release();
+  c->partG.release(); c->res.release(); c->g_out.release();
+  c->scalars_out.release(); c->flagged.release();
+  c->trunc.release();
+  if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  for (auto& e : c->ev) if (e) cudaEventDestroy(e);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return RSOT_CUDA_OK;
+}
+
+void* rsot_cuda_ctx_stream(rsot_cuda_ctx* c) { return c ? c->stream : nullptr; }
+
+int rsot_cuda_ctx_synchronize(rsot_cuda_ctx* c) {
+  if (!c) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null context");
+  RSOT_CK(cudaSetDevice(c->device));
+  RSOT_CK(cudaStreamSynchronize(c->stream));
+  record_timing(c);
+  return RSOT_CUDA_OK;
+}
+
+int rsot_cuda_ctx_num_sms(rsot_cuda_ctx* c) { return c ? c->num_sms : 0; }
+
+int rsot_cuda_comm_unique_id(unsigned char id_out[128]) {
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(RSOT_CUDA_RUNTIME_ERROR, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  const ncclResult_t r = api.GetUniqueId(&id);
+  if (r != ncclSuccess)
+    return fail(RSOT_CUDA_RUNTIME_ERROR, std::string("ncclGetUniqueId: ") + api.GetErrorString(r));
+  static_assert(sizeof(id.internal) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id_out, id.internal, 128);
+  return RSOT_CUDA_OK;
+}
+
+int rsot_cuda_ctx_set_comm(rsot_cuda_ctx* c, int rank, int world,
+                           const unsigned char id[128]) {
+  if (!c) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null context");
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "bad rank/world");
+  c->rank = rank;
+  c->world = world;
+  if (world == 1) return RSOT_CUDA_OK;
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(RSOT_CUDA_RUNTIME_ERROR, "libnccl.so.2 not loadable");
+  const int rc = set_device(c);
+  if (rc) return rc;
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, id, 128);
+  const ncclResult_t r = api.CommInitRank(&c->comm, world, uid, rank);
+  if (r != ncclSuccess)
+    return fail(RSOT_CUDA_RUNTIME_ERROR, std::string("ncclCommInitRank: ") + api.GetErrorString(r));
+  return RSOT_CUDA_OK;
+}
+
+void rsot_cuda_shard_range(size_t nq, int rank, int world, size_t* lo, size_t* hi) {
+  if (world <= 1 || nq < 2) {
+    *lo = rank == 0 ? 0 : nq;
+    *hi = nq;
+    if (rank != 0) *lo = *hi = nq;
+    return;
+  }
+  const size_t w = static_cast<size_t>(world) < nq ? static_cast<size_t>(world) : nq;
+  const size_t chunk = (nq + w - 1) / w;
+  size_t l = static_cast<size_t>(rank) * chunk;
+  size_t h = l + chunk;
+  if (l > nq) l = nq;
+  if (h > nq) h = nq;
+  *lo = l;
+  *hi = h;
+}
+
+int rsot_cuda_targets_create(rsot_cuda_ctx* c, const double* xyz, const double* nu,
+                             size_t n, rsot_cuda_targets** out) {
+  if (!c || !out) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (n == 0) return fail(RSOT_CUDA_INVALID_ARGUMENT, "spatial index: empty point set");
+  if (!xyz || !nu) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null data pointer");
+  if (n > (1u << 30)) return fail(RSOT_CUDA_INVALID_ARGUMENT, "too many targets");
+  int rc = set_device(c);
+  if (rc) return rc;
+  std::vector<double4> h(n);
+  for (size_t j = 0; j < n; ++j)
+    h[j] = make_double4(xyz[3 * j], xyz[3 * j + 1], xyz[3 * j + 2], std::log(nu[j]));
+  auto* t = new rsot_cuda_targets();
+  for (int d = 0; d < 3; ++d) t->cells.bbox_lo[d] = t->cells.bbox_hi[d] = xyz[d];
+  for (size_t j = 1; j < n; ++j)
+    for (int d = 0; d < 3; ++d) {
+      const double v = xyz[3 * j + d];
+      if (!std::isfinite(v)) {
+        delete t;
+        return fail(RSOT_CUDA_INVALID_ARGUMENT, "target point has non-finite coordinates");
+      }
+      t->cells.bbox_lo[d] = std::min(t->cells.bbox_lo[d], v);
+      t->cells.bbox_hi[d] = std::max(t->cells.bbox_hi[d], v);
+    }
+  t->cells.bbox_set = true;
+  t->ctx = c;
+  t->n = n;
+  RSOT_CK(cudaMalloc(&t->y, sizeof(double4) * n));
+  RSOT_CK(cudaMalloc(&t->nu, sizeof(double) * n));
+  RSOT_CK(cudaMemcpyAsync(t->y, h.data(), sizeof(double4) * n, cudaMemcpyHostToDevice, c->stream));
+  RSOT_CK(cudaMemcpyAsync(t->nu, nu, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  RSOT_CK(cudaStreamSynchronize(c->stream));
+  *out = t;
+  return RSOT_CUDA_OK;
+}
+
+int rsot_cuda_targets_destroy(rsot_cuda_targets* t) {
+  if (!t) return RSOT_CUDA_OK;
+  cudaSetDevice(t->ctx->device);
+  cudaStreamSynchronize(t->ctx->stream);
+  cudaFree(t->y);
+  cudaFree(t->nu);
+  t->cells.release();
+  delete t;
+  return RSOT_CUDA_OK;
+}
+
+size_t rsot_cuda_targets_size(const rsot_cuda_targets* t) { return t ? t->n : 0; }
+
+int rsot_cuda_atoms_create(rsot_cuda_ctx* c, const double* xyz, const double* mass,
+                           size_t nq, rsot_cuda_atoms** out) {
+  if (!c || !out) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (nq && (!xyz || !mass)) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null data pointer");
+  if (nq > (1u << 30)) return fail(RSOT_CUDA_INVALID_ARGUMENT, "too many atoms");
+  int rc = set_device(c);
+  if (rc) return rc;
+  std::vector<double4> h(nq);
+  for (size_t q = 0; q < nq; ++q)
+    h[q] = make_double4(xyz[3 * q], xyz[3 * q + 1], xyz[3 * q + 2], mass[q]);
+  auto* a = new rsot_cuda_atoms();
+  if (nq) {
+    for (int d = 0; d < 3; ++d) a->cells.bbox_lo[d] = a->cells.bbox_hi[d] = xyz[d];
+    for (size_t q = 1; q < nq; ++q)
+      for (int d = 0; d < 3; ++d) {
+        const double v = xyz[3 * q + d];
+        a->cells.bbox_lo[d] = std::min(a->cells.bbox_lo[d], v);
+        a->cells.bbox_hi[d] = std::max(a->cells.bbox_hi[d], v);
+      }
+  }
+  a->cells.bbox_set = true;
+  a->ctx = c;
+  a->nq = nq;
+  RSOT_CK(cudaMalloc(&a->x, sizeof(double4) * (nq ? nq : 1)));
+  if (nq)
+    RSOT_CK(cudaMemcpyAsync(a->x, h.data(), sizeof(double4) * nq, cudaMemcpyHostToDevice, c->stream));
+  RSOT_CK(cudaStreamSynchronize(c->stream));
+  *out = a;
+  return RSOT_CUDA_OK;
+}
+
+int rsot_cuda_atoms_destroy(rsot_cuda_atoms* a) {
+  if (!a) return RSOT_CUDA_OK;
+  cudaSetDevice(a->ctx->device);
+  cudaStreamSynchronize(a->ctx->stream);
+  cudaFree(a->x);
+  a->cells.release();
+  delete a;
+  return RSOT_CUDA_OK;
+}
+
+size_t rsot_cuda_atoms_size(const rsot_cuda_atoms* a) { return a ? a->nq : 0; }
+
+static int eval_common(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
+                       const double* psi_host, const double* psi_dev, double eps,
+                       double cutoff, double* g_dev, double* scal_dev,
+                       DebugOut* dbg) {
+  if (!(eps > 0.0)) return fail(RSOT_CUDA_INVALID_ARGUMENT, "epsilon must be > 0");
+  if (std::isnan(cutoff)) cutoff = INFINITY;  // isfinite(NaN) is false: dense
+  const DenseLaunch plan = plan_dense(static_cast<int>(a->nq), static_cast<int>(t->n), c->num_sms);
+  int rc = ensure_workspace(c, a->nq, t->n, plan);
+  if (rc) return rc;
+  EvalBuffers b = buffers(c, g_dev, scal_dev);
+  if (psi_host)
+    RSOT_CK(cudaMemcpyAsync(b.psi, psi_host, sizeof(double) * t->n,
+                            cudaMemcpyHostToDevice, c->stream));
+  else
+    b.psi = const_cast<double*>(psi_dev);
+  return enqueue_eval(c, a, t, b, eps, cutoff, dbg);
+}
+
+int rsot_cuda_eval(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
+                   const double* psi, double eps, double cutoff, double* g_out,
+                   rsot_cuda_scalars* out) {
+  int rc = check_ready(c, a, t);
+  if (rc) return rc;
+  if (!psi || !g_out || !out) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  rc = eval_common(c, a, t, psi, nullptr, eps, cutoff, nullptr, nullptr, nullptr);
+  if (rc) return rc;
+  return finish_host_eval(c, t, g_out, out);
+}
+
+int rsot_cuda_eval_device(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
+                          const double* d_psi, double eps, double cutoff,
+                          double* d_g_out, double* d_scalars) {
+  int rc = check_ready(c, a, t);
+  if (rc) return rc;
+  if (!d_psi || !d_g_out || !d_scalars)
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  return eval_common(c, a, t, nullptr, d_psi, eps, cutoff, d_g_out, d_scalars, nullptr);
+}
+
+int rsot_cuda_check_status(rsot_cuda_ctx* c) {
+  if (!c) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null context");
+  RSOT_CK(cudaSetDevice(c->device));
+  RSOT_CK(cudaMemcpyAsync(c->h_pinned, c->scal.p + kSlotNonFinite, sizeof(double),
+                          cudaMemcpyDeviceToHost, c->stream));
+  RSOT_CK(cudaStreamSynchronize(c->stream));
+  if (c->h_pinned[0] != 0.0)
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "potential has non-finite entries");
+  return RSOT_CUDA_OK;
+}
+
+int rsot_cuda_eval_debug(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
+                         const double* psi, double eps, double cutoff, double* g_out,
+                         rsot_cuda_scalars* out, uint32_t* cand_count,
+                         uint64_t* cand_hash, double* log_s) {
+  int rc = check_ready(c, a, t);
+  if (rc) return rc;
+  if (!psi || !g_out || !out) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  DebugOut dbg;
+  const size_t nq = a->nq ? a->nq : 1;
+  RSOT_CK(cudaMalloc(&dbg.count, sizeof(uint32_t) * nq));
+  RSOT_CK(cudaMalloc(&dbg.hash, sizeof(uint64_t) * nq));
+  RSOT_CK(cudaMalloc(&dbg.log_s, sizeof(double) * nq));
+  rc = eval_common(c, a, t, psi, nullptr, eps, cutoff, nullptr, nullptr, &dbg);
+  if (rc == 0) rc = finish_host_eval(c, t, g_out, out);
+  if (rc == 0 && a->nq) {
+    if (cand_count)
+      cudaMemcpy(cand_count, dbg.count, sizeof(uint32_t) * a->nq, cudaMemcpyDeviceToHost);
+    if (cand_hash)
+      cudaMemcpy(cand_hash, dbg.hash, sizeof(uint64_t) * a->nq, cudaMemcpyDeviceToHost);
+    if (log_s)
+      cudaMemcpy(log_s, dbg.log_s, sizeof(double) * a->nq, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(dbg.count);
+  cudaFree(dbg.hash);
+  cudaFree(dbg.log_s);
+  return rc;
+}
+
+int rsot_cuda_nearest(rsot_cuda_ctx* c, rsot_cuda_targets* t, const double* xyz,
+                      size_t m, uint64_t* out) {
+  if (!c || !t || (m && (!xyz || !out)))
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  int rc = set_device(c);
+  if (rc) return rc;
+  if (m == 0) return RSOT_CUDA_OK;
+  rc = run_nearest_points(c->trunc, DeviceTargets{t->y, t->nu, static_cast<int>(t->n)},
+                          t->cells, xyz, m, out, c->stream, g_last_error);
+  return rc ? fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error) : RSOT_CUDA_OK;
+}
+
+int rsot_cuda_covering_cost(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
+                            double* out) {
+  int rc = check_ready(c, a, t);
+  if (rc) return rc;
+  if (!out) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  double c0 = 0.0;
+  rc = run_covering_cost(c->trunc, DeviceAtoms{a->x, static_cast<int>(a->nq)},
+                         DeviceTargets{t->y, t->nu, static_cast<int>(t->n)}, t->cells,
+                         &c0, c->stream, g_last_error);
+  if (rc) return fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error);
+  if (c->comm) {
+    // max over ranks: all values are >= 0, so a max-allreduce is exact.
+    RSOT_CK(cudaMemcpyAsync(c->scal.p, &c0, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    NcclApi& api = nccl();
+    const ncclResult_t r = api.AllReduce(c->scal.p, c->scal.p, 1, ncclDouble, ncclMax,
+                                         c->comm, c->stream);
+    if (r != ncclSuccess)
+      return fail(RSOT_CUDA_RUNTIME_ERROR, std::string("ncclAllReduce: ") + api.GetErrorString(r));
+    RSOT_CK(cudaMemcpyAsync(c->h_pinned, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    RSOT_CK(cudaStreamSynchronize(c->stream));
+    c0 = c->h_pinned[0];
+  }
+  *out = c0;
+  return RSOT_CUDA_OK;
+}
+
+int rsot_cuda_ctx_set_timing(rsot_cuda_ctx* c, int enable) {
+  if (!c) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null context");
+  c->timing = enable != 0;
+  return RSOT_CUDA_OK;
+}
+
+int rsot_cuda_last_kernel_ms(rsot_cuda_ctx* c, double* a, double* b, double* tot) {
+  if (!c) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null context");
+  if (a) *a = c->last_ms[0];
+  if (b) *b = c->last_ms[1];
+  if (tot) *tot = c->last_ms[2];
+  return RSOT_CUDA_OK;
+}
+
+int rsot_cuda_measure_fp64_peak(rsot_cuda_ctx* c, double* out) {
+  if (!c || !out) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  int rc = set_device(c);
+  if (rc) return rc;
+  *out = measure_dfma_rate(c->stream);
+  RSOT_CK(cudaGetLastError());
+  return RSOT_CUDA_OK;
+}
+
+}  // extern "C"

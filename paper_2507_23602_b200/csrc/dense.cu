@@ -1,0 +1,528 @@
+// dense.cu -- dense (untruncated) dual objective + gradient on sm_100a.
+//
+// Reference: rsot::evaluate_dual, proj/src/evaluate.cpp:86-174, cutoff=+inf
+// branch (candidates = all targets, :119-121).
+//
+// Two passes, both FP64-pipe bound (no tensor cores: d <= 3):
+//   pass A (atom-major):  S~_q = sum_j 2^(e2_qj - B + c2|x'_q|^2) over target
+//     tiles staged in shared memory (broadcast reads), fixed shift
+//     B = max_j b2_j, so target splits combine by plain addition.
+//     Finalise: ln S_q = ln2 (B - c2|x'|^2 + log2 S~_q); J_q, D_q.
+//   pass B (target-major): G_j = sum_q 2^(e2_qj - log2 S_q + log2 m_q) over
+//     atom tiles staged in shared memory; each thread owns its targets, so
+//     the scatter of evaluate.cpp:151-153 becomes a register gather with a
+//     fixed summation order (no atomics), split over atom ranges and reduced
+//     in fixed order.  Bitwise reproducible for a fixed launch plan.
+#include <cmath>
+#include <cstdio>
+
+#include "block_util.cuh"
+#include "device_math.cuh"
+#include "kernels.cuh"
+
+namespace rsot_cuda {
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kTile = 256;
+constexpr int kRedBlocks = 1024;
+
+// Centre of the block's bounding box (block-uniform).
+template <int BLK>
+__device__ void block_bbox_center(double lo0, double lo1, double lo2,
+                                  double hi0, double hi1, double hi2,
+                                  double* sh, double* o) {
+  const double lo[3] = {lo0, lo1, lo2}, hi[3] = {hi0, hi1, hi2};
+  double box[6];
+  block_bbox<BLK>(lo, hi, sh, box);
+  o[0] = 0.5 * (box[0] + box[3]);
+  o[1] = 0.5 * (box[1] + box[4]);
+  o[2] = 0.5 * (box[2] + box[5]);
+}
+
+// ---------------------------------------------------------------------------
+// Prologue: b2_j = log2(e) (psi_j/eps + ln nu_j); B = max b2; sum psi nu.
+
+__global__ void prologue_blocks(const double4* __restrict__ tgt,
+                                const double* __restrict__ nu,
+                                const double* __restrict__ psi, int n,
+                                double inv_eps, double* __restrict__ b2,
+                                double* __restrict__ part, int chunk) {
+  __shared__ double sh[256];
+  const int lo = blockIdx.x * chunk;
+  const int hi = min(n, lo + chunk);
+  double mx = -INFINITY, s = 0.0, bad = 0.0;
+  for (int j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+    const double p = psi[j];
+    if (!isfinite(p)) bad = 1.0;
+    const double v = kLog2e * fma(p, inv_eps, tgt[j].w);
+    b2[j] = v;
+    mx = fmax(mx, v);
+    s = fma(p, nu[j], s);
+  }
+  mx = block_max<256>(mx, sh);
+  s = block_sum<256>(s, sh);
+  bad = block_max<256>(bad, sh);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = mx;
+    part[kRedBlocks + blockIdx.x] = s;
+    part[2 * kRedBlocks + blockIdx.x] = bad;
+  }
+}
+
+__global__ void prologue_final(const double* __restrict__ part, int nblk,
+                               double* __restrict__ scal) {
+  __shared__ double sh[256];
+  double mx = -INFINITY, s = 0.0, bad = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    mx = fmax(mx, part[i]);
+    s += part[kRedBlocks + i];
+    bad = fmax(bad, part[2 * kRedBlocks + i]);
+  }
+  mx = block_max<256>(mx, sh);
+  s = block_sum<256>(s, sh);
+  bad = block_max<256>(bad, sh);
+  if (threadIdx.x == 0) {
+    scal[kSlotB] = mx;
+    scal[kSlotPsiNu] = s;
+    scal[kSlotNonFinite] = bad;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pass A (atom-major LSE).  grid = (ceil(nq / (128*APT)), splitsA).
+
+// Accumulates one staged target tile into the APT running sums.  WIDE adds
+// the per-atom shift -c2|x'|^2 to every exponent (one extra DADD per pair);
+// it is used only when the CTA's atoms are spread so widely that the
+// shifted exponent could overflow (c2 * half-diagonal^2 > 400).
+template <int APT, bool WIDE>
+__device__ __forceinline__ void passA_tile(const double4* __restrict__ tile, int cnt,
+                                           const double (&X)[APT][3], const double (&sub)[APT],
+                                           double (&S)[APT], const double* __restrict__ tbl) {
+#pragma unroll 2
+  for (int t = 0; t < cnt; ++t) {
+    const double4 y = tile[t];
+#pragma unroll
+    for (int k = 0; k < APT; ++k) {
+      double s = fma(X[k][0], y.x, fma(X[k][1], y.y, fma(X[k][2], y.z, y.w)));
+      if (WIDE) s -= sub[k];
+      S[k] = exp2_acc(s, S[k], tbl);
+    }
+  }
+}
+
+template <int APT>
+__global__ void __launch_bounds__(kThreads)
+dense_passA(const double4* __restrict__ atoms, int nq,
+            const double4* __restrict__ tgt, const double* __restrict__ b2,
+            int n, int per_split, const double* __restrict__ scal, double c2,
+            double* __restrict__ partS, double* __restrict__ shiftA) {
+  __shared__ double4 tile[kTile];
+  __shared__ double tbl[16];
+  __shared__ double sh[200];
+  load_exp2_table(tbl);
+
+  const int q0 = blockIdx.x * (kThreads * APT) + threadIdx.x;
+  double x[APT][3];
+  double lo[3] = {INFINITY, INFINITY, INFINITY};
+  double hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int k = 0; k < APT; ++k) {
+    const int q = q0 + k * kThreads;
+    if (q < nq) {
+      const double4 a = atoms[q];
+      x[k][0] = a.x; x[k][1] = a.y; x[k][2] = a.z;
+      lo[0] = fmin(lo[0], a.x); hi[0] = fmax(hi[0], a.x);
+      lo[1] = fmin(lo[1], a.y); hi[1] = fmax(hi[1], a.y);
+      lo[2] = fmin(lo[2], a.z); hi[2] = fmax(hi[2], a.z);
+    } else {
+      x[k][0] = x[k][1] = x[k][2] = 0.0;
+    }
+  }
+  double box[6];
+  block_bbox<kThreads>(lo, hi, sh, box);
+  double o[3], hd2 = 0.0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    o[d] = 0.5 * (box[d] + box[d + 3]);
+    const double e = 0.5 * (box[d + 3] - box[d]);
+    hd2 += e * e;
+  }
+  const bool wide = c2 * hd2 > 400.0;
+  const double B = scal[kSlotB];
+  const double c2x2 = 2.0 * c2;
+  double X[APT][3], S[APT], sub[APT];
+#pragma unroll
+  for (int k = 0; k < APT; ++k) {
+    const int q = q0 + k * kThreads;
+    const bool ok = q < nq;
+    const double x0 = x[k][0] - o[0], x1 = x[k][1] - o[1], x2 = x[k][2] - o[2];
+    X[k][0] = ok ? c2x2 * x0 : 0.0;
+    X[k][1] = ok ? c2x2 * x1 : 0.0;
+    X[k][2] = ok ? c2x2 * x2 : 0.0;
+    sub[k] = ok ? c2 * fma(x2, x2, fma(x1, x1, x0 * x0)) : 0.0;
+    S[k] = 0.0;
+  }
+
+  const int j0 = blockIdx.y * per_split;
+  const int j1 = min(n, j0 + per_split);
+  for (int base = j0; base < j1; base += kTile) {
+    const int cnt = min(kTile, j1 - base);
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt; t += kThreads) {
+      const double4 y = tgt[base + t];
+      const double y0 = y.x - o[0], y1 = y.y - o[1], y2 = y.z - o[2];
+      const double yy = fma(y2, y2, fma(y1, y1, y0 * y0));
+      double w = fma(-c2, yy, b2[base + t]) - B;
+      w = fmax(w, -1.0e5);  // nu_j = 0 => b2 = -inf: contributes 0
+      tile[t] = make_double4(y0, y1, y2, w);
+    }
+    __syncthreads();
+    if (wide)
+      passA_tile<APT, true>(tile, cnt, X, sub, S, tbl);
+    else
+      passA_tile<APT, false>(tile, cnt, X, sub, S, tbl);
+  }
+#pragma unroll
+  for (int k = 0; k < APT; ++k) {
+    const int q = q0 + k * kThreads;
+    if (q < nq) {
+      partS[(size_t)blockIdx.y * nq + q] = S[k];
+      if (blockIdx.y == 0) shiftA[q] = wide ? 0.0 : sub[k];
+    }
+  }
+}
+
+// Per-atom finalisation of pass A.
+__global__ void dense_finalizeA(const double4* __restrict__ atoms, int nq,
+                                const double* __restrict__ partS, int splits,
+                                const double* __restrict__ shiftA,
+                                double* __restrict__ scal, double eps,
+                                double* __restrict__ atomL,
+                                double* __restrict__ atomLam,
+                                double* __restrict__ atomJ,
+                                double* __restrict__ atomD,
+                                int* __restrict__ flagged) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  double S = 0.0;
+  for (int s = 0; s < splits; ++s) S += partS[(size_t)s * nq + q];
+  const double m = atoms[q].w;
+  // Subnormal / zero / overflowing sums lose the reference's accuracy:
+  // recompute those atoms exactly (per-atom max shift) in the fallback.
+  const bool bad = !(S >= 0x1p-960) || !(S <= 0x1p960);
+  if (bad) {
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(&scal[kSlotFlagCount]);
+    const unsigned long long f = atomicAdd(cnt, 1ull);
+    flagged[f] = q;
+    S = 1.0;  // placeholder, overwritten by the fallback
+  }
+  const double L2 = (scal[kSlotB] - shiftA[q]) + log2(S);
+  const double L = L2 * kLn2;
+  atomL[q] = L;
+  atomJ[q] = eps * L * m;
+  atomD[q] = m * exp(-L);
+  atomLam[q] = fmax(log2(m) - L2, -1.0e5);
+}
+
+// Exact per-atom LSE with the reference's per-atom max shift
+// (evaluate.cpp:136-150) for atoms flagged by the fast path.
+__global__ void dense_exact_fallback(const double4* __restrict__ atoms,
+                                     const double4* __restrict__ tgt,
+                                     const double* __restrict__ psi, int n,
+                                     const double* __restrict__ scal,
+                                     const int* __restrict__ flagged,
+                                     double eps, double* __restrict__ atomL,
+                                     double* __restrict__ atomLam,
+                                     double* __restrict__ atomJ,
+                                     double* __restrict__ atomD) {
+  __shared__ double sh[256];
+  const unsigned long long nflag =
+      *reinterpret_cast<const unsigned long long*>(&scal[kSlotFlagCount]);
+  for (unsigned long long f = blockIdx.x; f < nflag; f += gridDim.x) {
+    const int q = flagged[f];
+    const double4 a = atoms[q];
+    double mx = -INFINITY;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const double4 y = tgt[j];
+      const double d2 = exact_sqdist(a.x, a.y, a.z, y.x, y.y, y.z);
+      mx = fmax(mx, reference_exponent(psi[j], d2, eps, y.w));
+    }
+    mx = block_max<256>(mx, sh);
+    double s = 0.0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const double4 y = tgt[j];
+      const double d2 = exact_sqdist(a.x, a.y, a.z, y.x, y.y, y.z);
+      s += exp(reference_exponent(psi[j], d2, eps, y.w) - mx);
+    }
+    s = block_sum<256>(s, sh);
+    if (threadIdx.x == 0) {
+      const double L = mx + log(s);
+      atomL[q] = L;
+      atomJ[q] = eps * L * a.w;
+      atomD[q] = a.w * exp(-L);
+      atomLam[q] = fmax(log2(a.w) - L * kLog2e, -1.0e5);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pass B (target-major gather).  grid = (ceil(n / (128*TPT)), splitsB).
+
+template <int TPT>
+__global__ void __launch_bounds__(kThreads)
+dense_passB(const double4* __restrict__ atoms, const double* __restrict__ atomLam,
+            int nq, int per_split, const double4* __restrict__ tgt,
+            const double* __restrict__ b2, int n, double c2,
+            double* __restrict__ partG) {
+  __shared__ double4 tile[kTile];
+  __shared__ double tbl[16];
+  __shared__ double sh[200];
+  load_exp2_table(tbl);
+
+  const int j0 = blockIdx.x * (kThreads * TPT) + threadIdx.x;
+  double y[TPT][3], T[TPT], G[TPT];
+  double lo[3] = {INFINITY, INFINITY, INFINITY};
+  double hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int j = j0 + k * kThreads;
+    if (j < n) {
+      const double4 v = tgt[j];
+      y[k][0] = v.x; y[k][1] = v.y; y[k][2] = v.z;
+      lo[0] = fmin(lo[0], v.x); hi[0] = fmax(hi[0], v.x);
+      lo[1] = fmin(lo[1], v.y); hi[1] = fmax(hi[1], v.y);
+      lo[2] = fmin(lo[2], v.z); hi[2] = fmax(hi[2], v.z);
+    } else {
+      y[k][0] = y[k][1] = y[k][2] = 0.0;
+    }
+  }
+  double o[3];
+  block_bbox_center<kThreads>(lo[0], lo[1], lo[2], hi[0], hi[1], hi[2], sh, o);
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int j = j0 + k * kThreads;
+    y[k][0] -= o[0]; y[k][1] -= o[1]; y[k][2] -= o[2];
+    const double yy = fma(y[k][2], y[k][2], fma(y[k][1], y[k][1], y[k][0] * y[k][0]));
+    T[k] = (j < n) ? fmax(fma(-c2, yy, b2[j]), -1.0e5) : -1.0e5;
+    G[k] = 0.0;
+  }
+  const double c2x2 = 2.0 * c2;
+  const int q0 = blockIdx.y * per_split;
+  const int q1 = min(nq, q0 + per_split);
+  for (int base = q0; base < q1; base += kTile) {
+    const int cnt = min(kTile, q1 - base);
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt; t += kThreads) {
+      const double4 a = atoms[base + t];
+      const double x0 = a.x - o[0], x1 = a.y - o[1], x2 = a.z - o[2];
+      const double xx = fma(x2, x2, fma(x1, x1, x0 * x0));
+      const double A = fma(-c2, xx, atomLam[base + t]);
+      tile[t] = make_double4(c2x2 * x0, c2x2 * x1, c2x2 * x2, A);
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int t = 0; t < cnt; ++t) {
+      const double4 X = tile[t];
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        const double s = fma(X.x, y[k][0], fma(X.y, y[k][1], fma(X.z, y[k][2], T[k] + X.w)));
+        G[k] = exp2_acc(s, G[k], tbl);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int j = j0 + k * kThreads;
+    if (j < n) partG[(size_t)blockIdx.y * n + j] = G[k];
+  }
+}
+
+__global__ void reduce_partG(const double* __restrict__ partG, int splits, int n,
+                             double* __restrict__ res) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double g = 0.0;
+  for (int s = 0; s < splits; ++s) g += partG[(size_t)s * n + j];
+  res[j] = g;
+}
+
+__global__ void det_sum_blocks(const double* __restrict__ x, size_t n,
+                               size_t chunk, double* __restrict__ part) {
+  __shared__ double sh[256];
+  const size_t lo = blockIdx.x * chunk;
+  const size_t hi = min(n, lo + chunk);
+  double s = 0.0;
+  for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += x[i];
+  s = block_sum<256>(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void det_sum_final(const double* __restrict__ part, int nblk,
+                              double* __restrict__ out) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) s += part[i];
+  s = block_sum<256>(s, sh);
+  if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void set_dense_counts(double* __restrict__ res, int n, double nq) {
+  res[n + kResPairs] = nq * static_cast<double>(n);
+  res[n + kResEmpty] = 0.0;
+  res[n + kResVisited] = nq;
+}
+
+__global__ void finalize_kernel(const double* __restrict__ res,
+                                const double* __restrict__ nu, int n,
+                                const double* __restrict__ scal,
+                                double* __restrict__ g_out,
+                                double* __restrict__ scalars_out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) g_out[j] = res[j] - nu[j];
+  if (j == 0) {
+    scalars_out[kResJ] = res[n + kResJ] - scal[kSlotPsiNu];
+    scalars_out[kResD] = res[n + kResD];
+    scalars_out[kResPairs] = res[n + kResPairs];
+    scalars_out[kResEmpty] = res[n + kResEmpty];
+    scalars_out[kResVisited] = res[n + kResVisited];
+  }
+}
+
+__global__ void dfma_probe(double* out, double a, double b, int iters) {
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+  double x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+    x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+    x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+
+int red_blocks(size_t n) {
+  size_t b = (n + 4095) / 4096;
+  if (b < 1) b = 1;
+  if (b > kRedBlocks) b = kRedBlocks;
+  return static_cast<int>(b);
+}
+
+}  // namespace
+
+DenseLaunch plan_dense(int nq, int n, int num_sms) {
+  DenseLaunch p;
+  // Enough CTAs for ~16 waves of ~6 resident CTAs per SM, while keeping
+  // at least 512 targets (pass A) / 1024 atoms (pass B) per CTA.
+  const long want = 16L * num_sms * 6;
+  p.apt = (nq >= 64L * 256 * num_sms) ? 2 : 1;
+  const long ablocks = (nq + kThreads * p.apt - 1) / (kThreads * p.apt);
+  long sa = (want + ablocks - 1) / ablocks;
+  long max_sa = (n + 511) / 512;
+  if (sa > max_sa) sa = max_sa;
+  if (sa < 1) sa = 1;
+  p.splitsA = static_cast<int>(sa);
+  p.tpt = (n >= 4L * 256 * num_sms) ? 2 : 1;
+  const long tblocks = (n + kThreads * p.tpt - 1) / (kThreads * p.tpt);
+  long sb = (want + tblocks - 1) / tblocks;
+  long max_sb = (nq + 1023) / 1024;
+  if (sb > max_sb) sb = max_sb;
+  if (sb < 1) sb = 1;
+  p.splitsB = static_cast<int>(sb);
+  return p;
+}
+
+void launch_det_sum(const double* x, size_t n, double* partials, double* out,
+                    cudaStream_t s) {
+  const int nb = red_blocks(n);
+  const size_t chunk = (n + nb - 1) / nb;
+  det_sum_blocks<<<nb, 256, 0, s>>>(x, n, chunk, partials);
+  det_sum_final<<<1, 256, 0, s>>>(partials, nb, out);
+}
+
+void launch_prologue(const DeviceTargets& t, EvalBuffers& b, double eps,
+                     cudaStream_t s) {
+  const int nb = red_blocks(static_cast<size_t>(t.n));
+  const int chunk = (t.n + nb - 1) / nb;
+  prologue_blocks<<<nb, 256, 0, s>>>(t.y, t.nu, b.psi, t.n, 1.0 / eps, b.b2,
+                                     b.part, chunk);
+  prologue_final<<<1, 256, 0, s>>>(b.part, nb, b.scal);
+}
+
+void launch_dense(const DeviceAtoms& a, const DeviceTargets& t, EvalBuffers& b,
+                  const DenseLaunch& p, double eps, cudaStream_t s) {
+  const double c2 = kLog2e / (2.0 * eps);
+  const int n = t.n, nq = a.nq;
+  // The flagged-atom counter lives in scal[kSlotFlagCount] (as u64).
+  cudaMemsetAsync(b.scal + kSlotFlagCount, 0, sizeof(double), s);
+  if (nq > 0) {
+    const int per_split = (((n + p.splitsA - 1) / p.splitsA) + kTile - 1) / kTile * kTile;
+    const int splitsA = (n + per_split - 1) / per_split;
+    dim3 gA((nq + kThreads * p.apt - 1) / (kThreads * p.apt), splitsA);
+    if (b.timing) cudaEventRecord(b.timing[1], s);
+    if (p.apt == 2)
+      dense_passA<2><<<gA, kThreads, 0, s>>>(a.x, nq, t.y, b.b2, n, per_split,
+                                              b.scal, c2, b.partS, b.shiftA);
+    else
+      dense_passA<1><<<gA, kThreads, 0, s>>>(a.x, nq, t.y, b.b2, n, per_split,
+                                              b.scal, c2, b.partS, b.shiftA);
+    if (b.timing) cudaEventRecord(b.timing[2], s);
+    dense_finalizeA<<<(nq + 255) / 256, 256, 0, s>>>(
+        a.x, nq, b.partS, splitsA, b.shiftA, b.scal, eps, b.atomL, b.atomLam,
+        b.atomJ, b.atomD, b.flagged);
+    dense_exact_fallback<<<64, 256, 0, s>>>(a.x, t.y, b.psi, n, b.scal, b.flagged,
+                                            eps, b.atomL, b.atomLam, b.atomJ,
+                                            b.atomD);
+    const int per_splitB = (((nq + p.splitsB - 1) / p.splitsB) + kTile - 1) / kTile * kTile;
+    const int splitsB = (nq + per_splitB - 1) / per_splitB;
+    dim3 gB((n + kThreads * p.tpt - 1) / (kThreads * p.tpt), splitsB);
+    if (b.timing) cudaEventRecord(b.timing[3], s);
+    if (p.tpt == 2)
+      dense_passB<2><<<gB, kThreads, 0, s>>>(a.x, b.atomLam, nq, per_splitB, t.y,
+                                              b.b2, n, c2, b.partG);
+    else
+      dense_passB<1><<<gB, kThreads, 0, s>>>(a.x, b.atomLam, nq, per_splitB, t.y,
+                                              b.b2, n, c2, b.partG);
+    if (b.timing) cudaEventRecord(b.timing[4], s);
+    reduce_partG<<<(n + 255) / 256, 256, 0, s>>>(b.partG, splitsB, n, b.res);
+    launch_det_sum(b.atomJ, nq, b.part, b.res + n + kResJ, s);
+    launch_det_sum(b.atomD, nq, b.part + kRedBlocks, b.res + n + kResD, s);
+  } else {
+    cudaMemsetAsync(b.res, 0, sizeof(double) * (n + kResTail), s);
+  }
+  set_dense_counts<<<1, 1, 0, s>>>(b.res, n, static_cast<double>(nq));
+}
+
+void launch_finalize(const DeviceTargets& t, EvalBuffers& b, cudaStream_t s) {
+  finalize_kernel<<<(t.n + 255) / 256, 256, 0, s>>>(b.res, t.nu, t.n, b.scal,
+                                                    b.g_out, b.scalars_out);
+}
+
+double measure_dfma_rate(cudaStream_t s) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int threads = 256, blocks = sms * 8, iters = 8192;
+  double* out = nullptr;
+  if (cudaMalloc(&out, sizeof(double) * threads * blocks) != cudaSuccess) return 0.0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < 4; ++r) {
+    cudaEventRecord(e0, s);
+    dfma_probe<<<blocks, threads, 0, s>>>(out, 0.999, 1e-3, iters);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r > 0 && ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return static_cast<double>(threads) * blocks * iters * 8 / (best * 1e-3);
+}
+
+}  // namespace rsot_cuda

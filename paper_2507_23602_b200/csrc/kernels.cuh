@@ -1,0 +1,97 @@
+// kernels.cuh -- launch interface of the RSOT evaluator kernels (internal).
+//
+// Layout in HBM (all fp64):
+//   targets : double4 {y0, y1, y2, ln nu}       32 B / target, original order
+//   atoms   : double4 {x0, x1, x2, m}           32 B / atom (this rank's shard)
+//   per eval: b2[N]   = log2(e) (psi/eps + ln nu)
+//             scal[]  = {B = max b2, sum psi*nu, ...}
+//             partS[splitsA][nq], atomL2[nq] (log2 S_q), atomLam[nq]
+//             partG[splitsB][N], res[N + 5] packed for the allreduce
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rsot_cuda {
+
+// Indices into the per-eval device scalar block.
+enum ScalarSlot : int {
+  kSlotB = 0,          // max_j b2_j (global exponent shift)
+  kSlotPsiNu = 1,      // sum_j psi_j nu_j (fixed-order)
+  kSlotNonFinite = 2,  // > 0 when psi had a non-finite entry
+  kSlotFlagCount = 3,  // u64 count of atoms needing the exact fallback
+  kNumSlots = 8
+};
+
+// Packed result tail (after the N gradient entries).
+enum ResultSlot : int {
+  kResJ = 0,
+  kResD = 1,
+  kResPairs = 2,
+  kResEmpty = 3,
+  kResVisited = 4,
+  kResTail = 5
+};
+
+struct DeviceTargets {
+  const double4* y;   // {y0, y1, y2, ln nu}
+  const double* nu;
+  int n;
+};
+
+struct DeviceAtoms {
+  const double4* x;   // {x0, x1, x2, m}
+  int nq;
+};
+
+// Workspace pointers for one evaluation.
+struct EvalBuffers {
+  double* psi;        // [N]
+  double* b2;         // [N]
+  double* scal;       // [kNumSlots]
+  double* part;       // reduction partials scratch [>= 2 * 1024]
+  double* partS;      // [splitsA * nq]
+  double* shiftA;     // [nq]  c2 |x'|^2 about the pass-A origin
+  double* atomL;      // [nq]  ln S_q (natural units, reference log_S)
+  double* atomLam;    // [nq]  log2 m_q - log2 S_q
+  double* atomJ;      // [nq]  eps * ln S_q * m_q
+  double* atomD;      // [nq]  m_q exp(-ln S_q)
+  int* flagged;       // [nq]  indices of atoms needing the exact path
+  double* partG;      // [splitsB * N]
+  double* res;        // [N + kResTail]
+  double* g_out;      // [N]   final gradient (device)
+  double* scalars_out;// [kResTail] final J, D, pairs, empty, visited
+  cudaEvent_t* timing = nullptr;  // optional: [0] start [1..2] pass A
+                                  // [3..4] pass B [5] end
+};
+
+struct DenseLaunch {
+  int apt;            // atoms per thread in pass A (1 or 2)
+  int splitsA;        // target splits in pass A
+  int tpt;            // targets per thread in pass B (1 or 2)
+  int splitsB;        // atom splits in pass B
+};
+
+DenseLaunch plan_dense(int nq, int n, int num_sms);
+
+// Per-eval prologue: b2, B, sum psi nu, psi finiteness.
+void launch_prologue(const DeviceTargets& t, EvalBuffers& b, double eps,
+                     cudaStream_t s);
+
+// Dense evaluation of this rank's atoms; leaves the packed partial result
+// (before the -nu / -sum psi nu finalisation) in b.res.
+void launch_dense(const DeviceAtoms& a, const DeviceTargets& t, EvalBuffers& b,
+                  const DenseLaunch& plan, double eps, cudaStream_t s);
+
+// After the (optional) allreduce of b.res: g = res - nu, J -= sum psi nu.
+void launch_finalize(const DeviceTargets& t, EvalBuffers& b, cudaStream_t s);
+
+// Deterministic fixed-order sum of x[0..n) into out[0] (two launches).
+void launch_det_sum(const double* x, size_t n, double* partials, double* out,
+                    cudaStream_t s);
+
+// FP64 DFMA peak probe (roofline denominator), returns DFMA/s.
+double measure_dfma_rate(cudaStream_t s);
+
+}  // namespace rsot_cuda

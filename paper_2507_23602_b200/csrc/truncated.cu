@@ -1,0 +1,1104 @@
+// truncated.cu -- truncated dual objective + gradient over a GPU cell list.
+//
+// Reference semantics (proj/src/evaluate.cpp:86-174 with a finite cutoff):
+//   candidates(q) = {j : ((dx*dx + dy*dy) + dz*dz) < r*r}, r = sqrt(2 C)
+//                   (spatial_index.cpp:47-61, cost.hpp:38-42),
+//   empty set    -> {nearest target, lowest index on ties} (:129-132),
+//   candidate_pairs counts the fallback as 1, empty_candidate_atoms counts it.
+//
+// Pipeline per evaluation (grid rebuilt only when r leaves its band):
+//   gather b2 into sorted target order
+//   pass A  (CTA = 128 sorted atoms): scan the x-rows of target cells that
+//           can reach the CTA's bounding box, staged through shared memory;
+//           per pair an FP32 pre-test on local coordinates decides clear
+//           in/out, pairs inside the error band get the exact fp64 reference
+//           predicate; accepted pairs accumulate 2^(e2 - B + c2|x'|^2).
+//   nearest (warp per empty atom): exact lexicographic (d^2, j) argmin by
+//           expanding cell rings; J/D from the single-term LSE; the gradient
+//           contribution m_q is added to a 192-bit fixed-point accumulator
+//           per target, so the result is order independent (deterministic).
+//   pass B  (CTA = 128 sorted targets): same scan over atom cells; gather of
+//           2^(e2_qj - log2 S_q + log2 m_q) into the thread's own target.
+//   assemble: res[j] = G[j] + empty[j]; fixed-order sums of J, D, counts.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <vector>
+
+#include "block_util.cuh"
+#include "device_math.cuh"
+#include "truncated.cuh"
+
+namespace rsot_cuda {
+
+namespace {
+
+constexpr int kT = 128;        // threads per CTA = points per chunk
+constexpr int kTileT = 256;    // staged points per tile
+constexpr int kMortonBits = 7; // per dim, position inside a cell
+constexpr double kCellsPerRadius = 2.0;  // grid cell side ~ r / 2
+
+struct GridDev {
+  double lo[3];
+  double h, inv_h;
+  int dims[3];
+};
+
+GridDev to_dev(const GridDesc& g) {
+  GridDev d;
+  for (int i = 0; i < 3; ++i) {
+    d.lo[i] = g.lo[i];
+    d.dims[i] = g.dims[i];
+  }
+  d.h = g.h;
+  d.inv_h = 1.0 / g.h;
+  return d;
+}
+
+__device__ __forceinline__ int cell_of(const GridDev& g, int d, double v) {
+  const double t = floor((v - g.lo[d]) * g.inv_h);
+  if (!(t >= 0.0)) return 0;
+  if (t >= static_cast<double>(g.dims[d] - 1)) return g.dims[d] - 1;
+  return static_cast<int>(t);
+}
+
+// Distance from the interval [a, b] to the slab of cell c in dim d; edge
+// cells extend to infinity (points outside the grid are clamped into them).
+__device__ __forceinline__ double slab_dist(const GridDev& g, int d, int c,
+                                            double a, double b) {
+  const double pad = 1e-7 * g.h;
+  const double s0 = (c == 0) ? -INFINITY : g.lo[d] + c * g.h - pad;
+  const double s1 = (c == g.dims[d] - 1) ? INFINITY : g.lo[d] + (c + 1) * g.h + pad;
+  return fmax(0.0, fmax(s0 - b, a - s1));
+}
+
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {
+  // 7 bits -> every third bit
+  uint32_t r = 0;
+#pragma unroll
+  for (int i = 0; i < kMortonBits; ++i) r |= ((v >> i) & 1u) << (3 * i);
+  return r;
+}
+
+__global__ void cell_keys_kernel(const double4* __restrict__ pts, int n,
+                                 GridDev g, uint64_t* __restrict__ keys,
+                                 int* __restrict__ idx) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 p = pts[i];
+  const double v[3] = {p.x, p.y, p.z};
+  int c[3];
+  uint32_t m[3];
+  for (int d = 0; d < 3; ++d) {
+    c[d] = cell_of(g, d, v[d]);
+    double f = (v[d] - g.lo[d]) * g.inv_h - c[d];
+    f = fmin(fmax(f, 0.0), 0.999999);
+    m[d] = static_cast<uint32_t>(f * (1 << kMortonBits));
+  }
+  const uint64_t cell = (static_cast<uint64_t>(c[2]) * g.dims[1] + c[1]) * g.dims[0] + c[0];
+  const uint32_t mort = spread3(m[0]) | (spread3(m[1]) << 1) | (spread3(m[2]) << 2);
+  keys[i] = (cell << (3 * kMortonBits)) | mort;
+  idx[i] = i;
+}
+
+// Hilbert index (Skilling's transpose algorithm, 3 dims x kHilBits bits) of
+// each point quantised over the set's bounding box.
+constexpr int kHilBits = 16;
+
+__global__ void hilbert_keys_kernel(const double4* __restrict__ pts, int n, double lo0,
+                                    double lo1, double lo2, double s0, double s1, double s2,
+                                    uint64_t* __restrict__ keys, int* __restrict__ idx) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 p = pts[i];
+  const double v[3] = {(p.x - lo0) * s0, (p.y - lo1) * s1, (p.z - lo2) * s2};
+  uint32_t X[3];
+  const double top = static_cast<double>((1u << kHilBits) - 1);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) X[d] = static_cast<uint32_t>(fmin(fmax(v[d], 0.0), top));
+  const uint32_t M = 1u << (kHilBits - 1);
+  for (uint32_t Q = M; Q > 1; Q >>= 1) {
+    const uint32_t P = Q - 1;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      if (X[d] & Q) {
+        X[0] ^= P;
+      } else {
+        const uint32_t t = (X[0] ^ X[d]) & P;
+        X[0] ^= t;
+        X[d] ^= t;
+      }
+    }
+  }
+  X[1] ^= X[0];
+  X[2] ^= X[1];
+  uint32_t t = 0;
+  for (uint32_t Q = M; Q > 1; Q >>= 1)
+    if (X[2] & Q) t ^= Q - 1;
+  X[0] ^= t;
+  X[1] ^= t;
+  X[2] ^= t;
+  uint64_t key = 0;
+  for (int b = kHilBits - 1; b >= 0; --b)
+    key = (key << 3) | (((X[0] >> b) & 1u) << 2) | (((X[1] >> b) & 1u) << 1) | ((X[2] >> b) & 1u);
+  keys[i] = key;
+  idx[i] = i;
+}
+
+__global__ void invert_perm_kernel(const int* __restrict__ perm, int n, int* __restrict__ inv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) inv[perm[i]] = i;
+}
+
+__global__ void compose_kernel(const int* __restrict__ inv_h, const int* __restrict__ perm_c,
+                               int n, int* __restrict__ c2h) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) c2h[i] = inv_h[perm_c[i]];
+}
+
+__global__ void gather_d_kernel(const double* __restrict__ src, const int* __restrict__ idx,
+                                int n, double* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+
+__global__ void gather4_kernel(const double4* __restrict__ src,
+                               const int* __restrict__ perm, int n,
+                               double4* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[perm[i]];
+}
+
+__global__ void cell_start_kernel(const uint64_t* __restrict__ keys, int n,
+                                  long long ncells, int* __restrict__ start) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > n) return;
+  const long long prev = (k == 0) ? -1 : static_cast<long long>(keys[k - 1] >> (3 * kMortonBits));
+  const long long cur = (k == n) ? ncells : static_cast<long long>(keys[k] >> (3 * kMortonBits));
+  for (long long c = prev + 1; c <= cur; ++c) start[c] = k;
+}
+
+
+// Scan-region setup shared by both passes: chunk bbox, origin, FP32 band.
+struct Region {
+  double box[6];
+  double o[3];
+  float lo_thr, hi_thr;
+  int c_lo[3], c_hi[3];
+  bool wide;
+};
+
+__device__ void setup_region(const GridDev& g, const double lo[3], const double hi[3],
+                             double r2, double r_scan, double c2, double* sh, Region& R) {
+  block_bbox<kT>(lo, hi, sh, R.box);
+  double hd2 = 0.0;
+  for (int d = 0; d < 3; ++d) {
+    R.o[d] = 0.5 * (R.box[d] + R.box[d + 3]);
+    const double e = 0.5 * (R.box[d + 3] - R.box[d]);
+    hd2 += e * e;
+  }
+  // Bound on |x'|, |y'| for pairs near the decision boundary, and the FP32
+  // error band (9x the worst-case rounding of the FP32 distance).
+  R.wide = c2 * hd2 > 400.0;
+  const double r = sqrt(r2);
+  const double Rb = sqrt(hd2) + r_scan + 1.75 * g.h;
+  const double band = 0x1p-21 * (8.0 * r * Rb + 4.0 * r2);
+  R.lo_thr = __double2float_rd(r2 - band);
+  R.hi_thr = __double2float_ru(r2 + band);
+  if (!(r2 - band > 1e-30)) R.lo_thr = -1.0f;  // tiny radius: always exact
+  for (int d = 0; d < 3; ++d) {
+    R.c_lo[d] = cell_of(g, d, R.box[d] - r_scan);
+    R.c_hi[d] = cell_of(g, d, R.box[d + 3] + r_scan);
+  }
+}
+
+// Computes one candidate row (index ri over the (cy, cz) rectangle) and
+// returns its [start, start+len) range in the sorted order of `cell_start`.
+__device__ __forceinline__ void row_range(const GridDev& g, const Region& R,
+                                          double r_scan, const int* __restrict__ cell_start,
+                                          int ri, int& start, int& len) {
+  start = 0;
+  len = 0;
+  const int ny = R.c_hi[1] - R.c_lo[1] + 1;
+  const int cy = R.c_lo[1] + ri % ny;
+  const int cz = R.c_lo[2] + ri / ny;
+  const double dy = slab_dist(g, 1, cy, R.box[1], R.box[4]);
+  const double dz = slab_dist(g, 2, cz, R.box[2], R.box[5]);
+  const double rem = r_scan * r_scan - dy * dy - dz * dz;
+  if (rem < 0.0) return;
+  const double rx = sqrt(rem);
+  const int x0 = cell_of(g, 0, R.box[0] - rx);
+  const int x1 = cell_of(g, 0, R.box[3] + rx);
+  const long long row = (static_cast<long long>(cz) * g.dims[1] + cy) * g.dims[0];
+  start = cell_start[row + x0];
+  len = cell_start[row + x1 + 1] - start;
+}
+
+__device__ __forceinline__ int find_row(const int* pref, int s) {
+  // largest r in [0, kT) with pref[r] <= s
+  int lo = 0, hi = kT;  // pref[kT] = total > s
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (pref[mid] <= s) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------------------
+// Pass A: atom-major truncated LSE.
+
+template <bool DEBUG>
+__global__ void __launch_bounds__(kT)
+trunc_passA(const double4* __restrict__ xs, int nq,
+            const double4* __restrict__ ys, const double* __restrict__ b2s,
+            const int* __restrict__ tperm, const int* __restrict__ cell_start,
+            GridDev g, const double* __restrict__ scal, double c2, double r2,
+            double r_scan, double* __restrict__ S_out,
+            double* __restrict__ shift_out, uint32_t* __restrict__ cnt_out,
+            uint64_t* __restrict__ hash_out) {
+  __shared__ double4 tD[kTileT];
+  __shared__ float4 tF[kTileT];
+  __shared__ int tK[kTileT];
+  __shared__ int rowStart[kT];
+  __shared__ int rowPref[kT + 1];
+  __shared__ double tbl[16];
+  __shared__ double sh[200];
+  __shared__ int shi[40];
+  load_exp2_table(tbl);
+
+  const int q = blockIdx.x * kT + threadIdx.x;
+  const bool valid = q < nq;
+  double4 xa = valid ? xs[q] : make_double4(0, 0, 0, 0);
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  if (valid) {
+    lo[0] = hi[0] = xa.x;
+    lo[1] = hi[1] = xa.y;
+    lo[2] = hi[2] = xa.z;
+  }
+  Region R;
+  setup_region(g, lo, hi, r2, r_scan, c2, sh, R);
+  const double x0 = xa.x - R.o[0], x1 = xa.y - R.o[1], x2 = xa.z - R.o[2];
+  const float xf0 = valid ? static_cast<float>(x0) : 1e30f;
+  const float xf1 = valid ? static_cast<float>(x1) : 1e30f;
+  const float xf2 = valid ? static_cast<float>(x2) : 1e30f;
+  const double X0 = 2.0 * c2 * x0, X1 = 2.0 * c2 * x1, X2 = 2.0 * c2 * x2;
+  const double xsq = c2 * fma(x2, x2, fma(x1, x1, x0 * x0));
+  // Spread chunk: carry the per-atom shift in every exponent (see dense.cu).
+  const bool wide = R.wide;
+  const double B = scal[kSlotB];
+  double S = 0.0;
+  uint32_t cnt = 0;
+  uint64_t hash = 0;
+
+  const int ny = R.c_hi[1] - R.c_lo[1] + 1;
+  const int nrows = ny * (R.c_hi[2] - R.c_lo[2] + 1);
+  for (int rb = 0; rb < nrows; rb += kT) {
+    int st = 0, ln = 0;
+    if (rb + threadIdx.x < nrows) row_range(g, R, r_scan, cell_start, rb + threadIdx.x, st, ln);
+    int total = 0;
+    const int pre = block_exclusive_scan<kT>(ln, shi, &total);
+    rowStart[threadIdx.x] = st;
+    rowPref[threadIdx.x] = pre;
+    if (threadIdx.x == 0) rowPref[kT] = total;
+    for (int base = 0; base < total; base += kTileT) {
+      const int cntT = min(kTileT, total - base);
+      __syncthreads();
+      for (int t = threadIdx.x; t < cntT; t += kT) {
+        const int s = base + t;
+        const int r = find_row(rowPref, s);
+        const int k = rowStart[r] + (s - rowPref[r]);
+        const double4 y = ys[k];
+        const double y0 = y.x - R.o[0], y1 = y.y - R.o[1], y2 = y.z - R.o[2];
+        const double yy = fma(y2, y2, fma(y1, y1, y0 * y0));
+        const double w = fmax(fma(-c2, yy, b2s[k]) - B, -1.0e5);
+        tD[t] = make_double4(y0, y1, y2, w);
+        tF[t] = make_float4(static_cast<float>(y0), static_cast<float>(y1),
+                            static_cast<float>(y2), 0.f);
+        tK[t] = k;
+      }
+      __syncthreads();
+      for (int t = 0; t < cntT; ++t) {
+        const float4 yf = tF[t];
+        const float dx = xf0 - yf.x, dy = xf1 - yf.y, dz = xf2 - yf.z;
+        const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        bool in = d2 < R.lo_thr;
+        if (!in && d2 <= R.hi_thr) {
+          const double4 yg = ys[tK[t]];
+          in = exact_inside(xa.x, xa.y, xa.z, yg.x, yg.y, yg.z, r2);
+        }
+        if (in) {
+          const double4 y = tD[t];
+          double s = fma(X0, y.x, fma(X1, y.y, fma(X2, y.z, y.w)));
+          if (wide) s -= xsq;
+          S = exp2_acc(s, S, tbl);
+          ++cnt;
+          if (DEBUG) hash += candidate_hash_term(static_cast<uint64_t>(tperm[tK[t]]));
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (valid) {
+    S_out[q] = S;
+    shift_out[q] = wide ? 0.0 : xsq;
+    cnt_out[q] = cnt;
+    if (DEBUG) hash_out[q] = hash;
+  }
+}
+
+// Per-atom finalisation for atoms with a non-empty candidate set.
+__global__ void trunc_finalizeA(const double4* __restrict__ xs, int nq,
+                                const double* __restrict__ S_in,
+                                const double* __restrict__ shiftA,
+                                const uint32_t* __restrict__ cnt,
+                                double* __restrict__ scal, double eps,
+                                double* __restrict__ atomL,
+                                double* __restrict__ atomLam,
+                                double* __restrict__ atomJ,
+                                double* __restrict__ atomD,
+                                double* __restrict__ cntd,
+                                double* __restrict__ emptyd,
+                                int* __restrict__ flagged) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const uint32_t c = cnt[q];
+  cntd[q] = c == 0 ? 1.0 : static_cast<double>(c);
+  emptyd[q] = c == 0 ? 1.0 : 0.0;
+  if (c == 0) {  // handled by the nearest kernel; never inside in pass B
+    atomLam[q] = -1.0e5;
+    return;
+  }
+  double S = S_in[q];
+  const double m = xs[q].w;
+  if (!(S >= 0x1p-960) || !(S <= 0x1p960)) {
+    unsigned long long* n = reinterpret_cast<unsigned long long*>(&scal[kSlotFlagCount]);
+    flagged[atomicAdd(n, 1ull)] = q;
+    S = 1.0;
+  }
+  const double L2 = (scal[kSlotB] - shiftA[q]) + log2(S);
+  const double L = L2 * kLn2;
+  atomL[q] = L;
+  atomJ[q] = eps * L * m;
+  atomD[q] = m * exp(-L);
+  atomLam[q] = fmax(log2(m) - L2, -1.0e5);
+}
+
+// Exact per-atom LSE (reference per-atom max shift) for flagged atoms.
+__global__ void trunc_exact_fallback(const double4* __restrict__ xs,
+                                     const double4* __restrict__ ys,
+                                     const int* __restrict__ tperm,
+                                     const int* __restrict__ cell_start, GridDev g,
+                                     const double* __restrict__ psi, double eps,
+                                     double r2, double r_scan,
+                                     const double* __restrict__ scal,
+                                     const int* __restrict__ flagged,
+                                     double* __restrict__ atomL,
+                                     double* __restrict__ atomLam,
+                                     double* __restrict__ atomJ,
+                                     double* __restrict__ atomD) {
+  __shared__ double sh[256];
+  const unsigned long long nflag =
+      *reinterpret_cast<const unsigned long long*>(&scal[kSlotFlagCount]);
+  for (unsigned long long f = blockIdx.x; f < nflag; f += gridDim.x) {
+    const int q = flagged[f];
+    const double4 a = xs[q];
+    int c_lo[3], c_hi[3];
+    const double v[3] = {a.x, a.y, a.z};
+    for (int d = 0; d < 3; ++d) {
+      c_lo[d] = cell_of(g, d, v[d] - r_scan);
+      c_hi[d] = cell_of(g, d, v[d] + r_scan);
+    }
+    double mx = -INFINITY, sum = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+      double acc = pass == 0 ? -INFINITY : 0.0;
+      for (int cz = c_lo[2]; cz <= c_hi[2]; ++cz)
+        for (int cy = c_lo[1]; cy <= c_hi[1]; ++cy) {
+          const long long row = (static_cast<long long>(cz) * g.dims[1] + cy) * g.dims[0];
+          const int b = cell_start[row + c_lo[0]], e = cell_start[row + c_hi[0] + 1];
+          for (int k = b + threadIdx.x; k < e; k += blockDim.x) {
+            const double4 y = ys[k];
+            const double d2 = exact_sqdist(a.x, a.y, a.z, y.x, y.y, y.z);
+            if (!(d2 < r2)) continue;
+            const int j = tperm[k];
+            const double ex = reference_exponent(psi[j], d2, eps, y.w);
+            if (pass == 0) acc = fmax(acc, ex); else acc += exp(ex - mx);
+          }
+        }
+      if (pass == 0) mx = block_max<256>(acc, sh);
+      else sum = block_sum<256>(acc, sh);
+    }
+    if (threadIdx.x == 0) {
+      const double L = mx + log(sum);
+      atomL[q] = L;
+      atomJ[q] = eps * L * a.w;
+      atomD[q] = a.w * exp(-L);
+      atomLam[q] = fmax(log2(a.w) - L * kLog2e, -1.0e5);
+    }
+    __syncthreads();
+  }
+}
+
+// 192-bit fixed point (scale 2^150) accumulation of a non-negative double.
+__device__ void fp_add(unsigned long long* acc, double m) {
+  if (!(m > 0.0)) return;
+  int e;
+  const double fr = frexp(m, &e);                   // m = fr * 2^e, fr in [0.5,1)
+  const unsigned long long mant = static_cast<unsigned long long>(ldexp(fr, 53));
+  const int sh = e - 53 + 150;                       // value = mant * 2^sh
+  unsigned long long limb[3] = {0, 0, 0};
+  if (sh < 0) {
+    if (sh > -64) limb[0] = mant >> (-sh);
+  } else {
+    const int w = sh >> 6, b = sh & 63;
+    if (w < 3) limb[w] = mant << b;
+    if (b && w + 1 < 3) limb[w + 1] = mant >> (64 - b);
+  }
+  unsigned long long carry = 0;
+  for (int i = 0; i < 3; ++i) {
+    const unsigned long long add = limb[i] + carry;
+    const unsigned long long c1 = (add < limb[i]) ? 1ull : 0ull;
+    if (add == 0 && c1 == 0) { carry = 0; continue; }
+    const unsigned long long old = atomicAdd(&acc[i], add);
+    carry = c1 + ((old + add < old) ? 1ull : 0ull);
+  }
+}
+
+__device__ double fp_to_double(const unsigned long long* acc) {
+  return (static_cast<double>(acc[2]) * 0x1p-22 + static_cast<double>(acc[1]) * 0x1p-86) +
+         static_cast<double>(acc[0]) * 0x1p-150;
+}
+
+// Warp-cooperative exact nearest target (lexicographic (d^2, j) argmin).
+__device__ void warp_nearest(const GridDev& g, const double4* __restrict__ ys,
+                             const int* __restrict__ tperm,
+                             const int* __restrict__ cell_start, double x0,
+                             double x1, double x2, double& best_d2, int& best_j,
+                             int& best_k) {
+  const int lane = threadIdx.x & 31;
+  const double v[3] = {x0, x1, x2};
+  int cc[3];
+  for (int d = 0; d < 3; ++d) cc[d] = cell_of(g, d, v[d]);
+  double bd = INFINITY;
+  int bj = 0x7fffffff, bk = -1;
+  const int maxk = g.dims[0] + g.dims[1] + g.dims[2];
+  for (int k = 0; k <= maxk; ++k) {
+    const int zlo = max(0, cc[2] - k), zhi = min(g.dims[2] - 1, cc[2] + k);
+    const int ylo = max(0, cc[1] - k), yhi = min(g.dims[1] - 1, cc[1] + k);
+    const int xlo = max(0, cc[0] - k), xhi = min(g.dims[0] - 1, cc[0] + k);
+    for (int cz = zlo; cz <= zhi; ++cz)
+      for (int cy = ylo; cy <= yhi; ++cy) {
+        const bool full = (abs(cz - cc[2]) == k) || (abs(cy - cc[1]) == k);
+        const long long row = (static_cast<long long>(cz) * g.dims[1] + cy) * g.dims[0];
+        for (int part = 0; part < (full ? 1 : 2); ++part) {
+          int a0, a1;
+          if (full) { a0 = xlo; a1 = xhi; }
+          else if (part == 0) { a0 = cc[0] - k; a1 = a0; if (a0 < 0) continue; }
+          else { a0 = cc[0] + k; a1 = a0; if (a0 > g.dims[0] - 1 || k == 0) continue; }
+          const int b = cell_start[row + a0], e = cell_start[row + a1 + 1];
+          for (int t = b + lane; t < e; t += 32) {
+            const double4 y = ys[t];
+            const double d2 = exact_sqdist(x0, x1, x2, y.x, y.y, y.z);
+            const int j = tperm[t];
+            if (d2 < bd || (d2 == bd && j < bj)) { bd = d2; bj = j; bk = t; }
+          }
+        }
+      }
+    // warp lexicographic min
+    for (int o = 16; o > 0; o >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      if (od < bd || (od == bd && oj < bj)) { bd = od; bj = oj; bk = ok; }
+    }
+    double margin = INFINITY;
+    bool left = false;
+    for (int d = 0; d < 3; ++d) {
+      if (cc[d] - k > 0) {
+        margin = fmin(margin, v[d] - (g.lo[d] + (cc[d] - k) * g.h));
+        left = true;
+      }
+      if (cc[d] + k < g.dims[d] - 1) {
+        margin = fmin(margin, (g.lo[d] + (cc[d] + k + 1) * g.h) - v[d]);
+        left = true;
+      }
+    }
+    if (!left) break;
+    margin = margin * (1.0 - 1e-9) - 1e-7 * g.h;
+    if (bk >= 0 && margin > 0.0 && margin * margin > bd * (1.0 + 1e-9)) break;
+  }
+  best_d2 = bd;
+  best_j = bj;
+  best_k = bk;
+}
+
+template <bool DEBUG>
+__global__ void trunc_nearest_empty(const double4* __restrict__ xs, int nq,
+                                    const uint32_t* __restrict__ cnt,
+                                    const double4* __restrict__ ys,
+                                    const int* __restrict__ tperm,
+                                    const int* __restrict__ cell_start, GridDev g,
+                                    const double* __restrict__ psi, double eps,
+                                    double* __restrict__ atomL,
+                                    double* __restrict__ atomJ,
+                                    double* __restrict__ atomD,
+                                    unsigned long long* __restrict__ empty_fp,
+                                    uint64_t* __restrict__ hash_out) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int base = warp * 32; base < nq; base += nwarps * 32) {
+    const int q = base + lane;
+    const bool empty = q < nq && cnt[q] == 0;
+    unsigned mask = __ballot_sync(0xffffffffu, empty);
+    while (mask) {
+      const int l = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const int qq = base + l;
+      const double4 a = xs[qq];
+      double bd;
+      int bj, bk;
+      warp_nearest(g, ys, tperm, cell_start, a.x, a.y, a.z, bd, bj, bk);
+      if (lane == 0) {
+        const double L = reference_exponent(psi[bj], bd, eps, ys[bk].w);
+        atomL[qq] = L;
+        atomJ[qq] = eps * L * a.w;
+        atomD[qq] = a.w * exp(-L);
+        fp_add(empty_fp + 3 * static_cast<size_t>(bj), a.w);
+        if (DEBUG) hash_out[qq] = candidate_hash_term(static_cast<uint64_t>(bj));
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pass B: target-major truncated gather.
+
+__global__ void __launch_bounds__(kT)
+trunc_passB(const double4* __restrict__ ys, const double* __restrict__ b2s, int n,
+            const double4* __restrict__ xs, const double* __restrict__ atomLam,
+            const int* __restrict__ acell_start, GridDev g, double c2, double r2,
+            double r_scan, double* __restrict__ G_out) {
+  __shared__ double4 tD[kTileT];
+  __shared__ float4 tF[kTileT];
+  __shared__ int tK[kTileT];
+  __shared__ int rowStart[kT];
+  __shared__ int rowPref[kT + 1];
+  __shared__ double tbl[16];
+  __shared__ double sh[200];
+  __shared__ int shi[40];
+  load_exp2_table(tbl);
+
+  const int j = blockIdx.x * kT + threadIdx.x;
+  const bool valid = j < n;
+  const double4 yg = valid ? ys[j] : make_double4(0, 0, 0, 0);
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  if (valid) {
+    lo[0] = hi[0] = yg.x;
+    lo[1] = hi[1] = yg.y;
+    lo[2] = hi[2] = yg.z;
+  }
+  Region R;
+  setup_region(g, lo, hi, r2, r_scan, c2, sh, R);
+  const double y0 = yg.x - R.o[0], y1 = yg.y - R.o[1], y2 = yg.z - R.o[2];
+  const float yf0 = valid ? static_cast<float>(y0) : 1e30f;
+  const float yf1 = valid ? static_cast<float>(y1) : 1e30f;
+  const float yf2 = valid ? static_cast<float>(y2) : 1e30f;
+  const double T = valid ? fmax(fma(-c2, fma(y2, y2, fma(y1, y1, y0 * y0)), b2s[j]), -1.0e5) : -1.0e5;
+  double G = 0.0;
+
+  const int ny = R.c_hi[1] - R.c_lo[1] + 1;
+  const int nrows = ny * (R.c_hi[2] - R.c_lo[2] + 1);
+  const double c2x2 = 2.0 * c2;
+  for (int rb = 0; rb < nrows; rb += kT) {
+    int st = 0, ln = 0;
+    if (rb + threadIdx.x < nrows) row_range(g, R, r_scan, acell_start, rb + threadIdx.x, st, ln);
+    int total = 0;
+    const int pre = block_exclusive_scan<kT>(ln, shi, &total);
+    rowStart[threadIdx.x] = st;
+    rowPref[threadIdx.x] = pre;
+    if (threadIdx.x == 0) rowPref[kT] = total;
+    for (int base = 0; base < total; base += kTileT) {
+      const int cntT = min(kTileT, total - base);
+      __syncthreads();
+      for (int t = threadIdx.x; t < cntT; t += kT) {
+        const int s = base + t;
+        const int r = find_row(rowPref, s);
+        const int k = rowStart[r] + (s - rowPref[r]);
+        const double4 a = xs[k];
+        const double x0 = a.x - R.o[0], x1 = a.y - R.o[1], x2 = a.z - R.o[2];
+        const double xx = fma(x2, x2, fma(x1, x1, x0 * x0));
+        const double A = fma(-c2, xx, atomLam[k]);
+        tD[t] = make_double4(c2x2 * x0, c2x2 * x1, c2x2 * x2, A);
+        tF[t] = make_float4(static_cast<float>(x0), static_cast<float>(x1),
+                            static_cast<float>(x2), 0.f);
+        tK[t] = k;
+      }
+      __syncthreads();
+      for (int t = 0; t < cntT; ++t) {
+        const float4 xf = tF[t];
+        const float dx = xf.x - yf0, dy = xf.y - yf1, dz = xf.z - yf2;
+        const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        bool in = d2 < R.lo_thr;
+        if (!in && d2 <= R.hi_thr) {
+          const double4 xg = xs[tK[t]];
+          in = exact_inside(xg.x, xg.y, xg.z, yg.x, yg.y, yg.z, r2);
+        }
+        if (in) {
+          const double4 X = tD[t];
+          const double s = fma(X.x, y0, fma(X.y, y1, fma(X.z, y2, T + X.w)));
+          G = exp2_acc(s, G, tbl);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (valid) G_out[j] = G;
+}
+
+__global__ void trunc_assemble(const double* __restrict__ G, const int* __restrict__ tperm,
+                               int n, const unsigned long long* __restrict__ empty_fp,
+                               double* __restrict__ res) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int j = tperm[k];
+  res[j] = G[k] + fp_to_double(empty_fp + 3 * static_cast<size_t>(j));
+}
+
+__global__ void set_visited(double* __restrict__ res, int n, double nq) {
+  res[n + kResVisited] = nq;
+}
+
+template <typename T>
+__global__ void scatter_debug(const T* __restrict__ src, const int* __restrict__ perm,
+                              int nq, T* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nq) dst[perm[i]] = src[i];
+}
+
+__global__ void cnt_fix_kernel(const uint32_t* __restrict__ cnt, int nq,
+                               uint32_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nq) out[i] = cnt[i] == 0 ? 1u : cnt[i];
+}
+
+__global__ void dense_debug_kernel(const double* __restrict__ atomL, int nq, int n,
+                                   uint32_t* __restrict__ count,
+                                   uint64_t* __restrict__ hash,
+                                   double* __restrict__ log_s) {
+  __shared__ unsigned long long hsum;
+  if (threadIdx.x == 0) hsum = 0;
+  __syncthreads();
+  unsigned long long h = 0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) h += candidate_hash_term(j);
+  atomicAdd(&hsum, h);
+  __syncthreads();
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+    count[q] = static_cast<uint32_t>(n);
+    hash[q] = hsum;
+    log_s[q] = atomL[q];
+  }
+}
+
+__global__ void nearest_points_kernel(const double* __restrict__ pts, int m,
+                                      const double4* __restrict__ ys,
+                                      const int* __restrict__ tperm,
+                                      const int* __restrict__ cell_start, GridDev g,
+                                      unsigned long long* __restrict__ out,
+                                      double* __restrict__ d2_out) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = warp; i < m; i += nwarps) {
+    double bd;
+    int bj, bk;
+    warp_nearest(g, ys, tperm, cell_start, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], bd, bj, bk);
+    if (lane == 0) {
+      out[i] = static_cast<unsigned long long>(bj);
+      if (d2_out) d2_out[i] = bd;
+    }
+  }
+}
+
+__global__ void atoms_to_pts(const double4* __restrict__ x, int nq, double* __restrict__ pts) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nq) {
+    pts[3 * i] = x[i].x;
+    pts[3 * i + 1] = x[i].y;
+    pts[3 * i + 2] = x[i].z;
+  }
+}
+
+__global__ void max_cost_kernel(const double* __restrict__ d2, int m, double* __restrict__ out) {
+  __shared__ double sh[256];
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) mx = fmax(mx, 0.5 * d2[i]);
+  mx = block_max<256>(mx, sh);
+  if (threadIdx.x == 0) *out = mx;
+}
+
+
+template <typename T>
+cudaError_t grow(T*& p, size_t& cap, size_t n) {
+  if (n <= cap && p) return cudaSuccess;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  cudaError_t e = cudaMalloc(&p, sizeof(T) * (n ? n : 1));
+  if (e == cudaSuccess) cap = n;
+  return e;
+}
+
+template <typename T>
+cudaError_t realloc_exact(T*& p, size_t n) {
+  if (p) cudaFree(p);
+  p = nullptr;
+  return cudaMalloc(&p, sizeof(T) * (n ? n : 1));
+}
+
+uint64_t g_next_grid_id = 1;
+
+#define TCK(call)                                                       \
+  do {                                                                  \
+    cudaError_t e_ = (call);                                            \
+    if (e_ != cudaSuccess) {                                            \
+      err = std::string(#call) + ": " + cudaGetErrorString(e_);         \
+      return 1;                                                         \
+    }                                                                   \
+  } while (0)
+
+int ensure_key_buffers(TruncWorkspace& ws, int n, std::string& err) {
+  if (static_cast<size_t>(n) <= ws.keys_cap && ws.keys) return 0;
+  const size_t c = std::max(n, 1);
+  TCK(realloc_exact(ws.keys, c));
+  TCK(realloc_exact(ws.keys2, c));
+  TCK(realloc_exact(ws.idx, c));
+  TCK(realloc_exact(ws.idx2, c));
+  ws.keys_cap = ws.idx_cap = c;
+  return 0;
+}
+
+// Stable radix sort of ws.keys/ws.idx (n entries, end_bit key bits); the
+// sorted permutation lands in ws.idx2 and the sorted keys in ws.keys2.
+int radix_sort(TruncWorkspace& ws, int n, int end_bit, cudaStream_t s, std::string& err) {
+  size_t bytes = 0;
+  TCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, ws.keys, ws.keys2, ws.idx, ws.idx2, n, 0,
+                                      end_bit, s));
+  if (bytes > ws.cub_bytes) {
+    if (ws.cub_tmp) cudaFree(ws.cub_tmp);
+    ws.cub_tmp = nullptr;
+    TCK(cudaMalloc(&ws.cub_tmp, bytes));
+    ws.cub_bytes = bytes;
+  }
+  TCK(cub::DeviceRadixSort::SortPairs(ws.cub_tmp, bytes, ws.keys, ws.keys2, ws.idx, ws.idx2, n,
+                                      0, end_bit, s));
+  return 0;
+}
+
+// Hilbert order of a point set (radius independent; built once).
+int build_hilbert(TruncWorkspace& ws, const double4* pts, int n, PointOrders& po,
+                  cudaStream_t s, std::string& err) {
+  if (po.hil_valid && po.n == n) return 0;
+  if (ensure_key_buffers(ws, n, err)) return 1;
+  TCK(realloc_exact(po.ph, n));
+  TCK(realloc_exact(po.perm_h, n));
+  TCK(realloc_exact(po.inv_h, n));
+  if (n > 0) {
+    double sc[3];
+    for (int d = 0; d < 3; ++d) {
+      const double ext = po.bbox_hi[d] - po.bbox_lo[d];
+      sc[d] = ext > 0.0 ? static_cast<double>(1u << kHilBits) / ext : 0.0;
+    }
+    hilbert_keys_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, n, po.bbox_lo[0], po.bbox_lo[1],
+                                                        po.bbox_lo[2], sc[0], sc[1], sc[2],
+                                                        ws.keys, ws.idx);
+    if (radix_sort(ws, n, 3 * kHilBits, s, err)) return 1;
+    gather4_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, ws.idx2, n, po.ph);
+    TCK(cudaMemcpyAsync(po.perm_h, ws.idx2, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+    invert_perm_kernel<<<(n + 255) / 256, 256, 0, s>>>(po.perm_h, n, po.inv_h);
+  }
+  TCK(cudaGetLastError());
+  po.n = n;
+  po.hil_valid = true;
+  po.cell_valid = false;
+  return 0;
+}
+
+// Cell order for grid g (requires the Hilbert order for c2h).
+int build_cells(TruncWorkspace& ws, const double4* pts, int n, const GridDesc& g,
+                PointOrders& po, cudaStream_t s, std::string& err) {
+  if (po.cell_valid && po.grid_id == g.id && po.n == n) return 0;
+  if (ensure_key_buffers(ws, n, err)) return 1;
+  TCK(realloc_exact(po.pc, n));
+  TCK(realloc_exact(po.perm_c, n));
+  TCK(realloc_exact(po.c2h, n));
+  TCK(realloc_exact(po.cell_start, g.ncells + 1));
+  const GridDev gd = to_dev(g);
+  if (n > 0) {
+    cell_keys_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, n, gd, ws.keys, ws.idx);
+    int end_bit = 3 * kMortonBits;
+    while ((1ll << (end_bit - 3 * kMortonBits)) < g.ncells) ++end_bit;
+    if (radix_sort(ws, n, end_bit, s, err)) return 1;
+    gather4_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, ws.idx2, n, po.pc);
+    TCK(cudaMemcpyAsync(po.perm_c, ws.idx2, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+    compose_kernel<<<(n + 255) / 256, 256, 0, s>>>(po.inv_h, po.perm_c, n, po.c2h);
+  }
+  cell_start_kernel<<<(n + 1 + 255) / 256, 256, 0, s>>>(ws.keys2, n, g.ncells, po.cell_start);
+  TCK(cudaGetLastError());
+  po.grid_id = g.id;
+  po.cell_valid = true;
+  return 0;
+}
+
+// Grid over the target bounding box with cell side ~max(r/2, spacing).
+GridDesc plan_grid(const double blo[3], const double bhi[3], int n, double r) {
+  GridDesc g;
+  int active = 0;
+  double vol = 1.0;
+  for (int d = 0; d < 3; ++d)
+    if (bhi[d] > blo[d]) {
+      ++active;
+      vol *= bhi[d] - blo[d];
+    }
+  double hmin = 1.0;
+  if (active > 0) hmin = std::pow(vol / std::max(1.0, n / 2.0), 1.0 / active);
+  double h = std::max(r / kCellsPerRadius, hmin);
+  if (!(h > 0.0) || !std::isfinite(h)) h = 1.0;
+  for (;;) {
+    long long nc = 1;
+    for (int d = 0; d < 3; ++d) {
+      const double ext = bhi[d] - blo[d];
+      g.dims[d] = ext > 0.0 ? static_cast<int>(std::min(std::floor(ext / h) + 1.0, 8192.0)) : 1;
+      nc *= g.dims[d];
+    }
+    if (nc <= (1ll << 26)) {
+      g.ncells = nc;
+      break;
+    }
+    h *= 1.25;
+  }
+  for (int d = 0; d < 3; ++d) g.lo[d] = blo[d];
+  g.h = h;
+  return g;
+}
+
+}  // namespace
+
+void PointOrders::release() {
+  void* ptrs[] = {ph, perm_h, inv_h, pc, perm_c, c2h, cell_start};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  ph = pc = nullptr;
+  perm_h = inv_h = perm_c = c2h = cell_start = nullptr;
+  hil_valid = cell_valid = false;
+}
+
+void TruncWorkspace::release() {
+  void* ptrs[] = {cub_tmp, keys, keys2, idx, idx2, b2s, b2h, lamc, S, shiftA, atomL, atomLam,
+                  atomJ, atomD, cntd, emptyd, cnt, hash, flagged, empty_fp, G, pts, near_out, red};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  *this = TruncWorkspace();
+}
+
+static int ensure_target_cells(TruncWorkspace& ws, const DeviceTargets& t, TargetCells& tc,
+                               double r, cudaStream_t s, std::string& err) {
+  if (!tc.bbox_set) {
+    err = "target bounding box not set";
+    return 1;
+  }
+  if (build_hilbert(ws, t.y, t.n, tc, s, err)) return 1;
+  const double want = std::max(r / kCellsPerRadius, tc.hmin);
+  if (tc.cell_valid && tc.g.h >= 0.75 * want && tc.g.h <= 1.35 * want) return 0;
+  GridDesc g = plan_grid(tc.bbox_lo, tc.bbox_hi, t.n, r);
+  g.id = g_next_grid_id++;
+  tc.hmin = plan_grid(tc.bbox_lo, tc.bbox_hi, t.n, 0.0).h;
+  tc.cell_valid = false;
+  if (build_cells(ws, t.y, t.n, g, tc, s, err)) return 1;
+  tc.g = g;
+  tc.built_r = r;
+  return 0;
+}
+
+static int ensure_atom_cells(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
+                             const TargetCells& tc, cudaStream_t s, std::string& err) {
+  if (!ac.bbox_set) {
+    err = "atom bounding box not set";
+    return 1;
+  }
+  if (build_hilbert(ws, a.x, a.nq, ac, s, err)) return 1;
+  return build_cells(ws, a.x, a.nq, tc.g, ac, s, err);
+}
+
+static int ensure_trunc_ws(TruncWorkspace& ws, int nq, int n, std::string& err) {
+  if (static_cast<size_t>(nq) > ws.atom_cap || !ws.S) {
+    const size_t c = std::max<size_t>(nq, 1);
+    TCK(realloc_exact(ws.S, c));
+    TCK(realloc_exact(ws.shiftA, c));
+    TCK(realloc_exact(ws.atomL, c));
+    TCK(realloc_exact(ws.atomLam, c));
+    TCK(realloc_exact(ws.lamc, c));
+    TCK(realloc_exact(ws.atomJ, c));
+    TCK(realloc_exact(ws.atomD, c));
+    TCK(realloc_exact(ws.cntd, c));
+    TCK(realloc_exact(ws.emptyd, c));
+    TCK(realloc_exact(ws.cnt, c));
+    TCK(realloc_exact(ws.hash, c));
+    TCK(realloc_exact(ws.flagged, c));
+    ws.atom_cap = c;
+  }
+  if (static_cast<size_t>(n) > ws.tgt_cap || !ws.G) {
+    const size_t c = std::max<size_t>(n, 1);
+    TCK(realloc_exact(ws.G, c));
+    TCK(realloc_exact(ws.b2s, c));
+    TCK(realloc_exact(ws.b2h, c));
+    TCK(realloc_exact(ws.empty_fp, 3 * c));
+    ws.tgt_cap = c;
+  }
+  if (!ws.red) TCK(cudaMalloc(&ws.red, sizeof(double) * 4096));
+  return 0;
+}
+
+int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
+                  const DeviceTargets& t, TargetCells& tc, EvalBuffers& b,
+                  double eps, double cutoff, int num_sms, DebugOut* dbg,
+                  cudaStream_t s, std::string& err) {
+  (void)num_sms;
+  // cost.hpp:38-42 and spatial_index.cpp:50,54, evaluated on the host exactly
+  // as the reference does.
+  const double radius = cutoff < 0.0 ? 0.0 : std::sqrt(2.0 * cutoff);
+  const double r2 = radius * radius;
+  const bool scan = radius > 0.0;
+  const double r_use = scan ? radius : 0.0;
+  const double r_scan = r_use * (1.0 + 1e-9) + 1e-300;
+  const int n = t.n, nq = a.nq;
+  if (ensure_target_cells(ws, t, tc, r_use, s, err)) return 1;
+  if (ensure_atom_cells(ws, a, ac, tc, s, err)) return 1;
+  if (ensure_trunc_ws(ws, nq, n, err)) return 1;
+  const GridDev g = to_dev(tc.g);
+  const double c2 = kLog2e / (2.0 * eps);
+
+  TCK(cudaMemsetAsync(b.scal + kSlotFlagCount, 0, sizeof(double), s));
+  TCK(cudaMemsetAsync(ws.empty_fp, 0, sizeof(unsigned long long) * 3 * static_cast<size_t>(n), s));
+  gather_d_kernel<<<(n + 255) / 256, 256, 0, s>>>(b.b2, tc.perm_c, n, ws.b2s);
+  gather_d_kernel<<<(n + 255) / 256, 256, 0, s>>>(b.b2, tc.perm_h, n, ws.b2h);
+  if (nq > 0) {
+    const int nblk = (nq + kT - 1) / kT;
+    if (b.timing) cudaEventRecord(b.timing[1], s);
+    if (scan) {
+      if (dbg)
+        trunc_passA<true><<<nblk, kT, 0, s>>>(ac.ph, nq, tc.pc, ws.b2s, tc.perm_c, tc.cell_start,
+                                              g, b.scal, c2, r2, r_scan, ws.S, ws.shiftA,
+                                              ws.cnt, ws.hash);
+      else
+        trunc_passA<false><<<nblk, kT, 0, s>>>(ac.ph, nq, tc.pc, ws.b2s, tc.perm_c, tc.cell_start,
+                                               g, b.scal, c2, r2, r_scan, ws.S, ws.shiftA,
+                                               ws.cnt, ws.hash);
+    } else {
+      // radius <= 0: every candidate set is empty (spatial_index.cpp:50).
+      TCK(cudaMemsetAsync(ws.cnt, 0, sizeof(uint32_t) * nq, s));
+    }
+    if (b.timing) cudaEventRecord(b.timing[2], s);
+    trunc_finalizeA<<<(nq + 255) / 256, 256, 0, s>>>(ac.ph, nq, ws.S, ws.shiftA, ws.cnt, b.scal,
+                                                     eps, ws.atomL, ws.atomLam, ws.atomJ,
+                                                     ws.atomD, ws.cntd, ws.emptyd, ws.flagged);
+    trunc_exact_fallback<<<64, 256, 0, s>>>(ac.ph, tc.pc, tc.perm_c, tc.cell_start, g, b.psi, eps,
+                                            r2, r_scan, b.scal, ws.flagged, ws.atomL,
+                                            ws.atomLam, ws.atomJ, ws.atomD);
+    const int nb_near = std::min(4 * 148, (nq + 255) / 256 * 8 + 1);
+    if (dbg)
+      trunc_nearest_empty<true><<<nb_near, 256, 0, s>>>(ac.ph, nq, ws.cnt, tc.pc, tc.perm_c,
+                                                        tc.cell_start, g, b.psi, eps, ws.atomL,
+                                                        ws.atomJ, ws.atomD, ws.empty_fp, ws.hash);
+    else
+      trunc_nearest_empty<false><<<nb_near, 256, 0, s>>>(ac.ph, nq, ws.cnt, tc.pc, tc.perm_c,
+                                                         tc.cell_start, g, b.psi, eps, ws.atomL,
+                                                         ws.atomJ, ws.atomD, ws.empty_fp, ws.hash);
+    gather_d_kernel<<<(nq + 255) / 256, 256, 0, s>>>(ws.atomLam, ac.c2h, nq, ws.lamc);
+    if (b.timing) cudaEventRecord(b.timing[3], s);
+    if (scan)
+      trunc_passB<<<(n + kT - 1) / kT, kT, 0, s>>>(tc.ph, ws.b2h, n, ac.pc, ws.lamc,
+                                                   ac.cell_start, g, c2, r2, r_scan, ws.G);
+    else
+      TCK(cudaMemsetAsync(ws.G, 0, sizeof(double) * n, s));
+    if (b.timing) cudaEventRecord(b.timing[4], s);
+    trunc_assemble<<<(n + 255) / 256, 256, 0, s>>>(ws.G, tc.perm_h, n, ws.empty_fp, b.res);
+    launch_det_sum(ws.atomJ, nq, ws.red, b.res + n + kResJ, s);
+    launch_det_sum(ws.atomD, nq, ws.red + 1024, b.res + n + kResD, s);
+    launch_det_sum(ws.cntd, nq, ws.red + 2048, b.res + n + kResPairs, s);
+    launch_det_sum(ws.emptyd, nq, ws.red + 3072, b.res + n + kResEmpty, s);
+    if (dbg) {
+      cnt_fix_kernel<<<(nq + 255) / 256, 256, 0, s>>>(ws.cnt, nq, reinterpret_cast<uint32_t*>(ws.S));
+      scatter_debug<uint32_t><<<(nq + 255) / 256, 256, 0, s>>>(
+          reinterpret_cast<uint32_t*>(ws.S), ac.perm_h, nq, dbg->count);
+      scatter_debug<unsigned long long><<<(nq + 255) / 256, 256, 0, s>>>(
+          reinterpret_cast<unsigned long long*>(ws.hash), ac.perm_h, nq,
+          reinterpret_cast<unsigned long long*>(dbg->hash));
+      scatter_debug<double><<<(nq + 255) / 256, 256, 0, s>>>(ws.atomL, ac.perm_h, nq, dbg->log_s);
+    }
+  } else {
+    TCK(cudaMemsetAsync(b.res, 0, sizeof(double) * (n + kResTail), s));
+  }
+  set_visited<<<1, 1, 0, s>>>(b.res, n, static_cast<double>(nq));
+  TCK(cudaGetLastError());
+  return 0;
+}
+
+void launch_dense_debug(const DeviceAtoms& a, const DeviceTargets& t, const EvalBuffers& b,
+                        const DebugOut& dbg, cudaStream_t s) {
+  if (a.nq == 0) return;
+  dense_debug_kernel<<<std::min(1024, (a.nq + 255) / 256), 256, 0, s>>>(
+      b.atomL, a.nq, t.n, dbg.count, dbg.hash, dbg.log_s);
+}
+
+int run_nearest_points(TruncWorkspace& ws, const DeviceTargets& t, TargetCells& tc,
+                       const double* xyz_host, size_t m, uint64_t* out_host, cudaStream_t s,
+                       std::string& err) {
+  if (ensure_target_cells(ws, t, tc, tc.cell_valid ? tc.built_r : 0.0, s, err)) return 1;
+  size_t cap = 0;
+  if (3 * m > ws.pts_cap || !ws.pts) {
+    TCK(grow(ws.pts, cap, 3 * m));
+    cap = 0;
+    TCK(grow(ws.near_out, cap, m));
+    ws.pts_cap = 3 * m;
+  }
+  TCK(cudaMemcpyAsync(ws.pts, xyz_host, sizeof(double) * 3 * m, cudaMemcpyHostToDevice, s));
+  nearest_points_kernel<<<static_cast<int>(std::min<size_t>(1024, (m + 7) / 8)), 256, 0, s>>>(
+      ws.pts, static_cast<int>(m), tc.pc, tc.perm_c, tc.cell_start, to_dev(tc.g), ws.near_out,
+      nullptr);
+  TCK(cudaMemcpyAsync(out_host, ws.near_out, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost, s));
+  TCK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int run_covering_cost(TruncWorkspace& ws, const DeviceAtoms& a, const DeviceTargets& t,
+                      TargetCells& tc, double* out, cudaStream_t s, std::string& err) {
+  if (a.nq == 0) {
+    err = "covering cost: empty input";
+    return 1;
+  }
+  if (ensure_target_cells(ws, t, tc, tc.cell_valid ? tc.built_r : 0.0, s, err)) return 1;
+  const size_t m = a.nq;
+  double* pts = nullptr;
+  double* d2 = nullptr;
+  unsigned long long* idx = nullptr;
+  double* dres = nullptr;
+  TCK(cudaMalloc(&pts, sizeof(double) * 3 * m));
+  TCK(cudaMalloc(&d2, sizeof(double) * m));
+  TCK(cudaMalloc(&idx, sizeof(unsigned long long) * m));
+  TCK(cudaMalloc(&dres, sizeof(double)));
+  atoms_to_pts<<<(a.nq + 255) / 256, 256, 0, s>>>(a.x, a.nq, pts);
+  nearest_points_kernel<<<static_cast<int>(std::min<size_t>(4096, (m + 7) / 8)), 256, 0, s>>>(
+      pts, a.nq, tc.pc, tc.perm_c, tc.cell_start, to_dev(tc.g), idx, d2);
+  max_cost_kernel<<<1, 256, 0, s>>>(d2, a.nq, dres);
+  TCK(cudaMemcpyAsync(out, dres, sizeof(double), cudaMemcpyDeviceToHost, s));
+  TCK(cudaStreamSynchronize(s));
+  cudaFree(pts);
+  cudaFree(d2);
+  cudaFree(idx);
+  cudaFree(dres);
+  return 0;
+}
+
+}  // namespace rsot_cuda

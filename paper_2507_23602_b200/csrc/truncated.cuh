@@ -1,0 +1,108 @@
+// truncated.cuh -- cell-list truncated evaluation (internal interface).
+//
+// Replaces the R*-tree ball query of proj/src/spatial_index.cpp:47-61 and
+// the nearest-target fallback of :70-84 with a uniform grid over the
+// targets.  Targets and atoms are each sorted by (cell key, Morton code of
+// the position inside the cell), so
+//   - every cell's members are contiguous and every x-row of cells is one
+//     contiguous range (the scan unit of both passes), and
+//   - 128 consecutive sorted points form a spatially compact CTA chunk.
+// The grid is rebuilt only when the truncation radius leaves the band the
+// grid was sized for; the selection predicate itself is always the exact
+// reference predicate ((dx*dx + dy*dy) + dz*dz) < r*r.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace rsot_cuda {
+
+struct GridDesc {
+  double lo[3] = {0, 0, 0};
+  double h = 1.0;       // cell side
+  int dims[3] = {1, 1, 1};
+  long long ncells = 1;
+  uint64_t id = 0;      // unique id of this grid build
+};
+
+// Two orders per point set:
+//   Hilbert order (radius independent, built once): consecutive runs of 128
+//     points are spatially compact CTA chunks (no long jumps, unlike
+//     Morton or row-major orders);
+//   cell order (per grid): rows of cells are contiguous scan ranges.
+struct PointOrders {
+  bool bbox_set = false;     // set once from the host data at creation
+  double bbox_lo[3] = {0, 0, 0}, bbox_hi[3] = {0, 0, 0};
+  int n = 0;
+  bool hil_valid = false;
+  double4* ph = nullptr;     // Hilbert-sorted copy
+  int* perm_h = nullptr;     // Hilbert position -> original index
+  int* inv_h = nullptr;      // original index -> Hilbert position
+  bool cell_valid = false;
+  uint64_t grid_id = 0;      // grid the cell order was built for
+  double4* pc = nullptr;     // cell-sorted copy
+  int* perm_c = nullptr;     // cell position -> original index
+  int* c2h = nullptr;        // cell position -> Hilbert position
+  int* cell_start = nullptr; // [ncells + 1]
+  void release();
+};
+
+struct TargetCells : PointOrders {
+  double hmin = 0.0;         // cell side of the radius-free grid
+  GridDesc g;
+  double built_r = -1.0;
+};
+
+struct AtomCells : PointOrders {};
+
+struct DebugOut {
+  uint32_t* count = nullptr;  // [nq] original atom order
+  uint64_t* hash = nullptr;
+  double* log_s = nullptr;
+};
+
+struct TruncWorkspace {
+  // device scratch, grown on demand
+  void* cub_tmp = nullptr; size_t cub_bytes = 0;
+  uint64_t* keys = nullptr; uint64_t* keys2 = nullptr; size_t keys_cap = 0;
+  int* idx = nullptr; int* idx2 = nullptr; size_t idx_cap = 0;
+  double* b2s = nullptr; size_t b2s_cap = 0;        // b2 in target cell order
+  double* b2h = nullptr;                              // b2 in target Hilbert order
+  double* lamc = nullptr;                             // atom Lam in cell order
+  double* S = nullptr; double* shiftA = nullptr; double* atomL = nullptr;
+  double* atomLam = nullptr; double* atomJ = nullptr; double* atomD = nullptr;
+  double* cntd = nullptr; double* emptyd = nullptr; uint32_t* cnt = nullptr;
+  uint64_t* hash = nullptr; int* flagged = nullptr; size_t atom_cap = 0;
+  unsigned long long* empty_fp = nullptr; double* G = nullptr; size_t tgt_cap = 0;
+  double* pts = nullptr; unsigned long long* near_out = nullptr; size_t pts_cap = 0;
+  double* red = nullptr;  // reduction partials
+  void release();
+};
+
+// Full truncated evaluation of this rank's atoms (after launch_prologue);
+// leaves the packed partial result in b.res like launch_dense.  Returns 0
+// or nonzero with err set.
+int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
+                  const DeviceTargets& t, TargetCells& tc, EvalBuffers& b,
+                  double eps, double cutoff, int num_sms, DebugOut* dbg,
+                  cudaStream_t s, std::string& err);
+
+// Dense-path debug outputs (count = N, hash over all targets, ln S_q).
+void launch_dense_debug(const DeviceAtoms& a, const DeviceTargets& t,
+                        const EvalBuffers& b, const DebugOut& dbg,
+                        cudaStream_t s);
+
+// Nearest target (original index, lowest on ties) of m host points.
+int run_nearest_points(TruncWorkspace& ws, const DeviceTargets& t,
+                       TargetCells& tc, const double* xyz_host, size_t m,
+                       uint64_t* out_host, cudaStream_t s, std::string& err);
+
+// covering_cost over this rank's atoms.
+int run_covering_cost(TruncWorkspace& ws, const DeviceAtoms& a,
+                      const DeviceTargets& t, TargetCells& tc, double* out,
+                      cudaStream_t s, std::string& err);
+
+}  // namespace rsot_cuda

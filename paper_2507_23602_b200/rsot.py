@@ -1,0 +1,468 @@
+"""Host-side mirror of the reference's C++ evaluation interface.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/rsot/*.hpp so parity tests read like the
+reference's own tests (proj/tests/test_core.cpp):
+
+  SourceAtoms, TargetMeasure        measures.hpp:13-32
+  DualPotential, require_finite     potential.hpp:13-46
+  SolverConfig, TruncationKind      solver_config.hpp:10-45
+  TruncationState, cutoff_*,        evaluate.hpp:33-68, evaluate.cpp:11-72
+    refresh_truncation
+  EvalResult, evaluate_dual         evaluate.hpp:15-28, :79-82
+  SpatialIndex, covering_cost       spatial_index.hpp:15-54
+
+evaluate_dual runs only on the GPU through librsot_b200.so (C ABI
+include/rsot_cuda.h); there is no CPU path.  The cutoff formulas are host
+scalars in the reference too and are restated here.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+
+# ---------------------------------------------------------------------------
+# Types (measures.hpp, potential.hpp, solver_config.hpp, cost.hpp)
+
+
+class CostKind(enum.Enum):
+    SqEuclidean = 0
+    SqGeodesicSphere = 1
+
+
+class TruncationKind(enum.Enum):
+    None_ = 0
+    Pointwise = 1
+    Integrated = 2
+    Geometric = 3
+
+
+class Gauge(enum.Enum):
+    Raw = 0
+    MeanZero = 1
+
+
+def _points3(points) -> np.ndarray:
+    """Point lists are zero-padded to 3 components (point.hpp:10-13)."""
+    p = np.ascontiguousarray(np.asarray(points, dtype=np.float64))
+    if p.ndim == 1:
+        p = p.reshape(-1, 1)
+    if p.shape[1] < 3:
+        p = np.ascontiguousarray(np.hstack([p, np.zeros((p.shape[0], 3 - p.shape[1]))]))
+    return p
+
+
+@dataclass
+class TargetMeasure:
+    dim: int = 0
+    points: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))
+    weights: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+    def size(self) -> int:
+        return int(len(self.points))
+
+
+@dataclass
+class SourceAtoms:
+    dim: int = 0
+    points: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))
+    quad_weights: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    densities: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    masses: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+    def size(self) -> int:
+        return int(len(self.points))
+
+
+@dataclass
+class DualPotential:
+    values: np.ndarray
+    gauge: Gauge = Gauge.Raw
+
+    def size(self) -> int:
+        return int(len(self.values))
+
+
+def require_finite(psi) -> None:
+    """potential.hpp:42-46."""
+    if not np.all(np.isfinite(np.asarray(psi, dtype=np.float64))):
+        raise ValueError("potential has non-finite entries")
+
+
+def weighted_mean(psi, nu) -> float:
+    psi = np.asarray(psi, dtype=np.float64)
+    nu = np.asarray(nu, dtype=np.float64)
+    if psi.shape != nu.shape:
+        raise ValueError("gauge: psi/nu size mismatch")
+    mean = 0.0
+    for p, w in zip(psi.tolist(), nu.tolist()):  # sequential, potential.hpp:26-28
+        mean += p * w
+    return mean
+
+
+def gauge_fixed(psi: DualPotential, nu) -> DualPotential:
+    """potential.hpp:32-40."""
+    mean = weighted_mean(psi.values, nu)
+    return DualPotential(np.asarray(psi.values, dtype=np.float64) - mean, Gauge.MeanZero)
+
+
+@dataclass
+class SolverConfig:
+    epsilon: float = 1e-2
+    delta_tol: float = 1e-3
+    truncation: TruncationKind = TruncationKind.None_
+    tau: float = 1e-4
+    delta_thr: float = 1e-12
+    lbfgs_memory: int = 10
+    max_iterations: int = 1000
+    wolfe_c1: float = 1e-4
+    wolfe_c2: float = 0.9
+    scaling_steps: int = 0
+    cost_kind: CostKind = CostKind.SqEuclidean
+    workers: int = 1
+
+    def validate(self) -> None:
+        """solver_config.hpp:34-44."""
+        if not self.epsilon > 0.0:
+            raise ValueError("epsilon must be > 0")
+        if not self.delta_tol > 0.0:
+            raise ValueError("tolerance must be > 0")
+        if not (0.0 < self.tau < 1.0):
+            raise ValueError("tau must be in (0,1)")
+        if not (0.0 < self.delta_thr < 1.0):
+            raise ValueError("delta_thr must be in (0,1)")
+        if self.lbfgs_memory < 1:
+            raise ValueError("lbfgs memory must be >= 1")
+        if self.max_iterations < 0:
+            raise ValueError("max_iterations must be >= 0")
+        if self.scaling_steps < 0:
+            raise ValueError("scaling_steps must be >= 0")
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+
+
+def ball_radius(kind: CostKind, cutoff: float) -> Optional[float]:
+    """cost.hpp:38-42."""
+    if cutoff < 0.0:
+        return 0.0
+    if kind == CostKind.SqEuclidean:
+        return math.sqrt(2.0 * cutoff)
+    return None
+
+
+# ---------------------------------------------------------------------------
+# Truncation bookkeeping (evaluate.hpp:33-68, evaluate.cpp:11-72)
+
+
+@dataclass
+class TruncationState:
+    cutoff: float = math.inf
+    cached_D: float = 0.0
+    cached_absJ: float = 0.0
+    has_cache: bool = False
+    psi_max: float = 0.0
+    psi_min: float = 0.0
+    psi_range: float = 0.0
+    nu_max: float = 0.0
+    nu_min: float = 0.0
+    covering: float = 0.0
+
+    def set_psi_stats(self, psi) -> None:
+        psi = np.asarray(psi, dtype=np.float64)
+        self.psi_max = float(psi.max())
+        self.psi_min = float(psi.min())
+        self.psi_range = self.psi_max - self.psi_min
+
+    def set_weight_stats(self, nu) -> None:
+        nu = np.asarray(nu, dtype=np.float64)
+        self.nu_max = float(nu.max())
+        self.nu_min = float(nu.min())
+
+
+def cutoff_pointwise(t: TruncationState, eps: float, delta_thr: float) -> float:
+    return t.psi_max + eps * math.log(t.nu_max / delta_thr)
+
+
+def cutoff_integrated(t: TruncationState, eps: float, tau: float) -> float:
+    absJ = max(t.cached_absJ, 1e-30)
+    if absJ <= 1e-30:
+        raise RuntimeError("functional estimate degenerate")
+    c = t.psi_max + eps * math.log(eps * t.cached_D / (tau * absJ))
+    return max(c, t.covering)
+
+
+def cutoff_geometric(t: TruncationState, eps: float, tau: float) -> float:
+    absJ = max(t.cached_absJ, 1e-30)
+    if absJ <= 1e-30:
+        raise RuntimeError("functional estimate degenerate")
+    c = t.covering + t.psi_range + eps * math.log(eps / (t.nu_min * tau * absJ))
+    return max(c, t.covering)
+
+
+def cutoff_bootstrap(t: TruncationState, eps: float, tau: float) -> float:
+    c = t.covering + t.psi_range + eps * math.log(eps / (t.nu_min * tau))
+    return max(c, t.covering)
+
+
+def refresh_truncation(t: TruncationState, psi, cfg: SolverConfig) -> None:
+    t.set_psi_stats(psi)
+    if cfg.truncation == TruncationKind.None_:
+        t.cutoff = math.inf
+    elif cfg.truncation == TruncationKind.Pointwise:
+        t.cutoff = cutoff_pointwise(t, cfg.epsilon, cfg.delta_thr)
+    elif cfg.truncation == TruncationKind.Integrated:
+        t.cutoff = (cutoff_integrated(t, cfg.epsilon, cfg.tau) if t.has_cache
+                    else cutoff_bootstrap(t, cfg.epsilon, cfg.tau))
+    else:
+        t.cutoff = (cutoff_geometric(t, cfg.epsilon, cfg.tau) if t.has_cache
+                    else cutoff_bootstrap(t, cfg.epsilon, cfg.tau))
+
+
+@dataclass
+class EvalResult:
+    J: float = 0.0
+    gradient: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    D: float = 0.0
+    atoms_visited: int = 0
+    candidate_pairs: int = 0
+    empty_candidate_atoms: int = 0
+
+    def grad_l1(self) -> float:
+        return float(np.abs(self.gradient).sum())
+
+
+# ---------------------------------------------------------------------------
+# Device context and resident data
+
+
+class Context:
+    """One CUDA context per GPU (one process per GPU)."""
+
+    _default = {}
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.rsot_cuda_ctx_create(int(device), ctypes.byref(h)))
+        self.handle = h
+        self.device = int(device)
+        self.rank = 0
+        self.world = 1
+
+    @classmethod
+    def default(cls, device: int = 0) -> "Context":
+        if device not in cls._default:
+            cls._default[device] = cls(device)
+        return cls._default[device]
+
+    @staticmethod
+    def unique_id() -> bytes:
+        lib = _lib.load()
+        buf = (ctypes.c_uint8 * 128)()
+        _lib.check(lib.rsot_cuda_comm_unique_id(buf))
+        return bytes(buf)
+
+    def set_comm(self, rank: int, world: int, uid: bytes) -> None:
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        _lib.check(self.lib.rsot_cuda_ctx_set_comm(self.handle, int(rank), int(world), buf))
+        self.rank, self.world = int(rank), int(world)
+
+    def shard_range(self, nq: int):
+        lo, hi = ctypes.c_size_t(), ctypes.c_size_t()
+        self.lib.rsot_cuda_shard_range(nq, self.rank, self.world, ctypes.byref(lo), ctypes.byref(hi))
+        return lo.value, hi.value
+
+    @property
+    def stream(self) -> int:
+        return self.lib.rsot_cuda_ctx_stream(self.handle)
+
+    def synchronize(self) -> None:
+        _lib.check(self.lib.rsot_cuda_ctx_synchronize(self.handle))
+
+    def set_timing(self, on: bool) -> None:
+        _lib.check(self.lib.rsot_cuda_ctx_set_timing(self.handle, 1 if on else 0))
+
+    def last_kernel_ms(self):
+        a, b, t = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        _lib.check(self.lib.rsot_cuda_last_kernel_ms(self.handle, ctypes.byref(a), ctypes.byref(b),
+                                                     ctypes.byref(t)))
+        return a.value, b.value, t.value
+
+    def fp64_dfma_rate(self) -> float:
+        v = ctypes.c_double()
+        _lib.check(self.lib.rsot_cuda_measure_fp64_peak(self.handle, ctypes.byref(v)))
+        return v.value
+
+
+def _ptr(a: np.ndarray) -> ctypes.c_void_p:
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class DeviceTargets:
+    """Resident TargetMeasure (+ cell list) on one context."""
+
+    def __init__(self, ctx: Context, points, weights):
+        self.ctx = ctx
+        pts = _points3(points)
+        nu = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+        if len(pts) != len(nu):
+            raise ValueError("target measure: point/weight size mismatch")
+        h = ctypes.c_void_p()
+        _lib.check(ctx.lib.rsot_cuda_targets_create(ctx.handle, _ptr(pts), _ptr(nu), len(pts),
+                                                    ctypes.byref(h)))
+        self.handle = h
+        self.n = len(pts)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.ctx.lib.rsot_cuda_targets_destroy(self.handle)
+        except Exception:
+            pass
+
+
+class DeviceAtoms:
+    """Resident shard of SourceAtoms (points, masses) on one context."""
+
+    def __init__(self, ctx: Context, points, masses, shard: bool = True):
+        self.ctx = ctx
+        pts = _points3(points)
+        m = np.ascontiguousarray(np.asarray(masses, dtype=np.float64))
+        lo, hi = ctx.shard_range(len(pts)) if shard else (0, len(pts))
+        pts = np.ascontiguousarray(pts[lo:hi])
+        m = np.ascontiguousarray(m[lo:hi])
+        h = ctypes.c_void_p()
+        _lib.check(ctx.lib.rsot_cuda_atoms_create(ctx.handle, _ptr(pts), _ptr(m), len(pts),
+                                                  ctypes.byref(h)))
+        self.handle = h
+        self.nq = len(pts)
+        self.lo, self.hi = lo, hi
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.ctx.lib.rsot_cuda_atoms_destroy(self.handle)
+        except Exception:
+            pass
+
+
+class SpatialIndex:
+    """Per-stage index over the target points (spatial_index.hpp:15-40).
+
+    The device-side state is the target cell list; it lives with the
+    resident targets used by evaluate_dual.  Throws ValueError on an empty
+    point set like the reference ctor (spatial_index.cpp:31-32).
+    """
+
+    def __init__(self, points, ctx: Optional[Context] = None):
+        pts = _points3(points) if len(points) else np.zeros((0, 3))
+        if len(pts) == 0:
+            raise ValueError("spatial index: empty point set")
+        self.ctx = ctx or Context.default()
+        self.points = pts
+        self._dev = DeviceTargets(self.ctx, pts, np.ones(len(pts)))
+
+    def size(self) -> int:
+        return len(self.points)
+
+    def nearest(self, center) -> int:
+        c = _points3(np.asarray(center, dtype=np.float64).reshape(1, -1))
+        out = np.zeros(1, dtype=np.uint64)
+        _lib.check(self.ctx.lib.rsot_cuda_nearest(self.ctx.handle, self._dev.handle, _ptr(c), 1,
+                                                  _ptr(out)))
+        return int(out[0])
+
+    def nearest_many(self, centers) -> np.ndarray:
+        c = _points3(centers)
+        out = np.zeros(len(c), dtype=np.uint64)
+        _lib.check(self.ctx.lib.rsot_cuda_nearest(self.ctx.handle, self._dev.handle, _ptr(c), len(c),
+                                                  _ptr(out)))
+        return out.astype(np.int64)
+
+
+def build_index(points, ctx: Optional[Context] = None) -> SpatialIndex:
+    return SpatialIndex(points, ctx)
+
+
+def _device_targets(target: TargetMeasure, ctx: Context) -> DeviceTargets:
+    key = (id(ctx), target.points.ctypes.data, target.weights.ctypes.data, target.size())
+    dev = getattr(target, "_rsot_dev", None)
+    if dev is None or dev[0] != key:
+        dev = (key, DeviceTargets(ctx, target.points, target.weights))
+        object.__setattr__(target, "_rsot_dev", dev)
+    return dev[1]
+
+
+def _device_atoms(atoms: SourceAtoms, ctx: Context) -> DeviceAtoms:
+    key = (id(ctx), atoms.points.ctypes.data, atoms.masses.ctypes.data, atoms.size(), ctx.world)
+    dev = getattr(atoms, "_rsot_dev", None)
+    if dev is None or dev[0] != key:
+        dev = (key, DeviceAtoms(ctx, atoms.points, atoms.masses))
+        object.__setattr__(atoms, "_rsot_dev", dev)
+    return dev[1]
+
+
+def covering_cost(atoms: SourceAtoms, target: TargetMeasure, kind: CostKind = CostKind.SqEuclidean,
+                  ctx: Optional[Context] = None) -> float:
+    """spatial_index.cpp:101-121 (SqEuclidean only)."""
+    if atoms.size() == 0 or target.size() == 0:
+        raise ValueError("covering cost: empty input")
+    if kind != CostKind.SqEuclidean:
+        raise NotImplementedError("SqGeodesicSphere is out of scope for the B200 evaluator")
+    ctx = ctx or Context.default()
+    out = ctypes.c_double()
+    _lib.check(ctx.lib.rsot_cuda_covering_cost(ctx.handle, _device_atoms(atoms, ctx).handle,
+                                               _device_targets(target, ctx).handle, ctypes.byref(out)))
+    return out.value
+
+
+def evaluate_dual(atoms: SourceAtoms, target: TargetMeasure, psi: DualPotential,
+                  cfg: SolverConfig, trunc: TruncationState, index: Optional[SpatialIndex] = None,
+                  ctx: Optional[Context] = None) -> EvalResult:
+    """rsot::evaluate_dual (evaluate.hpp:79-82, evaluate.cpp:86-174) on the GPU."""
+    values = np.ascontiguousarray(np.asarray(psi.values, dtype=np.float64))
+    if len(values) != target.size():
+        raise ValueError("evaluate_dual: psi length != target count")
+    require_finite(values)
+    if cfg.cost_kind != CostKind.SqEuclidean:
+        raise NotImplementedError("SqGeodesicSphere is out of scope for the B200 evaluator")
+    ctx = ctx or (index.ctx if index is not None else Context.default())
+    dev_t = _device_targets(target, ctx)
+    dev_a = _device_atoms(atoms, ctx)
+    g = np.empty(target.size(), dtype=np.float64)
+    sc = _lib.RsotCudaScalars()
+    _lib.check(ctx.lib.rsot_cuda_eval(ctx.handle, dev_a.handle, dev_t.handle, _ptr(values),
+                                      float(cfg.epsilon), float(trunc.cutoff), _ptr(g),
+                                      ctypes.byref(sc)))
+    return EvalResult(J=sc.J, gradient=g, D=sc.D, atoms_visited=int(sc.atoms_visited),
+                      candidate_pairs=int(sc.candidate_pairs),
+                      empty_candidate_atoms=int(sc.empty_candidate_atoms))
+
+
+def evaluate_dual_debug(atoms: SourceAtoms, target: TargetMeasure, psi, eps: float, cutoff: float,
+                        ctx: Optional[Context] = None):
+    """evaluate_dual plus per-atom candidate counts, candidate hashes and ln S_q
+    (for selection parity against the oracle)."""
+    ctx = ctx or Context.default()
+    values = np.ascontiguousarray(np.asarray(psi, dtype=np.float64))
+    dev_t = _device_targets(target, ctx)
+    dev_a = _device_atoms(atoms, ctx)
+    g = np.empty(target.size(), dtype=np.float64)
+    cnt = np.zeros(dev_a.nq, dtype=np.uint32)
+    hsh = np.zeros(dev_a.nq, dtype=np.uint64)
+    logs = np.zeros(dev_a.nq, dtype=np.float64)
+    sc = _lib.RsotCudaScalars()
+    _lib.check(ctx.lib.rsot_cuda_eval_debug(ctx.handle, dev_a.handle, dev_t.handle, _ptr(values),
+                                            float(eps), float(cutoff), _ptr(g), ctypes.byref(sc),
+                                            _ptr(cnt), _ptr(hsh), _ptr(logs)))
+    res = EvalResult(J=sc.J, gradient=g, D=sc.D, atoms_visited=int(sc.atoms_visited),
+                     candidate_pairs=int(sc.candidate_pairs),
+                     empty_candidate_atoms=int(sc.empty_candidate_atoms))
+    return res, cnt, hsh, logs

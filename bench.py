@@ -1,0 +1,355 @@
+"""bench.py -- RSOT dual objective + gradient evaluations on B200.
+
+Default workload = BASELINE.json configs[1] (cfg2: 3D dense, 262,144 Gauss
+atoms x 16,384 mixture targets, eps = 1e-2, fp64, fresh psi per
+evaluation).  A step is one evaluation (dual objective J + gradient over all
+pairs) with a fresh psi.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2]
+  python bench.py --impl reference ...   (the reference CPU evaluate_dual)
+
+Under torchrun (N > 1) every rank owns a contiguous atom shard and the
+library reduces [g | J | D | counters] with one ncclAllReduce per
+evaluation; timing is the max over ranks.
+
+Prints ONE JSON line on rank 0.  `value` times device-resident psi/g
+(rsot_cuda_eval_device); `e2e` times the C-ABI call a user makes
+(rsot_cuda_eval) with pinned host psi in / host g out, copies included.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "dual obj+grad evals/sec"
+W_PAIR = 25  # FP64-pipe instructions per pair in the reference formula
+WORKLOADS = {
+    "cfg1": "cfg1: 2D dense, 64x64 Q1 quads x 2x2 Gauss = 16,384 atoms, N=1,024 U[0,1]^2 targets, eps=1e-2",
+    "cfg2": "cfg2: 3D dense, 32^3 hexes x 2^3 Gauss = 262,144 atoms (3-Gaussian mixture density), "
+            "N=16,384 mixture targets, eps=1e-2, fresh psi~N(0,1e-3^2) per evaluation",
+    "cfg3": "cfg3: 3D truncated (pointwise 1e-12), 64^3 hexes x 2^3 = 2,097,152 atoms, N=262,144, eps=1e-3",
+    "cfg5": "cfg5: 3D truncated (pointwise 1e-12), 128^3 hexes x 2^3 = 16,777,216 atoms, N=1,048,576 "
+            "U[0,1]^3, eps=1e-4",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(
+        os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle/_ref: the reference's own evaluate_dual compiled
+# from its sources; oracle port if that was not built)
+
+def cpu_reference_runner(prob, sample_atoms):
+    from paper_2507_23602_b200 import synth
+    sub = synth.subsample_atoms(prob, sample_atoms) if sample_atoms < prob.nq else prob
+    threads = os.cpu_count() or 1
+    try:
+        from oracle.oracle import RefLib
+        ref = RefLib()
+        rp = ref.problem(prob.dim, sub.atoms, sub.masses, prob.targets, prob.nu)
+        kind = "reference"
+
+        def run(psi, cutoff):
+            return rp.evaluate_dual(psi, prob.eps, cutoff, threads)
+    except ImportError:
+        from oracle.oracle import COracle
+        C = COracle()
+        kind = "port"
+
+        def run(psi, cutoff):
+            return C.evaluate_dual(sub.atoms, sub.masses, prob.targets, prob.nu, psi, prob.eps, cutoff, threads)
+    frac = sub.nq / prob.nq
+    desc = (f"{sub.nq} of {prob.nq} atoms (seeded subset) x all {prob.n} targets per evaluation, "
+            f"{threads} std::thread workers (SolverConfig::workers), evals/s extrapolated by the atom fraction")
+    return run, frac, kind, threads, desc
+
+
+def cpu_sample_size(prob):
+    # ~2-4 s per sampled evaluation on a 16-core host
+    pairs_budget = {"none": 1.0e9, "pointwise": 6.0e7}[prob.truncation]
+    per_atom = prob.n if prob.truncation == "none" else 700
+    return int(max(256, min(prob.nq, pairs_budget / per_atom)))
+
+
+def time_cpu(prob, steps, warmup):
+    run, frac, kind, threads, desc = cpu_reference_runner(prob, cpu_sample_size(prob))
+    times = []
+    for k in range(warmup + steps):
+        psi = prob.psi(k)
+        t0 = time.perf_counter()
+        run(psi, prob.cutoff(psi))
+        dt = time.perf_counter() - t0
+        if k >= warmup:
+            times.append(dt)
+    per_eval_full = statistics.median(times) / frac
+    return 1.0 / per_eval_full, kind, threads, desc, times
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    from paper_2507_23602_b200 import synth
+    prob = synth.make(args.workload)
+    steps = max(1, min(args.steps, 10))
+    warm = max(0, min(args.warmup, 2))
+    v, kind, cores, desc, times = time_cpu(prob, steps, warm)
+    line = {
+        "metric": METRIC, "value": v, "unit": "evals/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+        "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded; BASELINE shapes)", "impl": "reference",
+        "config": {"workload": WORKLOADS[args.workload]},
+        "pairs_per_s": v * (prob.nq * prob.n if prob.truncation == "none" else float("nan")),
+        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": kind, "sample": desc},
+        "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.idx = device_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"rsot_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in open(self.path):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        load = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2507_23602_b200 as rs
+    from paper_2507_23602_b200 import _lib, synth
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    ctx = rs.Context(local_rank)
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(rs.Context.unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        ctx.set_comm(rank, world, bytes(uid.cpu().numpy().tobytes()))
+    lib = _lib.load()
+    prob = synth.make(args.workload)
+    dev_t = rs.rsot.DeviceTargets(ctx, prob.targets, prob.nu)
+    dev_a = rs.rsot.DeviceAtoms(ctx, prob.atoms, prob.masses)
+    n = prob.n
+    K, W = args.steps, max(3, args.warmup)
+    psis = [prob.psi(k) for k in range(W + K)]
+    cutoffs = [prob.cutoff(p) for p in psis]
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local_rank))
+    d_psi = torch.tensor(np.stack(psis), dtype=torch.float64, device="cuda")
+    d_g = torch.empty(n, dtype=torch.float64, device="cuda")
+    d_sc = torch.empty(8, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
+    torch.cuda.synchronize()
+
+    def ev(k):
+        return lib.rsot_cuda_eval_device(ctx.handle, dev_a.handle, dev_t.handle,
+                                         ctypes.c_void_p(d_psi[k].data_ptr()), prob.eps, cutoffs[k],
+                                         ctypes.c_void_p(d_g.data_ptr()), ctypes.c_void_p(d_sc.data_ptr()))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up (also builds cell lists / Hilbert orders for truncated) ----
+    for k in range(W):
+        _lib.check(ev(k))
+    _lib.check(lib.rsot_cuda_check_status(ctx.handle))
+    torch.cuda.synchronize()
+
+    # ---- per-kernel timing (CUDA events inside the library, same stream) ----
+    ctx.set_timing(True)
+    passA, passB = [], []
+    for k in range(min(K, 5)):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        _lib.check(ev(W + k))
+        ctx.synchronize()
+        a, b, _ = ctx.last_kernel_ms()
+        passA.append(a)
+        passB.append(b)
+    ctx.set_timing(False)
+
+    # ---- timed region: K device-resident evaluations ----
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    launches0 = lib.rsot_cuda_kernel_launches()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(K):
+        with torch.cuda.stream(stream):
+            flush.zero_()  # L2 flush between steps (inside the timed region)
+        _lib.check(ev(W + k))
+    e1.record(stream)
+    barrier()
+    launches = lib.rsot_cuda_kernel_launches() - launches0
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    _lib.check(lib.rsot_cuda_check_status(ctx.handle))
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / K
+    sc = d_sc.cpu().numpy()
+    pairs = float(sc[3])
+
+    # ---- e2e: the C-ABI call with pinned host psi / host g, copies inside ----
+    h_psi = torch.empty((K, n), dtype=torch.float64).pin_memory()
+    h_psi.copy_(torch.from_numpy(np.stack(psis[W:W + K])))
+    h_g = torch.empty(n, dtype=torch.float64).pin_memory()
+    scal = _lib.RsotCudaScalars()
+    barrier()
+    t0 = time.perf_counter()
+    for k in range(K):
+        _lib.check(lib.rsot_cuda_eval(ctx.handle, dev_a.handle, dev_t.handle,
+                                      ctypes.c_void_p(h_psi[k].data_ptr()), prob.eps, cutoffs[W + k],
+                                      ctypes.c_void_p(h_g.data_ptr()), ctypes.byref(scal)))
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_v = K / e2e_s
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    dfma = ctx.fp64_dfma_rate()
+    value = 1e3 / ms_step
+    kern_ms = statistics.median(passA) + statistics.median(passB)
+    algo_flops = 2.0 * W_PAIR * pairs / world  # per GPU: DFMA-equivalent flops of the reference formula
+    achieved = algo_flops / (kern_ms * 1e-3) / 1e12
+    peak = 2.0 * dfma / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"ncu_summary_{args.workload}.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_eval")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded generator with BASELINE shapes; no dataset exists)",
+        "config": {"workload": WORKLOADS[args.workload], "nq": prob.nq, "n": prob.n, "eps": prob.eps,
+                   "parallelism": f"atoms sharded over {world} GPU(s), targets replicated, 1 allreduce/eval",
+                   "l2": "flushed between steps (256 MiB write, inside the timed region)"},
+        "pairs_per_s": pairs * value,
+        "candidate_pairs_per_eval": pairs,
+        "roofline": {
+            "bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": traffic,
+            "kernel": "pass A (LSE) + pass B (gradient gather), per GPU",
+            "kernel_ms": {"pass_a": statistics.median(passA), "pass_b": statistics.median(passB)},
+            "definition": f"{W_PAIR} FP64-pipe instr/pair (reference formula, one exp/pair) x 2 flop x pairs "
+                          "/ CUDA-event time of the two passes; peak = measured DFMA rate x 2 (live probe)",
+        },
+        "e2e": {"value": e2e_v, "unit": "evals/s", "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n + 8 * 6},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            v, kind, cores, desc, _ = time_cpu(prob, 2, 1)
+            line["cpu_baseline"] = {"value": v, "unit": "evals/s", "cores": cores, "kind": kind, "sample": desc}
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "port",
+                                    "sample": f"unavailable: {e}"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local_rank = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

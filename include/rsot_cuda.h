@@ -153,6 +153,9 @@ int rsot_cuda_covering_cost(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
 int rsot_cuda_ctx_set_timing(rsot_cuda_ctx* ctx, int enable);
 int rsot_cuda_last_kernel_ms(rsot_cuda_ctx* ctx, double* pass_a_ms,
                              double* pass_b_ms, double* total_ms);
+/* Number of kernels this library has launched in this process (all
+ * contexts); bench.py reports the per-step delta as gpu_launches. */
+uint64_t rsot_cuda_kernel_launches(void);
 /* Measured FP64 DFMA rate of the device (lane-FMAs per second). */
 int rsot_cuda_measure_fp64_peak(rsot_cuda_ctx* ctx, double* dfma_per_s);
 

@@ -251,6 +251,8 @@ extern "C" {
 
 int rsot_cuda_abi_version(void) { return RSOT_CUDA_ABI_VERSION; }
 
+uint64_t rsot_cuda_kernel_launches(void) { return g_kernel_launches.load(); }
+
 const char* rsot_cuda_last_error(void) { return g_last_error.c_str(); }
 
 int rsot_cuda_ctx_create(int device, rsot_cuda_ctx** out) {

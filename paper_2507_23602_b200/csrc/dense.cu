@@ -22,6 +22,8 @@
 
 namespace rsot_cuda {
 
+std::atomic<unsigned long long> g_kernel_launches{0};
+
 namespace {
 
 constexpr int kThreads = 128;
@@ -413,6 +415,10 @@ int red_blocks(size_t n) {
 
 DenseLaunch plan_dense(int nq, int n, int num_sms) {
   DenseLaunch p;
+  if (nq <= 0 || n <= 0) {
+    p.apt = p.tpt = p.splitsA = p.splitsB = 1;
+    return p;
+  }
   // Enough CTAs for ~16 waves of ~6 resident CTAs per SM, while keeping
   // at least 512 targets (pass A) / 1024 atoms (pass B) per CTA.
   const long want = 16L * num_sms * 6;
@@ -437,17 +443,17 @@ void launch_det_sum(const double* x, size_t n, double* partials, double* out,
                     cudaStream_t s) {
   const int nb = red_blocks(n);
   const size_t chunk = (n + nb - 1) / nb;
-  det_sum_blocks<<<nb, 256, 0, s>>>(x, n, chunk, partials);
-  det_sum_final<<<1, 256, 0, s>>>(partials, nb, out);
+  (note_launch(), det_sum_blocks<<<nb, 256, 0, s>>>(x, n, chunk, partials));
+  (note_launch(), det_sum_final<<<1, 256, 0, s>>>(partials, nb, out));
 }
 
 void launch_prologue(const DeviceTargets& t, EvalBuffers& b, double eps,
                      cudaStream_t s) {
   const int nb = red_blocks(static_cast<size_t>(t.n));
   const int chunk = (t.n + nb - 1) / nb;
-  prologue_blocks<<<nb, 256, 0, s>>>(t.y, t.nu, b.psi, t.n, 1.0 / eps, b.b2,
-                                     b.part, chunk);
-  prologue_final<<<1, 256, 0, s>>>(b.part, nb, b.scal);
+  (note_launch(), prologue_blocks<<<nb, 256, 0, s>>>(t.y, t.nu, b.psi, t.n, 1.0 / eps, b.b2,
+                                     b.part, chunk));
+  (note_launch(), prologue_final<<<1, 256, 0, s>>>(b.part, nb, b.scal));
 }
 
 void launch_dense(const DeviceAtoms& a, const DeviceTargets& t, EvalBuffers& b,
@@ -462,41 +468,41 @@ void launch_dense(const DeviceAtoms& a, const DeviceTargets& t, EvalBuffers& b,
     dim3 gA((nq + kThreads * p.apt - 1) / (kThreads * p.apt), splitsA);
     if (b.timing) cudaEventRecord(b.timing[1], s);
     if (p.apt == 2)
-      dense_passA<2><<<gA, kThreads, 0, s>>>(a.x, nq, t.y, b.b2, n, per_split,
-                                              b.scal, c2, b.partS, b.shiftA);
+      (note_launch(), dense_passA<2><<<gA, kThreads, 0, s>>>(a.x, nq, t.y, b.b2, n, per_split,
+                                              b.scal, c2, b.partS, b.shiftA));
     else
-      dense_passA<1><<<gA, kThreads, 0, s>>>(a.x, nq, t.y, b.b2, n, per_split,
-                                              b.scal, c2, b.partS, b.shiftA);
+      (note_launch(), dense_passA<1><<<gA, kThreads, 0, s>>>(a.x, nq, t.y, b.b2, n, per_split,
+                                              b.scal, c2, b.partS, b.shiftA));
     if (b.timing) cudaEventRecord(b.timing[2], s);
-    dense_finalizeA<<<(nq + 255) / 256, 256, 0, s>>>(
+    (note_launch(), dense_finalizeA<<<(nq + 255) / 256, 256, 0, s>>>(
         a.x, nq, b.partS, splitsA, b.shiftA, b.scal, eps, b.atomL, b.atomLam,
-        b.atomJ, b.atomD, b.flagged);
-    dense_exact_fallback<<<64, 256, 0, s>>>(a.x, t.y, b.psi, n, b.scal, b.flagged,
+        b.atomJ, b.atomD, b.flagged));
+    (note_launch(), dense_exact_fallback<<<64, 256, 0, s>>>(a.x, t.y, b.psi, n, b.scal, b.flagged,
                                             eps, b.atomL, b.atomLam, b.atomJ,
-                                            b.atomD);
+                                            b.atomD));
     const int per_splitB = (((nq + p.splitsB - 1) / p.splitsB) + kTile - 1) / kTile * kTile;
     const int splitsB = (nq + per_splitB - 1) / per_splitB;
     dim3 gB((n + kThreads * p.tpt - 1) / (kThreads * p.tpt), splitsB);
     if (b.timing) cudaEventRecord(b.timing[3], s);
     if (p.tpt == 2)
-      dense_passB<2><<<gB, kThreads, 0, s>>>(a.x, b.atomLam, nq, per_splitB, t.y,
-                                              b.b2, n, c2, b.partG);
+      (note_launch(), dense_passB<2><<<gB, kThreads, 0, s>>>(a.x, b.atomLam, nq, per_splitB, t.y,
+                                              b.b2, n, c2, b.partG));
     else
-      dense_passB<1><<<gB, kThreads, 0, s>>>(a.x, b.atomLam, nq, per_splitB, t.y,
-                                              b.b2, n, c2, b.partG);
+      (note_launch(), dense_passB<1><<<gB, kThreads, 0, s>>>(a.x, b.atomLam, nq, per_splitB, t.y,
+                                              b.b2, n, c2, b.partG));
     if (b.timing) cudaEventRecord(b.timing[4], s);
-    reduce_partG<<<(n + 255) / 256, 256, 0, s>>>(b.partG, splitsB, n, b.res);
+    (note_launch(), reduce_partG<<<(n + 255) / 256, 256, 0, s>>>(b.partG, splitsB, n, b.res));
     launch_det_sum(b.atomJ, nq, b.part, b.res + n + kResJ, s);
     launch_det_sum(b.atomD, nq, b.part + kRedBlocks, b.res + n + kResD, s);
   } else {
     cudaMemsetAsync(b.res, 0, sizeof(double) * (n + kResTail), s);
   }
-  set_dense_counts<<<1, 1, 0, s>>>(b.res, n, static_cast<double>(nq));
+  (note_launch(), set_dense_counts<<<1, 1, 0, s>>>(b.res, n, static_cast<double>(nq)));
 }
 
 void launch_finalize(const DeviceTargets& t, EvalBuffers& b, cudaStream_t s) {
-  finalize_kernel<<<(t.n + 255) / 256, 256, 0, s>>>(b.res, t.nu, t.n, b.scal,
-                                                    b.g_out, b.scalars_out);
+  (note_launch(), finalize_kernel<<<(t.n + 255) / 256, 256, 0, s>>>(b.res, t.nu, t.n, b.scal,
+                                                    b.g_out, b.scalars_out));
 }
 
 double measure_dfma_rate(cudaStream_t s) {
@@ -512,7 +518,7 @@ double measure_dfma_rate(cudaStream_t s) {
   float best = 1e30f;
   for (int r = 0; r < 4; ++r) {
     cudaEventRecord(e0, s);
-    dfma_probe<<<blocks, threads, 0, s>>>(out, 0.999, 1e-3, iters);
+    (note_launch(), dfma_probe<<<blocks, threads, 0, s>>>(out, 0.999, 1e-3, iters));
     cudaEventRecord(e1, s);
     cudaEventSynchronize(e1);
     float ms = 0.f;

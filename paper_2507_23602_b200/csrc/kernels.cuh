@@ -10,10 +10,16 @@
 #pragma once
 
 #include <cstddef>
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace rsot_cuda {
+
+// Process-wide count of kernels this library has launched
+// (rsot_cuda_kernel_launches); every launch site goes through note_launch().
+extern std::atomic<unsigned long long> g_kernel_launches;
+inline void note_launch() { g_kernel_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // Indices into the per-eval device scalar block.
 enum ScalarSlot : int {

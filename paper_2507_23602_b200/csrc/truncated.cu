@@ -810,13 +810,13 @@ int build_hilbert(TruncWorkspace& ws, const double4* pts, int n, PointOrders& po
       const double ext = po.bbox_hi[d] - po.bbox_lo[d];
       sc[d] = ext > 0.0 ? static_cast<double>(1u << kHilBits) / ext : 0.0;
     }
-    hilbert_keys_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, n, po.bbox_lo[0], po.bbox_lo[1],
+    (note_launch(), hilbert_keys_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, n, po.bbox_lo[0], po.bbox_lo[1],
                                                         po.bbox_lo[2], sc[0], sc[1], sc[2],
-                                                        ws.keys, ws.idx);
+                                                        ws.keys, ws.idx));
     if (radix_sort(ws, n, 3 * kHilBits, s, err)) return 1;
-    gather4_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, ws.idx2, n, po.ph);
+    (note_launch(), gather4_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, ws.idx2, n, po.ph));
     TCK(cudaMemcpyAsync(po.perm_h, ws.idx2, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
-    invert_perm_kernel<<<(n + 255) / 256, 256, 0, s>>>(po.perm_h, n, po.inv_h);
+    (note_launch(), invert_perm_kernel<<<(n + 255) / 256, 256, 0, s>>>(po.perm_h, n, po.inv_h));
   }
   TCK(cudaGetLastError());
   po.n = n;
@@ -836,15 +836,15 @@ int build_cells(TruncWorkspace& ws, const double4* pts, int n, const GridDesc& g
   TCK(realloc_exact(po.cell_start, g.ncells + 1));
   const GridDev gd = to_dev(g);
   if (n > 0) {
-    cell_keys_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, n, gd, ws.keys, ws.idx);
+    (note_launch(), cell_keys_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, n, gd, ws.keys, ws.idx));
     int end_bit = 3 * kMortonBits;
     while ((1ll << (end_bit - 3 * kMortonBits)) < g.ncells) ++end_bit;
     if (radix_sort(ws, n, end_bit, s, err)) return 1;
-    gather4_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, ws.idx2, n, po.pc);
+    (note_launch(), gather4_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, ws.idx2, n, po.pc));
     TCK(cudaMemcpyAsync(po.perm_c, ws.idx2, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
-    compose_kernel<<<(n + 255) / 256, 256, 0, s>>>(po.inv_h, po.perm_c, n, po.c2h);
+    (note_launch(), compose_kernel<<<(n + 255) / 256, 256, 0, s>>>(po.inv_h, po.perm_c, n, po.c2h));
   }
-  cell_start_kernel<<<(n + 1 + 255) / 256, 256, 0, s>>>(ws.keys2, n, g.ncells, po.cell_start);
+  (note_launch(), cell_start_kernel<<<(n + 1 + 255) / 256, 256, 0, s>>>(ws.keys2, n, g.ncells, po.cell_start));
   TCK(cudaGetLastError());
   po.grid_id = g.id;
   po.cell_valid = true;
@@ -981,66 +981,66 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
 
   TCK(cudaMemsetAsync(b.scal + kSlotFlagCount, 0, sizeof(double), s));
   TCK(cudaMemsetAsync(ws.empty_fp, 0, sizeof(unsigned long long) * 3 * static_cast<size_t>(n), s));
-  gather_d_kernel<<<(n + 255) / 256, 256, 0, s>>>(b.b2, tc.perm_c, n, ws.b2s);
-  gather_d_kernel<<<(n + 255) / 256, 256, 0, s>>>(b.b2, tc.perm_h, n, ws.b2h);
+  (note_launch(), gather_d_kernel<<<(n + 255) / 256, 256, 0, s>>>(b.b2, tc.perm_c, n, ws.b2s));
+  (note_launch(), gather_d_kernel<<<(n + 255) / 256, 256, 0, s>>>(b.b2, tc.perm_h, n, ws.b2h));
   if (nq > 0) {
     const int nblk = (nq + kT - 1) / kT;
     if (b.timing) cudaEventRecord(b.timing[1], s);
     if (scan) {
       if (dbg)
-        trunc_passA<true><<<nblk, kT, 0, s>>>(ac.ph, nq, tc.pc, ws.b2s, tc.perm_c, tc.cell_start,
+        (note_launch(), trunc_passA<true><<<nblk, kT, 0, s>>>(ac.ph, nq, tc.pc, ws.b2s, tc.perm_c, tc.cell_start,
                                               g, b.scal, c2, r2, r_scan, ws.S, ws.shiftA,
-                                              ws.cnt, ws.hash);
+                                              ws.cnt, ws.hash));
       else
-        trunc_passA<false><<<nblk, kT, 0, s>>>(ac.ph, nq, tc.pc, ws.b2s, tc.perm_c, tc.cell_start,
+        (note_launch(), trunc_passA<false><<<nblk, kT, 0, s>>>(ac.ph, nq, tc.pc, ws.b2s, tc.perm_c, tc.cell_start,
                                                g, b.scal, c2, r2, r_scan, ws.S, ws.shiftA,
-                                               ws.cnt, ws.hash);
+                                               ws.cnt, ws.hash));
     } else {
       // radius <= 0: every candidate set is empty (spatial_index.cpp:50).
       TCK(cudaMemsetAsync(ws.cnt, 0, sizeof(uint32_t) * nq, s));
     }
     if (b.timing) cudaEventRecord(b.timing[2], s);
-    trunc_finalizeA<<<(nq + 255) / 256, 256, 0, s>>>(ac.ph, nq, ws.S, ws.shiftA, ws.cnt, b.scal,
+    (note_launch(), trunc_finalizeA<<<(nq + 255) / 256, 256, 0, s>>>(ac.ph, nq, ws.S, ws.shiftA, ws.cnt, b.scal,
                                                      eps, ws.atomL, ws.atomLam, ws.atomJ,
-                                                     ws.atomD, ws.cntd, ws.emptyd, ws.flagged);
-    trunc_exact_fallback<<<64, 256, 0, s>>>(ac.ph, tc.pc, tc.perm_c, tc.cell_start, g, b.psi, eps,
+                                                     ws.atomD, ws.cntd, ws.emptyd, ws.flagged));
+    (note_launch(), trunc_exact_fallback<<<64, 256, 0, s>>>(ac.ph, tc.pc, tc.perm_c, tc.cell_start, g, b.psi, eps,
                                             r2, r_scan, b.scal, ws.flagged, ws.atomL,
-                                            ws.atomLam, ws.atomJ, ws.atomD);
+                                            ws.atomLam, ws.atomJ, ws.atomD));
     const int nb_near = std::min(4 * 148, (nq + 255) / 256 * 8 + 1);
     if (dbg)
-      trunc_nearest_empty<true><<<nb_near, 256, 0, s>>>(ac.ph, nq, ws.cnt, tc.pc, tc.perm_c,
+      (note_launch(), trunc_nearest_empty<true><<<nb_near, 256, 0, s>>>(ac.ph, nq, ws.cnt, tc.pc, tc.perm_c,
                                                         tc.cell_start, g, b.psi, eps, ws.atomL,
-                                                        ws.atomJ, ws.atomD, ws.empty_fp, ws.hash);
+                                                        ws.atomJ, ws.atomD, ws.empty_fp, ws.hash));
     else
-      trunc_nearest_empty<false><<<nb_near, 256, 0, s>>>(ac.ph, nq, ws.cnt, tc.pc, tc.perm_c,
+      (note_launch(), trunc_nearest_empty<false><<<nb_near, 256, 0, s>>>(ac.ph, nq, ws.cnt, tc.pc, tc.perm_c,
                                                          tc.cell_start, g, b.psi, eps, ws.atomL,
-                                                         ws.atomJ, ws.atomD, ws.empty_fp, ws.hash);
-    gather_d_kernel<<<(nq + 255) / 256, 256, 0, s>>>(ws.atomLam, ac.c2h, nq, ws.lamc);
+                                                         ws.atomJ, ws.atomD, ws.empty_fp, ws.hash));
+    (note_launch(), gather_d_kernel<<<(nq + 255) / 256, 256, 0, s>>>(ws.atomLam, ac.c2h, nq, ws.lamc));
     if (b.timing) cudaEventRecord(b.timing[3], s);
     if (scan)
-      trunc_passB<<<(n + kT - 1) / kT, kT, 0, s>>>(tc.ph, ws.b2h, n, ac.pc, ws.lamc,
-                                                   ac.cell_start, g, c2, r2, r_scan, ws.G);
+      (note_launch(), trunc_passB<<<(n + kT - 1) / kT, kT, 0, s>>>(tc.ph, ws.b2h, n, ac.pc, ws.lamc,
+                                                   ac.cell_start, g, c2, r2, r_scan, ws.G));
     else
       TCK(cudaMemsetAsync(ws.G, 0, sizeof(double) * n, s));
     if (b.timing) cudaEventRecord(b.timing[4], s);
-    trunc_assemble<<<(n + 255) / 256, 256, 0, s>>>(ws.G, tc.perm_h, n, ws.empty_fp, b.res);
+    (note_launch(), trunc_assemble<<<(n + 255) / 256, 256, 0, s>>>(ws.G, tc.perm_h, n, ws.empty_fp, b.res));
     launch_det_sum(ws.atomJ, nq, ws.red, b.res + n + kResJ, s);
     launch_det_sum(ws.atomD, nq, ws.red + 1024, b.res + n + kResD, s);
     launch_det_sum(ws.cntd, nq, ws.red + 2048, b.res + n + kResPairs, s);
     launch_det_sum(ws.emptyd, nq, ws.red + 3072, b.res + n + kResEmpty, s);
     if (dbg) {
-      cnt_fix_kernel<<<(nq + 255) / 256, 256, 0, s>>>(ws.cnt, nq, reinterpret_cast<uint32_t*>(ws.S));
-      scatter_debug<uint32_t><<<(nq + 255) / 256, 256, 0, s>>>(
-          reinterpret_cast<uint32_t*>(ws.S), ac.perm_h, nq, dbg->count);
-      scatter_debug<unsigned long long><<<(nq + 255) / 256, 256, 0, s>>>(
+      (note_launch(), cnt_fix_kernel<<<(nq + 255) / 256, 256, 0, s>>>(ws.cnt, nq, reinterpret_cast<uint32_t*>(ws.S)));
+      (note_launch(), scatter_debug<uint32_t><<<(nq + 255) / 256, 256, 0, s>>>(
+          reinterpret_cast<uint32_t*>(ws.S), ac.perm_h, nq, dbg->count));
+      (note_launch(), scatter_debug<unsigned long long><<<(nq + 255) / 256, 256, 0, s>>>(
           reinterpret_cast<unsigned long long*>(ws.hash), ac.perm_h, nq,
-          reinterpret_cast<unsigned long long*>(dbg->hash));
-      scatter_debug<double><<<(nq + 255) / 256, 256, 0, s>>>(ws.atomL, ac.perm_h, nq, dbg->log_s);
+          reinterpret_cast<unsigned long long*>(dbg->hash)));
+      (note_launch(), scatter_debug<double><<<(nq + 255) / 256, 256, 0, s>>>(ws.atomL, ac.perm_h, nq, dbg->log_s));
     }
   } else {
     TCK(cudaMemsetAsync(b.res, 0, sizeof(double) * (n + kResTail), s));
   }
-  set_visited<<<1, 1, 0, s>>>(b.res, n, static_cast<double>(nq));
+  (note_launch(), set_visited<<<1, 1, 0, s>>>(b.res, n, static_cast<double>(nq)));
   TCK(cudaGetLastError());
   return 0;
 }
@@ -1048,8 +1048,8 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
 void launch_dense_debug(const DeviceAtoms& a, const DeviceTargets& t, const EvalBuffers& b,
                         const DebugOut& dbg, cudaStream_t s) {
   if (a.nq == 0) return;
-  dense_debug_kernel<<<std::min(1024, (a.nq + 255) / 256), 256, 0, s>>>(
-      b.atomL, a.nq, t.n, dbg.count, dbg.hash, dbg.log_s);
+  (note_launch(), dense_debug_kernel<<<std::min(1024, (a.nq + 255) / 256), 256, 0, s>>>(
+      b.atomL, a.nq, t.n, dbg.count, dbg.hash, dbg.log_s));
 }
 
 int run_nearest_points(TruncWorkspace& ws, const DeviceTargets& t, TargetCells& tc,
@@ -1064,9 +1064,9 @@ int run_nearest_points(TruncWorkspace& ws, const DeviceTargets& t, TargetCells& 
     ws.pts_cap = 3 * m;
   }
   TCK(cudaMemcpyAsync(ws.pts, xyz_host, sizeof(double) * 3 * m, cudaMemcpyHostToDevice, s));
-  nearest_points_kernel<<<static_cast<int>(std::min<size_t>(1024, (m + 7) / 8)), 256, 0, s>>>(
+  (note_launch(), nearest_points_kernel<<<static_cast<int>(std::min<size_t>(1024, (m + 7) / 8)), 256, 0, s>>>(
       ws.pts, static_cast<int>(m), tc.pc, tc.perm_c, tc.cell_start, to_dev(tc.g), ws.near_out,
-      nullptr);
+      nullptr));
   TCK(cudaMemcpyAsync(out_host, ws.near_out, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost, s));
   TCK(cudaStreamSynchronize(s));
   return 0;
@@ -1088,10 +1088,10 @@ int run_covering_cost(TruncWorkspace& ws, const DeviceAtoms& a, const DeviceTarg
   TCK(cudaMalloc(&d2, sizeof(double) * m));
   TCK(cudaMalloc(&idx, sizeof(unsigned long long) * m));
   TCK(cudaMalloc(&dres, sizeof(double)));
-  atoms_to_pts<<<(a.nq + 255) / 256, 256, 0, s>>>(a.x, a.nq, pts);
-  nearest_points_kernel<<<static_cast<int>(std::min<size_t>(4096, (m + 7) / 8)), 256, 0, s>>>(
-      pts, a.nq, tc.pc, tc.perm_c, tc.cell_start, to_dev(tc.g), idx, d2);
-  max_cost_kernel<<<1, 256, 0, s>>>(d2, a.nq, dres);
+  (note_launch(), atoms_to_pts<<<(a.nq + 255) / 256, 256, 0, s>>>(a.x, a.nq, pts));
+  (note_launch(), nearest_points_kernel<<<static_cast<int>(std::min<size_t>(4096, (m + 7) / 8)), 256, 0, s>>>(
+      pts, a.nq, tc.pc, tc.perm_c, tc.cell_start, to_dev(tc.g), idx, d2));
+  (note_launch(), max_cost_kernel<<<1, 256, 0, s>>>(d2, a.nq, dres));
   TCK(cudaMemcpyAsync(out, dres, sizeof(double), cudaMemcpyDeviceToHost, s));
   TCK(cudaStreamSynchronize(s));
   cudaFree(pts);

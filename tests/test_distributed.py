@@ -1,0 +1,74 @@
+"""world_size-2 gloo test of the multi-GPU host logic on CPU.
+
+The B200 path shards atoms contiguously (rsot_cuda_shard_range), evaluates
+each shard, allreduces the packed partial buffer [g + nu | J + sum psi nu |
+D | pairs | empty | visited] and finalises once.  Here the
+shard evaluation is the CPU oracle, the collective is gloo, and the
+result must equal the single-process evaluation."""
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import random_instance
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cutoff, q):
+    import ctypes
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle.oracle import COracle
+    from paper_2507_23602_b200 import _lib
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(77)
+    A, M, T, W, psi = random_instance(rng, 3, 300, 2001, 0.05)
+    lib = _lib.load()
+    lo, hi = ctypes.c_size_t(), ctypes.c_size_t()
+    lib.rsot_cuda_shard_range(len(A), rank, world, ctypes.byref(lo), ctypes.byref(hi))
+    C = COracle()
+    part = C.evaluate_dual(A[lo.value:hi.value], M[lo.value:hi.value], T, W, psi, 0.02, cutoff)
+    psinu = float(np.sum(psi * W))
+    # un-finalise the shard result into the packed partial buffer
+    buf = np.concatenate([part["gradient"] + W, [part["J"] + psinu, part["D"], part["candidate_pairs"],
+                                                  part["empty_candidate_atoms"], part["atoms_visited"]]])
+    t = torch.from_numpy(buf)
+    dist.all_reduce(t)
+    red = t.numpy()
+    n = len(W)
+    g = red[:n] - W
+    J = red[n] - psinu
+    full = C.evaluate_dual(A, M, T, W, psi, 0.02, cutoff)
+    ok = (abs(J - full["J"]) <= 1e-12 * abs(full["J"]) and np.max(np.abs(g - full["gradient"])) <= 1e-14
+          and abs(red[n + 1] - full["D"]) <= 1e-12 * full["D"] and int(red[n + 2]) == full["candidate_pairs"]
+          and int(red[n + 3]) == full["empty_candidate_atoms"] and int(red[n + 4]) == len(A))
+    q.put((rank, bool(ok)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cutoff", [math.inf, 0.01])
+def test_two_rank_shard_allreduce_matches_single(cutoff):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, cutoff, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(res) == [(0, True), (1, True)]

@@ -1,0 +1,249 @@
+"""GPU parity tests: the sm_100a evaluator through the C ABI
+(include/rsot_cuda.h via paper_2507_23602_b200) against the CPU oracle and
+the golden vectors of the reference library.
+
+Tolerance (fp64, SURVEY.md §8d / north star): |dJ| <= 1e-10 |J|,
+||dg||_inf <= 1e-10 * max_k(nu~_k + nu_k), |dD| <= 1e-10 D; counters and
+per-atom candidate sets (size + hash) exact."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import assert_parity, load_golden, marginal_scale, random_instance
+import paper_2507_23602_b200 as rs
+from paper_2507_23602_b200 import _lib, synth
+from oracle.oracle import COracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+C = COracle()
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return rs.Context.default(0)
+
+
+def gpu_eval(ctx, A, M, T, W, psi, eps, cutoff, dim=3):
+    atoms = rs.SourceAtoms(dim=dim, points=A, masses=M)
+    tgt = rs.TargetMeasure(dim=dim, points=T, weights=W)
+    r = rs.evaluate_dual(atoms, tgt, rs.DualPotential(psi), rs.SolverConfig(epsilon=eps),
+                         rs.TruncationState(cutoff=cutoff), ctx=ctx)
+    return dict(J=r.J, D=r.D, gradient=r.gradient, atoms_visited=r.atoms_visited,
+                candidate_pairs=r.candidate_pairs, empty_candidate_atoms=r.empty_candidate_atoms)
+
+
+def test_loaded_native_library(ctx):
+    lib = _lib.load()
+    assert lib.rsot_cuda_ctx_num_sms(ctx.handle) >= 100
+
+
+# ---- reference frozen tests (proj/tests/test_core.cpp) through the API ----
+
+def test_frozen_2x2_values(ctx):
+    A = np.array([[0.0, 0, 0], [1.0, 0, 0]])
+    r = gpu_eval(ctx, A, np.array([0.5, 0.5]), A.copy(), np.array([0.75, 0.25]), np.zeros(2), 1.0, math.inf)
+    assert r["J"] == pytest.approx(-0.226625130922122, rel=1e-12)
+    assert r["gradient"][0] == pytest.approx(-0.011418450214431, rel=1e-10)
+    assert r["gradient"][1] == pytest.approx(+0.011418450214431, rel=1e-10)
+
+
+def test_symmetric_instance_zero_gradient(ctx):
+    A = np.array([[0.0, 0, 0], [1.0, 0, 0]])
+    r = gpu_eval(ctx, A, np.array([0.5, 0.5]), A.copy(), np.array([0.5, 0.5]), np.zeros(2), 1.0, math.inf)
+    assert np.all(np.abs(r["gradient"]) <= 1e-15)
+
+
+def test_single_target_short_circuit(ctx):
+    xs = (np.arange(16) + 0.5) / 16
+    A = np.zeros((16, 3))
+    A[:, 0] = xs
+    M = np.full(16, 1 / 16)
+    T = np.array([[0.4, 0, 0]])
+    expected = -np.sum(0.5 * (xs - 0.4) ** 2 * M)
+    for shift in (0.0, -3.0, 11.0):
+        r = gpu_eval(ctx, A, M, T, np.array([1.0]), np.array([shift]), 0.5, math.inf)
+        assert r["J"] == pytest.approx(expected, rel=1e-12)
+        assert abs(r["gradient"][0]) <= 1e-15
+
+
+def test_input_validation(ctx):
+    atoms = rs.SourceAtoms(dim=1, points=np.array([[0.0, 0, 0], [1.0, 0, 0]]), masses=np.array([.5, .5]))
+    tgt = rs.TargetMeasure(dim=1, points=atoms.points.copy(), weights=np.array([.75, .25]))
+    with pytest.raises(ValueError):
+        rs.evaluate_dual(atoms, tgt, rs.DualPotential(np.zeros(1)), rs.SolverConfig(epsilon=1.0),
+                         rs.TruncationState(), ctx=ctx)
+    with pytest.raises(ValueError):
+        rs.evaluate_dual(atoms, tgt, rs.DualPotential(np.array([np.nan, 0.0])), rs.SolverConfig(epsilon=1.0),
+                         rs.TruncationState(), ctx=ctx)
+    # the C ABI itself also refuses non-finite psi (device-side check)
+    lib = _lib.load()
+    g = np.zeros(2)
+    sc = _lib.RsotCudaScalars()
+    dev_a = rs.rsot._device_atoms(atoms, ctx)
+    dev_t = rs.rsot._device_targets(tgt, ctx)
+    bad = np.array([np.inf, 0.0])
+    rc = lib.rsot_cuda_eval(ctx.handle, dev_a.handle, dev_t.handle, rs.rsot._ptr(bad), 1.0, math.inf,
+                            rs.rsot._ptr(g), sc)
+    assert rc == _lib.RSOT_CUDA_INVALID_ARGUMENT
+    with pytest.raises(ValueError):
+        rs.SpatialIndex(np.zeros((0, 3)), ctx=ctx)
+
+
+def test_gradient_sums_to_zero_gauge_invariance(ctx):
+    rng = np.random.default_rng(31)
+    A, M, T, W, psi = random_instance(rng, 2, 12, 80)
+    base = gpu_eval(ctx, A, M, T, W, psi, 0.25, math.inf, dim=2)
+    assert abs(base["gradient"].sum()) <= 1e-10
+    for c in (1.0, -1.0, 100.0, -100.0):
+        r = gpu_eval(ctx, A, M, T, W, psi + c, 0.25, math.inf, dim=2)
+        assert abs(r["J"] - base["J"]) <= 1e-10
+        assert np.max(np.abs(r["gradient"] - base["gradient"])) <= 1e-10
+
+
+def test_empty_atom_set(ctx):
+    """N_q = 0: J = -sum psi nu, g = -nu (parallel.hpp:16-19 n<2 path)."""
+    rng = np.random.default_rng(3)
+    T = rng.uniform(size=(50, 3))
+    W = np.full(50, 1 / 50)
+    psi = rng.normal(0, 0.1, 50)
+    for cutoff in (math.inf, 0.01):
+        r = gpu_eval(ctx, np.zeros((0, 3)), np.zeros(0), T, W, psi, 0.1, cutoff)
+        want = C.evaluate_dual(np.zeros((0, 3)), np.zeros(0), T, W, psi, 0.1, cutoff)
+        assert r["J"] == pytest.approx(want["J"], rel=1e-14)
+        assert np.allclose(r["gradient"], -W, rtol=0, atol=1e-18)
+        assert r["atoms_visited"] == 0 and r["candidate_pairs"] == 0
+
+
+# ---- golden vectors of the reference library (tests/golden) ---------------
+
+@pytest.mark.parametrize("case", load_golden(), ids=lambda c: c["name"])
+def test_golden_vectors(ctx, case):
+    got = gpu_eval(ctx, case["A"], case["M"], case["T"], case["W"], case["psi"], case["eps"], case["cutoff"],
+                   dim=case["dim"])
+    want = dict(J=case["J"], D=case["D"], gradient=case["g"], atoms_visited=case["counts"][0],
+                candidate_pairs=case["counts"][1], empty_candidate_atoms=case["counts"][2])
+    assert_parity(got, want, marginal_scale(case["W"], case["g"]), TOL)
+
+
+# ---- random instances with per-atom selection parity ----------------------
+
+CASES = [
+    (3, 3000, 400, 0.02, math.inf), (3, 3000, 400, 0.02, 0.01), (3, 3000, 400, 0.02, 0.03),
+    (3, 3000, 400, 0.02, -1.0), (3, 3000, 400, 0.02, 0.0), (3, 3000, 400, 0.02, 0.002),
+    (2, 5000, 300, 0.05, math.inf), (2, 5000, 300, 0.005, 0.004), (1, 700, 50, 0.1, 0.02),
+    (3, 20000, 5000, 1e-3, 0.01), (3, 2, 2, 1.0, math.inf), (3, 100, 1, 0.5, math.inf),
+    (3, 100, 1, 0.5, 0.001), (3, 2000, 300, 1e-4, math.inf), (3, 2000, 3000, 1e-4, 1e-3),
+    (2, 3000, 500, 1e-3, math.inf), (3, 1000, 200, 0.05, 50.0), (3, 129, 257, 0.03, 0.02),
+]
+
+
+@pytest.mark.parametrize("dim,nq,n,eps,cutoff", CASES)
+def test_random_instances_with_selection_parity(ctx, dim, nq, n, eps, cutoff):
+    rng = np.random.default_rng(hash((dim, nq, n, eps, cutoff)) % (2 ** 32))
+    A, M, T, W, psi = random_instance(rng, dim, n, nq, 0.05)
+    atoms = rs.SourceAtoms(dim=dim, points=A, masses=M)
+    tgt = rs.TargetMeasure(dim=dim, points=T, weights=W)
+    res, cnt, hsh, logs = rs.evaluate_dual_debug(atoms, tgt, psi, eps, cutoff, ctx=ctx)
+    want = C.evaluate_dual(A, M, T, W, psi, eps, cutoff, per_atom=True)
+    got = dict(J=res.J, D=res.D, gradient=res.gradient, atoms_visited=res.atoms_visited,
+               candidate_pairs=res.candidate_pairs, empty_candidate_atoms=res.empty_candidate_atoms)
+    assert_parity(got, want, marginal_scale(W, want["gradient"]), TOL)
+    assert np.array_equal(cnt, want["count"])
+    assert np.array_equal(hsh, want["hash"])
+    assert np.max(np.abs(logs - want["log_s"]) / np.maximum(1.0, np.abs(want["log_s"]))) <= 1e-12
+
+
+def test_all_covering_cutoff_equals_dense(ctx):
+    """A finite cutoff covering every target selects every target (same
+    set as dense, evaluate.cpp:119-128)."""
+    rng = np.random.default_rng(8)
+    A, M, T, W, psi = random_instance(rng, 3, 300, 1000, 0.05)
+    d = gpu_eval(ctx, A, M, T, W, psi, 0.05, math.inf)
+    t = gpu_eval(ctx, A, M, T, W, psi, 0.05, 10.0)
+    assert t["candidate_pairs"] == d["candidate_pairs"] == 300 * 1000
+    assert abs(t["J"] - d["J"]) <= 1e-13 * abs(d["J"])
+    assert np.max(np.abs(t["gradient"] - d["gradient"])) <= 1e-14
+
+
+def test_bitwise_determinism(ctx):
+    rng = np.random.default_rng(41)
+    A, M, T, W, psi = random_instance(rng, 3, 2000, 20000, 0.05)
+    for cutoff in (math.inf, 0.005):
+        a = gpu_eval(ctx, A, M, T, W, psi, 0.01, cutoff)
+        b = gpu_eval(ctx, A, M, T, W, psi, 0.01, cutoff)
+        assert a["J"] == b["J"] and a["D"] == b["D"]
+        assert np.array_equal(a["gradient"], b["gradient"])
+
+
+def test_nearest_and_covering_cost(ctx):
+    rng = np.random.default_rng(12)
+    T = rng.uniform(size=(5000, 3))
+    Q = np.vstack([rng.uniform(size=(500, 3)), rng.uniform(-1, 2, size=(100, 3))])
+    idx = rs.SpatialIndex(T, ctx=ctx)
+    got = idx.nearest_many(Q)
+    assert np.array_equal(got, C.nearest(T, Q))
+    assert idx.nearest([5.0, 5.0, 5.0]) == int(np.argmin(((T - 5.0) ** 2).sum(axis=1)))
+    A = rng.uniform(size=(3000, 3))
+    atoms = rs.SourceAtoms(dim=3, points=A, masses=np.full(3000, 1 / 3000))
+    tgt = rs.TargetMeasure(dim=3, points=T, weights=np.full(5000, 1 / 5000))
+    assert rs.covering_cost(atoms, tgt, ctx=ctx) == C.covering_cost(A, T)
+    # worked example (test_geometry.cpp:270-290)
+    a1 = rs.SourceAtoms(dim=1, points=np.array([[0.0, 0, 0], [0.5, 0, 0], [1.0, 0, 0]]),
+                        masses=np.full(3, 1 / 3))
+    t1 = rs.TargetMeasure(dim=1, points=np.array([[0.0, 0, 0], [1.0, 0, 0]]), weights=np.array([.5, .5]))
+    assert rs.covering_cost(a1, t1, ctx=ctx) == pytest.approx(0.125)
+
+
+# ---- BASELINE configs -------------------------------------------------------
+
+def test_cfg1_full_parity(ctx):
+    """cfg1 (2D dense, 16384 x 1024): full-size parity vs the oracle."""
+    p = synth.make("cfg1")
+    psi = p.psi(0)
+    got = gpu_eval(ctx, p.atoms, p.masses, p.targets, p.nu, psi, p.eps, math.inf, dim=2)
+    want = C.evaluate_dual(p.atoms, p.masses, p.targets, p.nu, psi, p.eps, math.inf, workers=8)
+    assert_parity(got, want, marginal_scale(p.nu, want["gradient"]), TOL)
+
+
+@pytest.mark.parametrize("name,count", [("cfg2", 8192), ("cfg3", 4096), ("cfg5", 4096)])
+def test_config_subsample_parity(ctx, name, count):
+    """Seeded atom subsets of the BASELINE configs (full targets) vs the
+    oracle, including per-atom candidate sets for the truncated ones."""
+    p = synth.make(name)
+    psi = p.psi(0)
+    cut = p.cutoff(psi)
+    sub = synth.subsample_atoms(p, count)
+    atoms = rs.SourceAtoms(dim=p.dim, points=sub.atoms, masses=sub.masses)
+    tgt = rs.TargetMeasure(dim=p.dim, points=p.targets, weights=p.nu)
+    res, cnt, hsh, _ = rs.evaluate_dual_debug(atoms, tgt, psi, p.eps, cut, ctx=ctx)
+    want = C.evaluate_dual(sub.atoms, sub.masses, p.targets, p.nu, psi, p.eps, cut, workers=8, per_atom=True)
+    got = dict(J=res.J, D=res.D, gradient=res.gradient, atoms_visited=res.atoms_visited,
+               candidate_pairs=res.candidate_pairs, empty_candidate_atoms=res.empty_candidate_atoms)
+    assert_parity(got, want, marginal_scale(p.nu, want["gradient"]), TOL)
+    assert np.array_equal(cnt, want["count"]) and np.array_equal(hsh, want["hash"])
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg5"])
+def test_full_size_properties(ctx, name):
+    """Full BASELINE sizes: size-independent properties (gradient sums to
+    zero, counters consistent, determinism, J finite)."""
+    p = synth.make(name)
+    atoms = rs.SourceAtoms(dim=p.dim, points=p.atoms, masses=p.masses)
+    tgt = rs.TargetMeasure(dim=p.dim, points=p.targets, weights=p.nu)
+    psi = p.psi(0)
+    cfg = rs.SolverConfig(epsilon=p.eps)
+    tr = rs.TruncationState(cutoff=p.cutoff(psi))
+    r1 = rs.evaluate_dual(atoms, tgt, rs.DualPotential(psi), cfg, tr, ctx=ctx)
+    r2 = rs.evaluate_dual(atoms, tgt, rs.DualPotential(psi), cfg, tr, ctx=ctx)
+    assert r1.J == r2.J and np.array_equal(r1.gradient, r2.gradient)
+    assert abs(r1.gradient.sum()) <= 1e-10
+    assert np.all(r1.gradient >= -p.nu)  # nu~ = g + nu >= 0
+    assert r1.atoms_visited == p.nq
+    if p.truncation == "none":
+        assert r1.candidate_pairs == p.nq * p.n and r1.empty_candidate_atoms == 0
+    else:
+        assert p.nq <= r1.candidate_pairs < p.nq * p.n
+    assert math.isfinite(r1.J) and r1.D > 0

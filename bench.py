@@ -267,7 +267,7 @@ def run_ours(args, rank, world, local_rank):
         ms = float(t.item())
     ms_step = ms / K
     sc = d_sc.cpu().numpy()
-    pairs = float(sc[3])
+    pairs = float(sc[2])  # {J, D, pairs, empty, visited}
 
     # ---- e2e: the C-ABI call with pinned host psi / host g, copies inside ----
     h_psi = torch.empty((K, n), dtype=torch.float64).pin_memory()

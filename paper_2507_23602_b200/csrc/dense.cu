@@ -102,8 +102,8 @@ __global__ void prologue_final(const double* __restrict__ part, int nblk,
 template <int APT, bool WIDE>
 __device__ __forceinline__ void passA_tile(const double4* __restrict__ tile, int cnt,
                                            const double (&X)[APT][3], const double (&sub)[APT],
-                                           double (&S)[APT], const double* __restrict__ tbl) {
-#pragma unroll 2
+                                           double (&S)[APT], const int2* __restrict__ tbl) {
+#pragma unroll 4
   for (int t = 0; t < cnt; ++t) {
     const double4 y = tile[t];
 #pragma unroll
@@ -122,7 +122,7 @@ dense_passA(const double4* __restrict__ atoms, int nq,
             int n, int per_split, const double* __restrict__ scal, double c2,
             double* __restrict__ partS, double* __restrict__ shiftA) {
   __shared__ double4 tile[kTile];
-  __shared__ double tbl[16];
+  __shared__ int2 tbl[16];
   __shared__ double sh[200];
   load_exp2_table(tbl);
 
@@ -281,7 +281,7 @@ dense_passB(const double4* __restrict__ atoms, const double* __restrict__ atomLa
             const double* __restrict__ b2, int n, double c2,
             double* __restrict__ partG) {
   __shared__ double4 tile[kTile];
-  __shared__ double tbl[16];
+  __shared__ int2 tbl[16];
   __shared__ double sh[200];
   load_exp2_table(tbl);
 
@@ -326,7 +326,7 @@ dense_passB(const double4* __restrict__ atoms, const double* __restrict__ atomLa
       tile[t] = make_double4(c2x2 * x0, c2x2 * x1, c2x2 * x2, A);
     }
     __syncthreads();
-#pragma unroll 2
+#pragma unroll 4
     for (int t = 0; t < cnt; ++t) {
       const double4 X = tile[t];
 #pragma unroll
@@ -422,14 +422,14 @@ DenseLaunch plan_dense(int nq, int n, int num_sms) {
   // Enough CTAs for ~16 waves of ~6 resident CTAs per SM, while keeping
   // at least 512 targets (pass A) / 1024 atoms (pass B) per CTA.
   const long want = 16L * num_sms * 6;
-  p.apt = (nq >= 64L * 256 * num_sms) ? 2 : 1;
+  p.apt = (nq >= 2L * 256 * num_sms) ? 2 : 1;
   const long ablocks = (nq + kThreads * p.apt - 1) / (kThreads * p.apt);
   long sa = (want + ablocks - 1) / ablocks;
   long max_sa = (n + 511) / 512;
   if (sa > max_sa) sa = max_sa;
   if (sa < 1) sa = 1;
   p.splitsA = static_cast<int>(sa);
-  p.tpt = (n >= 4L * 256 * num_sms) ? 2 : 1;
+  p.tpt = (n >= 16L * 256) ? 2 : 1;
   const long tblocks = (n + kThreads * p.tpt - 1) / (kThreads * p.tpt);
   long sb = (want + tblocks - 1) / tblocks;
   long max_sb = (nq + 1023) / 1024;

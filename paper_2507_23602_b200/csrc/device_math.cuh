@@ -27,14 +27,16 @@ constexpr double kLn2 = 0.69314718055994530942;    // 0x1.62e42fefa39efp-1
 // the low mantissa bits.
 constexpr double kExpMagic = 0x1.8p48;
 
-// 2^(i/16), correctly rounded (mpmath, 200 bits).
-__device__ __constant__ double kExp2Table[16] = {
-    0x1.0000000000000p+0, 0x1.0b5586cf9890fp+0, 0x1.172b83c7d517bp+0,
-    0x1.2387a6e756238p+0, 0x1.306fe0a31b715p+0, 0x1.3dea64c123422p+0,
-    0x1.4bfdad5362a27p+0, 0x1.5ab07dd485429p+0, 0x1.6a09e667f3bcdp+0,
-    0x1.7a11473eb0187p+0, 0x1.8ace5422aa0dbp+0, 0x1.9c49182a3f090p+0,
-    0x1.ae89f995ad3adp+0, 0x1.c199bdd85529cp+0, 0x1.d5818dcfba487p+0,
-    0x1.ea4afa2a490dap+0};
+// 2^(i/16) correctly rounded (mpmath, 200 bits), stored as {lo, hi - (i<<16)}
+// so that the scale 2^k * 2^(i/16) for n = 16k + i is the double with words
+// {lo, hi' + (n << 16)}: one IMAD instead of split/shift/add.
+__device__ __constant__ int2 kExp2Table[16] = {
+    {0x00000000, 0x3ff00000}, {0x6cf9890f, 0x3fefb558}, {0x3c7d517b, 0x3fef72b8},
+    {0x6e756238, 0x3fef387a}, {0x0a31b715, 0x3fef06fe}, {0x4c123422, 0x3feedea6},
+    {(int)0xd5362a27, 0x3feebfda}, {(int)0xdd485429, 0x3feeab07}, {0x667f3bcd, 0x3feea09e},
+    {0x73eb0187, 0x3feea114}, {0x422aa0db, 0x3feeace5}, {(int)0x82a3f090, 0x3feec491},
+    {(int)0x995ad3ad, 0x3feee89f}, {(int)0xdd85529c, 0x3fef199b}, {(int)0xdcfba487, 0x3fef5818},
+    {(int)0xa2a490da, 0x3fefa4af}};
 
 // Near-minimax degree-5 fit of 2^r on [-1/32, 1/32] (mpmath chebyfit),
 // coefficients rounded to double; worst relative error 4.61e-15.
@@ -45,21 +47,22 @@ constexpr double kP2 = 0x1.ebfbdff555824p-3;
 constexpr double kP1 = 0x1.62e42fefa39f3p-1;
 constexpr double kP0 = 0x1.0000000000014p+0;
 
-// Copies the exp2 table into shared memory (16 doubles = 128 B: a
-// half-warp LDS.64 with any index pattern is one conflict-free wavefront).
-__device__ __forceinline__ void load_exp2_table(double* smem_tbl) {
+// Copies the exp2 table into shared memory (16 x 8 B = 128 B: a half-warp
+// LDS.64 with any index pattern is one conflict-free wavefront).
+__device__ __forceinline__ void load_exp2_table(int2* smem_tbl) {
   if (threadIdx.x < 16) smem_tbl[threadIdx.x] = kExp2Table[threadIdx.x];
 }
 
-// acc + 2^s.  Valid for s in [-1020, 1020]; s below -1020 contributes 0
-// (the contribution is < 2^-1020 and is dropped, the reference would add a
-// subnormal); s above 1020 yields +inf, which the callers detect and route
-// to the exact per-atom path (exponents are taken relative to an upper
-// bound, so this only happens for pathological inputs).
+// acc + 2^s.  Exact split s = n/16 + r (|r| <= 1/32) by the magic-constant
+// addition, 2^r by the polynomial, 2^(n/16) by table + exponent add.  n is
+// clamped to [-16320, 16000]: s below -1020 contributes at most 2^-1019
+// (the reference would add a subnormal or zero); s above 1000 yields at least
+// 2^999, which the callers detect (sum > 2^960) and route to the exact
+// per-atom path.  FP64 pipe: 3 DADD + 6 DFMA; INT: 2 IMNMX, LOP3, LEA, IMAD.
 __device__ __forceinline__ double exp2_acc(double s, double acc,
-                                           const double* __restrict__ tbl) {
+                                           const int2* __restrict__ tbl) {
   const double kk = __dadd_rn(s, kExpMagic);
-  const int n = __double2loint(kk);          // round(16 s)
+  const int n = min(max(__double2loint(kk), -16320), 16000);  // round(16 s)
   const double kd = __dadd_rn(kk, -kExpMagic);
   const double r = __dadd_rn(s, -kd);        // |r| <= 1/32
   double p = fma(kP5, r, kP4);
@@ -67,15 +70,9 @@ __device__ __forceinline__ double exp2_acc(double s, double acc,
   p = fma(p, r, kP2);
   p = fma(p, r, kP1);
   p = fma(p, r, kP0);
-  const int k = n >> 4;                      // floor division by 16
-  const double t = tbl[n & 15];
-  int hi = __double2hiint(t) + static_cast<int>(static_cast<unsigned>(k) << 20);
-  int lo = __double2loint(t);
-  hi = (k < -1020) ? 0 : hi;                 // flush tiny contributions
-  lo = (k < -1020) ? 0 : lo;
-  hi = (k > 1020) ? 0x7ff00000 : hi;         // overflow -> +inf (the caller
-  lo = (k > 1020) ? 0 : lo;                  // flags the atom for the exact path)
-  return fma(p, __hiloint2double(hi, lo), acc);
+  const int2 t = tbl[n & 15];
+  const double scale = __hiloint2double(t.y + n * 65536, t.x);
+  return fma(p, scale, acc);
 }
 
 // Exact reference predicate (point.hpp:35-40, spatial_index.cpp:54):

@@ -263,7 +263,7 @@ trunc_passA(const double4* __restrict__ xs, int nq,
   __shared__ int tK[kTileT];
   __shared__ int rowStart[kT];
   __shared__ int rowPref[kT + 1];
-  __shared__ double tbl[16];
+  __shared__ int2 tbl[16];
   __shared__ double sh[200];
   __shared__ int shi[40];
   load_exp2_table(tbl);
@@ -585,7 +585,7 @@ trunc_passB(const double4* __restrict__ ys, const double* __restrict__ b2s, int 
   __shared__ int tK[kTileT];
   __shared__ int rowStart[kT];
   __shared__ int rowPref[kT + 1];
-  __shared__ double tbl[16];
+  __shared__ int2 tbl[16];
   __shared__ double sh[200];
   __shared__ int shi[40];
   load_exp2_table(tbl);

@@ -66,7 +66,9 @@ def test_single_target_short_circuit(ctx):
     for shift in (0.0, -3.0, 11.0):
         r = gpu_eval(ctx, A, M, T, np.array([1.0]), np.array([shift]), 0.5, math.inf)
         assert r["J"] == pytest.approx(expected, rel=1e-12)
-        assert abs(r["gradient"][0]) <= 1e-15
+        # reference: doctest::Approx(0.0) (tolerance 1.2e-5); our exp2 is
+        # within a few ulp of 1 for the single target
+        assert abs(r["gradient"][0]) <= 1e-13
 
 
 def test_input_validation(ctx):

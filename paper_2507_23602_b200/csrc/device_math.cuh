@@ -75,6 +75,25 @@ __device__ __forceinline__ double exp2_acc(double s, double acc,
   return fma(p, scale, acc);
 }
 
+// acc + (take ? 2^s : 0) without a branch (the scale is zeroed on the INT
+// pipe for lanes that do not take the pair).
+__device__ __forceinline__ double exp2_acc_masked(double s, double acc,
+                                                  const int2* __restrict__ tbl, bool take) {
+  const double kk = __dadd_rn(s, kExpMagic);
+  const int n = min(max(__double2loint(kk), -16320), 16000);
+  const double kd = __dadd_rn(kk, -kExpMagic);
+  const double r = __dadd_rn(s, -kd);
+  double p = fma(kP5, r, kP4);
+  p = fma(p, r, kP3);
+  p = fma(p, r, kP2);
+  p = fma(p, r, kP1);
+  p = fma(p, r, kP0);
+  const int2 t = tbl[n & 15];
+  const int hi = take ? t.y + n * 65536 : 0;
+  const int lo = take ? t.x : 0;
+  return fma(p, __hiloint2double(hi, lo), acc);
+}
+
 // Exact reference predicate (point.hpp:35-40, spatial_index.cpp:54):
 // ((dx*dx + dy*dy) + dz*dz) < r2, every operation rounded separately.
 __device__ __forceinline__ bool exact_inside(double x0, double x1, double x2,

@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "block_util.cuh"
@@ -38,7 +39,7 @@ namespace {
 constexpr int kT = 128;        // threads per CTA = points per chunk
 constexpr int kTileT = 256;    // staged points per tile
 constexpr int kMortonBits = 7; // per dim, position inside a cell
-constexpr double kCellsPerRadius = 2.0;  // grid cell side ~ r / 2
+double g_cells_per_radius = 3.0;  // grid cell side ~ r / 3 (env RSOT_CELLS_PER_RADIUS)
 
 struct GridDev {
   double lo[3];
@@ -246,6 +247,56 @@ __device__ __forceinline__ int find_row(const int* pref, int s) {
   return lo;
 }
 
+// Warp bounding box (local fp32 coordinates) of the warp's own points.
+struct WarpBox {
+  float lo0, lo1, lo2, hi0, hi1, hi2;
+};
+
+__device__ __forceinline__ WarpBox warp_box(bool valid, float a, float b, float c) {
+  WarpBox w;
+  w.lo0 = valid ? a : INFINITY; w.hi0 = valid ? a : -INFINITY;
+  w.lo1 = valid ? b : INFINITY; w.hi1 = valid ? b : -INFINITY;
+  w.lo2 = valid ? c : INFINITY; w.hi2 = valid ? c : -INFINITY;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    w.lo0 = fminf(w.lo0, __shfl_xor_sync(0xffffffffu, w.lo0, o));
+    w.lo1 = fminf(w.lo1, __shfl_xor_sync(0xffffffffu, w.lo1, o));
+    w.lo2 = fminf(w.lo2, __shfl_xor_sync(0xffffffffu, w.lo2, o));
+    w.hi0 = fmaxf(w.hi0, __shfl_xor_sync(0xffffffffu, w.hi0, o));
+    w.hi1 = fmaxf(w.hi1, __shfl_xor_sync(0xffffffffu, w.hi1, o));
+    w.hi2 = fmaxf(w.hi2, __shfl_xor_sync(0xffffffffu, w.hi2, o));
+  }
+  return w;
+}
+
+// Compacts the indices of the staged points of a tile that can be within
+// the (conservative) FP32 threshold of ANY point of the warp's box into the
+// warp's list; returns the list length.  Never drops a point some lane
+// would accept or send to the exact test: for x in the box the box distance
+// is <= |x - y| (the threshold carries a relative margin for rounding).
+__device__ __forceinline__ int warp_cull(const float4* __restrict__ tF, int cnt, const WarpBox& w,
+                                         float thr, unsigned char* __restrict__ list) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  int nsel = 0;
+  for (int g = 0; g < cnt; g += 32) {
+    const int t = g + lane;
+    bool keep = false;
+    if (t < cnt) {
+      const float4 y = tF[t];
+      const float dx = fmaxf(fmaxf(w.lo0 - y.x, y.x - w.hi0), 0.f);
+      const float dy = fmaxf(fmaxf(w.lo1 - y.y, y.y - w.hi1), 0.f);
+      const float dz = fmaxf(fmaxf(w.lo2 - y.z, y.z - w.hi2), 0.f);
+      keep = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= thr;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (keep) list[nsel + __popc(m & lt)] = static_cast<unsigned char>(t);
+    nsel += __popc(m);
+  }
+  __syncwarp();
+  return nsel;
+}
+
 // ---------------------------------------------------------------------------
 // Pass A: atom-major truncated LSE.
 
@@ -266,6 +317,7 @@ trunc_passA(const double4* __restrict__ xs, int nq,
   __shared__ int2 tbl[16];
   __shared__ double sh[200];
   __shared__ int shi[40];
+  __shared__ unsigned char wlist[kT / 32][kTileT];
   load_exp2_table(tbl);
 
   const int q = blockIdx.x * kT + threadIdx.x;
@@ -287,6 +339,9 @@ trunc_passA(const double4* __restrict__ xs, int nq,
   const double xsq = c2 * fma(x2, x2, fma(x1, x1, x0 * x0));
   // Spread chunk: carry the per-atom shift in every exponent (see dense.cu).
   const bool wide = R.wide;
+  const WarpBox wb = warp_box(valid, xf0, xf1, xf2);
+  const float cull_thr = R.hi_thr * 1.0001f;
+  unsigned char* const mylist = wlist[threadIdx.x >> 5];
   const double B = scal[kSlotB];
   double S = 0.0;
   uint32_t cnt = 0;
@@ -319,22 +374,52 @@ trunc_passA(const double4* __restrict__ xs, int nq,
         tK[t] = k;
       }
       __syncthreads();
-      for (int t = 0; t < cntT; ++t) {
-        const float4 yf = tF[t];
-        const float dx = xf0 - yf.x, dy = xf1 - yf.y, dz = xf2 - yf.z;
-        const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        bool in = d2 < R.lo_thr;
-        if (!in && d2 <= R.hi_thr) {
-          const double4 yg = ys[tK[t]];
-          in = exact_inside(xa.x, xa.y, xa.z, yg.x, yg.y, yg.z, r2);
+      const int nsel = warp_cull(tF, cntT, wb, cull_thr, mylist);
+      // Two list items per step: the selection is resolved per lane (FP32
+      // test; exact fp64 reference predicate only inside the error band),
+      // then the exponentials run branch-free for the whole warp with the
+      // accumulation masked per lane, so there is no divergent code and
+      // the two items' FP64 chains interleave.
+      for (int i = 0; i < nsel; i += 2) {
+        const int t0 = mylist[i];
+        const int t1 = (i + 1 < nsel) ? mylist[i + 1] : t0;
+        const bool has1 = i + 1 < nsel;
+        const float4 ya = tF[t0];
+        const float4 yb = tF[t1];
+        const float ax = xf0 - ya.x, ay = xf1 - ya.y, az = xf2 - ya.z;
+        const float bx = xf0 - yb.x, by = xf1 - yb.y, bz = xf2 - yb.z;
+        const float d2a = fmaf(az, az, fmaf(ay, ay, ax * ax));
+        const float d2b = fmaf(bz, bz, fmaf(by, by, bx * bx));
+        bool in0 = d2a < R.lo_thr;
+        bool in1 = has1 && d2b < R.lo_thr;
+        const bool bd0 = !in0 && d2a <= R.hi_thr;
+        const bool bd1 = has1 && !in1 && d2b <= R.hi_thr;
+        if (__any_sync(0xffffffffu, bd0 || bd1)) {
+          if (bd0) {
+            const double4 yg = ys[tK[t0]];
+            in0 = exact_inside(xa.x, xa.y, xa.z, yg.x, yg.y, yg.z, r2);
+          }
+          if (bd1) {
+            const double4 yg = ys[tK[t1]];
+            in1 = exact_inside(xa.x, xa.y, xa.z, yg.x, yg.y, yg.z, r2);
+          }
         }
-        if (in) {
-          const double4 y = tD[t];
-          double s = fma(X0, y.x, fma(X1, y.y, fma(X2, y.z, y.w)));
-          if (wide) s -= xsq;
-          S = exp2_acc(s, S, tbl);
-          ++cnt;
-          if (DEBUG) hash += candidate_hash_term(static_cast<uint64_t>(tperm[tK[t]]));
+        if (__any_sync(0xffffffffu, in0 || in1)) {
+          const double4 y0 = tD[t0];
+          const double4 y1 = tD[t1];
+          double s0 = fma(X0, y0.x, fma(X1, y0.y, fma(X2, y0.z, y0.w)));
+          double s1 = fma(X0, y1.x, fma(X1, y1.y, fma(X2, y1.z, y1.w)));
+          if (wide) {
+            s0 -= xsq;
+            s1 -= xsq;
+          }
+          S = exp2_acc_masked(s0, S, tbl, in0);
+          S = exp2_acc_masked(s1, S, tbl, in1);
+          cnt += static_cast<uint32_t>(in0) + static_cast<uint32_t>(in1);
+          if (DEBUG) {
+            if (in0) hash += candidate_hash_term(static_cast<uint64_t>(tperm[tK[t0]]));
+            if (in1) hash += candidate_hash_term(static_cast<uint64_t>(tperm[tK[t1]]));
+          }
         }
       }
     }
@@ -588,6 +673,7 @@ trunc_passB(const double4* __restrict__ ys, const double* __restrict__ b2s, int 
   __shared__ int2 tbl[16];
   __shared__ double sh[200];
   __shared__ int shi[40];
+  __shared__ unsigned char wlist[kT / 32][kTileT];
   load_exp2_table(tbl);
 
   const int j = blockIdx.x * kT + threadIdx.x;
@@ -607,6 +693,9 @@ trunc_passB(const double4* __restrict__ ys, const double* __restrict__ b2s, int 
   const float yf2 = valid ? static_cast<float>(y2) : 1e30f;
   const double T = valid ? fmax(fma(-c2, fma(y2, y2, fma(y1, y1, y0 * y0)), b2s[j]), -1.0e5) : -1.0e5;
   double G = 0.0;
+  const WarpBox wb = warp_box(valid, yf0, yf1, yf2);
+  const float cull_thr = R.hi_thr * 1.0001f;
+  unsigned char* const mylist = wlist[threadIdx.x >> 5];
 
   const int ny = R.c_hi[1] - R.c_lo[1] + 1;
   const int nrows = ny * (R.c_hi[2] - R.c_lo[2] + 1);
@@ -636,19 +725,38 @@ trunc_passB(const double4* __restrict__ ys, const double* __restrict__ b2s, int 
         tK[t] = k;
       }
       __syncthreads();
-      for (int t = 0; t < cntT; ++t) {
-        const float4 xf = tF[t];
-        const float dx = xf.x - yf0, dy = xf.y - yf1, dz = xf.z - yf2;
-        const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        bool in = d2 < R.lo_thr;
-        if (!in && d2 <= R.hi_thr) {
-          const double4 xg = xs[tK[t]];
-          in = exact_inside(xg.x, xg.y, xg.z, yg.x, yg.y, yg.z, r2);
+      const int nsel = warp_cull(tF, cntT, wb, cull_thr, mylist);
+      for (int i = 0; i < nsel; i += 2) {  // see pass A
+        const int t0 = mylist[i];
+        const int t1 = (i + 1 < nsel) ? mylist[i + 1] : t0;
+        const bool has1 = i + 1 < nsel;
+        const float4 xa = tF[t0];
+        const float4 xb = tF[t1];
+        const float ax = xa.x - yf0, ay = xa.y - yf1, az = xa.z - yf2;
+        const float bx = xb.x - yf0, by = xb.y - yf1, bz = xb.z - yf2;
+        const float d2a = fmaf(az, az, fmaf(ay, ay, ax * ax));
+        const float d2b = fmaf(bz, bz, fmaf(by, by, bx * bx));
+        bool in0 = d2a < R.lo_thr;
+        bool in1 = has1 && d2b < R.lo_thr;
+        const bool bd0 = !in0 && d2a <= R.hi_thr;
+        const bool bd1 = has1 && !in1 && d2b <= R.hi_thr;
+        if (__any_sync(0xffffffffu, bd0 || bd1)) {
+          if (bd0) {
+            const double4 xg = xs[tK[t0]];
+            in0 = exact_inside(xg.x, xg.y, xg.z, yg.x, yg.y, yg.z, r2);
+          }
+          if (bd1) {
+            const double4 xg = xs[tK[t1]];
+            in1 = exact_inside(xg.x, xg.y, xg.z, yg.x, yg.y, yg.z, r2);
+          }
         }
-        if (in) {
-          const double4 X = tD[t];
-          const double s = fma(X.x, y0, fma(X.y, y1, fma(X.z, y2, T + X.w)));
-          G = exp2_acc(s, G, tbl);
+        if (__any_sync(0xffffffffu, in0 || in1)) {
+          const double4 Xa = tD[t0];
+          const double4 Xb = tD[t1];
+          const double s0 = fma(Xa.x, y0, fma(Xa.y, y1, fma(Xa.z, y2, T + Xa.w)));
+          const double s1 = fma(Xb.x, y0, fma(Xb.y, y1, fma(Xb.z, y2, T + Xb.w)));
+          G = exp2_acc_masked(s0, G, tbl, in0);
+          G = exp2_acc_masked(s1, G, tbl, in1);
         }
       }
     }
@@ -738,6 +846,15 @@ __global__ void max_cost_kernel(const double* __restrict__ d2, int m, double* __
   if (threadIdx.x == 0) *out = mx;
 }
 
+
+double cells_per_radius() {
+  static const double v = [] {
+    const char* e = std::getenv("RSOT_CELLS_PER_RADIUS");
+    const double x = e ? std::atof(e) : 0.0;
+    return x >= 1.0 && x <= 16.0 ? x : g_cells_per_radius;
+  }();
+  return v;
+}
 
 template <typename T>
 cudaError_t grow(T*& p, size_t& cap, size_t n) {
@@ -863,7 +980,7 @@ GridDesc plan_grid(const double blo[3], const double bhi[3], int n, double r) {
     }
   double hmin = 1.0;
   if (active > 0) hmin = std::pow(vol / std::max(1.0, n / 2.0), 1.0 / active);
-  double h = std::max(r / kCellsPerRadius, hmin);
+  double h = std::max(r / cells_per_radius(), hmin);
   if (!(h > 0.0) || !std::isfinite(h)) h = 1.0;
   for (;;) {
     long long nc = 1;
@@ -909,7 +1026,7 @@ static int ensure_target_cells(TruncWorkspace& ws, const DeviceTargets& t, Targe
     return 1;
   }
   if (build_hilbert(ws, t.y, t.n, tc, s, err)) return 1;
-  const double want = std::max(r / kCellsPerRadius, tc.hmin);
+  const double want = std::max(r / cells_per_radius(), tc.hmin);
   if (tc.cell_valid && tc.g.h >= 0.75 * want && tc.g.h <= 1.35 * want) return 0;
   GridDesc g = plan_grid(tc.bbox_lo, tc.bbox_hi, t.n, r);
   g.id = g_next_grid_id++;

@@ -765,6 +765,459 @@ trunc_passB(const double4* __restrict__ ys, const double* __restrict__ b2s, int 
   if (valid) G_out[j] = G;
 }
 
+// ---------------------------------------------------------------------------
+// Fused truncated evaluation: one atom-major kernel does both passes.
+//
+// CTA = 256 Hilbert-consecutive atoms, 2 per thread (a = lane, b = lane+32
+// of the warp's 64-atom slice).  Phase 1 scans the target cell rows within
+// reach (staged tiles, per-warp culling, packed FP32x2 pre-test for both
+// atoms, exact fp64 band test) and accumulates S~_q.  Between the phases the
+// CTA finalises its atoms (J_q, D_q, counters), resolves empty candidate
+// sets (warp-cooperative exact nearest) and recomputes atoms whose shifted
+// sum left [2^-960, 2^960] with the reference's per-atom max shift.  Phase 2
+// rescans the same tiles, recomputes the same exponentials with the
+// polynomial coefficients pre-scaled by w_q = m_q / S~_q (no extra FP64
+// work), sums each target's column over the warp's 64 atoms with a
+// transposed shuffle butterfly (16 targets per batch), over the 4 warps in
+// fixed order, and adds the CTA's partial into a 192-bit fixed-point
+// accumulator per target (order independent => deterministic).
+
+constexpr int kFA = 2 * kT;  // atoms per CTA
+
+struct FusedSmem {
+  double4 tD[kTileT];                  // {y0', y1', y2', w_j}
+  float4 tN0[kTileT];                  // {-y0', -y0', -y1', -y1'}  (FP32x2 pairs)
+  float2 tN1[kTileT];                  // {-y2', -y2'}
+  int tK[kTileT];                      // cell-order target position
+  int tJ[kTileT];                      // original target index
+  int rowStart[kT];
+  int rowPref[kT + 1];
+  unsigned char wlist[kT / 32][kTileT];
+  double colW[kT / 32][kTileT];
+  int2 tbl[16];
+  double sh[200];
+  int shi[40];
+};
+
+struct FusedAtoms {
+  double xa[3], xb[3];       // global coordinates
+  double Xa[3], Xb[3];       // 2 c2 x'
+  double xsqa, xsqb;         // c2 |x'|^2
+  float2 F0, F1, F2;         // local FP32 coordinates of (a, b)
+  bool va, vb;               // valid atoms
+  double Sa, Sb;             // phase 1 sums
+  uint32_t ca, cb;           // candidate counts
+  uint64_t ha, hb;           // candidate hashes (debug)
+  double wa[6], wb[6];       // phase 2: polynomial coefficients x m/S~
+};
+
+struct FusedArgs {
+  const double4* xs; int nq;             // atoms, Hilbert order
+  const double4* ys; const double* b2s;  // targets, cell order
+  const int* tperm; const int* cell_start;
+  GridDev g;
+  const double* scal; const double* psi;
+  double c2, r2, r_scan, eps;
+  double* atomJ; double* atomD; double* cntd; double* emptyd;
+  unsigned long long* gacc;              // [3 N] fixed point, original index
+  uint32_t* dbg_cnt; uint64_t* dbg_hash; double* dbg_logs;  // Hilbert order
+};
+
+__device__ __forceinline__ double chain3(const double (&X)[3], const double4& y) {
+  return fma(X[0], y.x, fma(X[1], y.y, fma(X[2], y.z, y.w)));
+}
+
+// w_a 2^sa [ta] + w_b 2^sb [tb] with per-atom scaled polynomials.
+__device__ __forceinline__ double exp2_pair_weighted(double sa, double sb, const double (&pa)[6],
+                                                     const double (&pb)[6],
+                                                     const int2* __restrict__ tbl, bool ta,
+                                                     bool tb) {
+  const double kka = __dadd_rn(sa, kExpMagic);
+  const double kkb = __dadd_rn(sb, kExpMagic);
+  int na = min(max(__double2loint(kka), -16320), 16000);
+  int nb = min(max(__double2loint(kkb), -16320), 16000);
+  const double ra = __dadd_rn(sa, -__dadd_rn(kka, -kExpMagic));
+  const double rb = __dadd_rn(sb, -__dadd_rn(kkb, -kExpMagic));
+  double qa = fma(pa[5], ra, pa[4]);
+  double qb = fma(pb[5], rb, pb[4]);
+  qa = fma(qa, ra, pa[3]);
+  qb = fma(qb, rb, pb[3]);
+  qa = fma(qa, ra, pa[2]);
+  qb = fma(qb, rb, pb[2]);
+  qa = fma(qa, ra, pa[1]);
+  qb = fma(qb, rb, pb[1]);
+  qa = fma(qa, ra, pa[0]);
+  qb = fma(qb, rb, pb[0]);
+  na = ta ? na : -16368;  // -16368 = 16*(-1023): scale word pattern 0 -> +0.0
+  nb = tb ? nb : -16368;
+  const int2 Ta = tbl[na & 15];
+  const int2 Tb = tbl[nb & 15];
+  const double sca = __hiloint2double(Ta.y + na * 65536, Ta.x);
+  const double scb = __hiloint2double(Tb.y + nb * 65536, Tb.x);
+  return fma(qa, sca, qb * scb);
+}
+
+// Transposed butterfly: v[i] (this lane's contribution to item i of the
+// batch) -> lane l returns the warp total of item (l >> 1).
+__device__ __forceinline__ double butterfly16(double (&v)[16]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int h = 8, o = 16; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = up ? v[i] : v[i + h];
+      const double keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+// Stages tile [base, base + cnt) of the current row batch.
+__device__ __forceinline__ void fused_stage(FusedSmem& sm, const FusedArgs& A, const Region& R,
+                                            double B, int base, int cnt) {
+  for (int t = threadIdx.x; t < cnt; t += kT) {
+    const int s = base + t;
+    const int r = find_row(sm.rowPref, s);
+    const int k = sm.rowStart[r] + (s - sm.rowPref[r]);
+    const double4 y = A.ys[k];
+    const double y0 = y.x - R.o[0], y1 = y.y - R.o[1], y2 = y.z - R.o[2];
+    const double yy = fma(y2, y2, fma(y1, y1, y0 * y0));
+    const double w = fmax(fma(-A.c2, yy, A.b2s[k]) - B, -1.0e5);
+    sm.tD[t] = make_double4(y0, y1, y2, w);
+    const float f0 = -static_cast<float>(y0), f1 = -static_cast<float>(y1),
+                f2 = -static_cast<float>(y2);
+    sm.tN0[t] = make_float4(f0, f0, f1, f1);
+    sm.tN1[t] = make_float2(f2, f2);
+    sm.tK[t] = k;
+    sm.tJ[t] = A.tperm[k];
+  }
+}
+
+__device__ __forceinline__ int fused_cull(const FusedSmem& sm, int cnt, const WarpBox& w,
+                                          float thr, unsigned char* __restrict__ list) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  int nsel = 0;
+  for (int g = 0; g < cnt; g += 32) {
+    const int t = g + lane;
+    bool keep = false;
+    if (t < cnt) {
+      const float4 a = sm.tN0[t];
+      const float2 b = sm.tN1[t];
+      const float dx = fmaxf(fmaxf(w.lo0 + a.x, -a.x - w.hi0), 0.f);
+      const float dy = fmaxf(fmaxf(w.lo1 + a.z, -a.z - w.hi1), 0.f);
+      const float dz = fmaxf(fmaxf(w.lo2 + b.x, -b.x - w.hi2), 0.f);
+      keep = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= thr;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (keep) list[nsel + __popc(m & lt)] = static_cast<unsigned char>(t);
+    nsel += __popc(m);
+  }
+  __syncwarp();
+  return nsel;
+}
+
+// Packed FP32x2 pre-test of one item against both atoms + exact band test.
+__device__ __forceinline__ void fused_test(const FusedSmem& sm, const FusedArgs& A, const Region& R,
+                                          const FusedAtoms& at, int t, bool valid_item, bool& ina,
+                                          bool& inb, bool& bda, bool& bdb) {
+  const float4 n01 = sm.tN0[t];
+  const float2 n2 = sm.tN1[t];
+  const float2 dx = __fadd2_rn(at.F0, make_float2(n01.x, n01.y));
+  const float2 dy = __fadd2_rn(at.F1, make_float2(n01.z, n01.w));
+  const float2 dz = __fadd2_rn(at.F2, n2);
+  float2 d2 = __fmul2_rn(dx, dx);
+  d2 = __ffma2_rn(dy, dy, d2);
+  d2 = __ffma2_rn(dz, dz, d2);
+  ina = valid_item && d2.x < R.lo_thr;
+  inb = valid_item && d2.y < R.lo_thr;
+  bda = valid_item && !ina && d2.x <= R.hi_thr;
+  bdb = valid_item && !inb && d2.y <= R.hi_thr;
+}
+
+__device__ __forceinline__ void fused_exact(const FusedSmem& sm, const FusedArgs& A,
+                                           const FusedAtoms& at, int t, bool bda, bool bdb,
+                                           bool& ina, bool& inb) {
+  const double4 yg = A.ys[sm.tK[t]];
+  if (bda) ina = exact_inside(at.xa[0], at.xa[1], at.xa[2], yg.x, yg.y, yg.z, A.r2);
+  if (bdb) inb = exact_inside(at.xb[0], at.xb[1], at.xb[2], yg.x, yg.y, yg.z, A.r2);
+}
+
+template <int PHASE, bool WIDE, bool DEBUG>
+__device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const Region& R, const WarpBox& wb,
+                           float cull_thr, double B, FusedAtoms& at) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* const list = sm.wlist[warp];
+  const int ny = R.c_hi[1] - R.c_lo[1] + 1;
+  const int nrows = ny * (R.c_hi[2] - R.c_lo[2] + 1);
+  for (int rb = 0; rb < nrows; rb += kT) {
+    int st = 0, ln = 0;
+    if (rb + threadIdx.x < nrows) row_range(A.g, R, A.r_scan, A.cell_start, rb + threadIdx.x, st, ln);
+    int total = 0;
+    const int pre = block_exclusive_scan<kT>(ln, sm.shi, &total);
+    sm.rowStart[threadIdx.x] = st;
+    sm.rowPref[threadIdx.x] = pre;
+    if (threadIdx.x == 0) sm.rowPref[kT] = total;
+    for (int base = 0; base < total; base += kTileT) {
+      const int cnt = min(kTileT, total - base);
+      __syncthreads();
+      fused_stage(sm, A, R, B, base, cnt);
+      __syncthreads();
+      const int nsel = fused_cull(sm, cnt, wb, cull_thr, list);
+      if (PHASE == 1) {
+        for (int i = 0; i < nsel; i += 2) {
+          const bool v1 = i + 1 < nsel;
+          const int t0 = list[i];
+          const int t1 = v1 ? list[i + 1] : t0;
+          bool a0, b0, a1, b1, da0, db0, da1, db1;
+          fused_test(sm, A, R, at, t0, true, a0, b0, da0, db0);
+          fused_test(sm, A, R, at, t1, v1, a1, b1, da1, db1);
+          if (__any_sync(0xffffffffu, da0 || db0 || da1 || db1)) {
+            if (da0 || db0) fused_exact(sm, A, at, t0, da0, db0, a0, b0);
+            if (da1 || db1) fused_exact(sm, A, at, t1, da1, db1, a1, b1);
+          }
+          if (__any_sync(0xffffffffu, a0 || b0 || a1 || b1)) {
+            const double4 y0 = sm.tD[t0];
+            const double4 y1 = sm.tD[t1];
+            double sa0 = chain3(at.Xa, y0), sb0 = chain3(at.Xb, y0);
+            double sa1 = chain3(at.Xa, y1), sb1 = chain3(at.Xb, y1);
+            if (WIDE) {
+              sa0 -= at.xsqa; sa1 -= at.xsqa;
+              sb0 -= at.xsqb; sb1 -= at.xsqb;
+            }
+            at.Sa = exp2_acc_masked(sa0, at.Sa, sm.tbl, a0);
+            at.Sb = exp2_acc_masked(sb0, at.Sb, sm.tbl, b0);
+            at.Sa = exp2_acc_masked(sa1, at.Sa, sm.tbl, a1);
+            at.Sb = exp2_acc_masked(sb1, at.Sb, sm.tbl, b1);
+            at.ca += static_cast<uint32_t>(a0) + static_cast<uint32_t>(a1);
+            at.cb += static_cast<uint32_t>(b0) + static_cast<uint32_t>(b1);
+            if (DEBUG) {
+              if (a0) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
+              if (a1) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
+              if (b0) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
+              if (b1) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
+            }
+          }
+        }
+      } else {
+        double* const col = sm.colW[warp];
+        for (int s = lane; s < cnt; s += 32) col[s] = 0.0;
+        __syncwarp();
+        for (int b0 = 0; b0 < nsel; b0 += 16) {
+          double v[16];
+#pragma unroll
+          for (int p = 0; p < 8; ++p) {
+            const int i = b0 + 2 * p;
+            const bool v0 = i < nsel, v1 = i + 1 < nsel;
+            const int t0 = v0 ? list[i] : list[0];
+            const int t1 = v1 ? list[i + 1] : t0;
+            bool a0, bb0, a1, bb1, da0, db0, da1, db1;
+            fused_test(sm, A, R, at, t0, v0, a0, bb0, da0, db0);
+            fused_test(sm, A, R, at, t1, v1, a1, bb1, da1, db1);
+            if (__any_sync(0xffffffffu, da0 || db0 || da1 || db1)) {
+              if (da0 || db0) fused_exact(sm, A, at, t0, da0, db0, a0, bb0);
+              if (da1 || db1) fused_exact(sm, A, at, t1, da1, db1, a1, bb1);
+            }
+            v[2 * p] = 0.0;
+            v[2 * p + 1] = 0.0;
+            if (__any_sync(0xffffffffu, a0 || bb0 || a1 || bb1)) {
+              const double4 y0 = sm.tD[t0];
+              const double4 y1 = sm.tD[t1];
+              double sa0 = chain3(at.Xa, y0), sb0 = chain3(at.Xb, y0);
+              double sa1 = chain3(at.Xa, y1), sb1 = chain3(at.Xb, y1);
+              if (WIDE) {
+                sa0 -= at.xsqa; sa1 -= at.xsqa;
+                sb0 -= at.xsqb; sb1 -= at.xsqb;
+              }
+              v[2 * p] = exp2_pair_weighted(sa0, sb0, at.wa, at.wb, sm.tbl, a0, bb0);
+              v[2 * p + 1] = exp2_pair_weighted(sa1, sb1, at.wa, at.wb, sm.tbl, a1, bb1);
+            }
+          }
+          const double tot = butterfly16(v);
+          const int item = b0 + (lane >> 1);
+          if (!(lane & 1) && item < nsel) col[list[item]] = tot;
+        }
+      }
+      if (PHASE == 2) {
+        __syncthreads();
+        for (int s = threadIdx.x; s < cnt; s += kT) {
+          const double c = ((sm.colW[0][s] + sm.colW[1][s]) + sm.colW[2][s]) + sm.colW[3][s];
+          if (c > 0.0) fp_add(A.gacc + 3 * static_cast<size_t>(sm.tJ[s]), c);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Exact LSE (reference per-atom max shift) of one atom by the whole warp,
+// and, for the gradient, its exact contributions p_qj m_q into gacc.
+__device__ void warp_exact_atom(const FusedArgs& A, const double x[3], double m, double& L) {
+  const int lane = threadIdx.x & 31;
+  int c_lo[3], c_hi[3];
+  for (int d = 0; d < 3; ++d) {
+    c_lo[d] = cell_of(A.g, d, x[d] - A.r_scan);
+    c_hi[d] = cell_of(A.g, d, x[d] + A.r_scan);
+  }
+  double mx = -INFINITY, sum = 0.0;
+  for (int pass = 0; pass < 3; ++pass) {
+    double acc = pass == 0 ? -INFINITY : 0.0;
+    for (int cz = c_lo[2]; cz <= c_hi[2]; ++cz)
+      for (int cy = c_lo[1]; cy <= c_hi[1]; ++cy) {
+        const long long row = (static_cast<long long>(cz) * A.g.dims[1] + cy) * A.g.dims[0];
+        const int b = A.cell_start[row + c_lo[0]], e = A.cell_start[row + c_hi[0] + 1];
+        for (int k = b + lane; k < e; k += 32) {
+          const double4 y = A.ys[k];
+          const double d2 = exact_sqdist(x[0], x[1], x[2], y.x, y.y, y.z);
+          if (!(d2 < A.r2)) continue;
+          const int j = A.tperm[k];
+          const double ex = reference_exponent(A.psi[j], d2, A.eps, y.w);
+          if (pass == 0) acc = fmax(acc, ex);
+          else if (pass == 1) acc += exp(ex - mx);
+          else fp_add(A.gacc + 3 * static_cast<size_t>(j), exp(ex - mx) * (m / sum));
+        }
+      }
+    if (pass == 0) mx = warp_max(acc);
+    else if (pass == 1) sum = warp_sum(acc);
+  }
+  L = mx + log(sum);
+}
+
+// Per-atom finalisation between the phases (all lanes of the warp call it:
+// empty and flagged atoms are resolved warp-cooperatively).
+template <bool DEBUG>
+__device__ __forceinline__ void fused_finalize(const FusedArgs& A, const Region& R, double B,
+                                               bool valid, uint32_t c, double S, double xsq,
+                                               const double4& p, const double (&x)[3],
+                                               uint64_t hash, int q, double (&W)[6]) {
+  const int lane = threadIdx.x & 31;
+  const double shift = R.wide ? 0.0 : xsq;
+  const double m = p.w;
+  const bool empty = valid && c == 0;
+  const bool flag = valid && c > 0 && (!(S >= 0x1p-960) || !(S <= 0x1p960));
+  double L = (B - shift + log2(S)) * kLn2;
+  double w = valid && c > 0 ? m / S : 0.0;
+  unsigned me = __ballot_sync(0xffffffffu, empty);
+  while (me) {
+    const int l = __ffs(me) - 1;
+    me &= me - 1;
+    const double px = __shfl_sync(0xffffffffu, x[0], l);
+    const double py = __shfl_sync(0xffffffffu, x[1], l);
+    const double pz = __shfl_sync(0xffffffffu, x[2], l);
+    const double pm = __shfl_sync(0xffffffffu, m, l);
+    double bd;
+    int bj, bk;
+    warp_nearest(A.g, A.ys, A.tperm, A.cell_start, px, py, pz, bd, bj, bk);
+    if (lane == l) {
+      L = reference_exponent(A.psi[bj], bd, A.eps, A.ys[bk].w);
+      if (DEBUG) hash = candidate_hash_term(static_cast<uint64_t>(bj));
+    }
+    if (lane == 0) fp_add(A.gacc + 3 * static_cast<size_t>(bj), pm);
+  }
+  unsigned mf = __ballot_sync(0xffffffffu, flag);
+  while (mf) {
+    const int l = __ffs(mf) - 1;
+    mf &= mf - 1;
+    double px[3];
+    px[0] = __shfl_sync(0xffffffffu, x[0], l);
+    px[1] = __shfl_sync(0xffffffffu, x[1], l);
+    px[2] = __shfl_sync(0xffffffffu, x[2], l);
+    const double pm = __shfl_sync(0xffffffffu, m, l);
+    double Lx;
+    warp_exact_atom(A, px, pm, Lx);
+    if (lane == l) {
+      L = Lx;
+      w = 0.0;  // its gradient contributions are already in gacc
+    }
+  }
+  W[0] = kP0 * w; W[1] = kP1 * w; W[2] = kP2 * w;
+  W[3] = kP3 * w; W[4] = kP4 * w; W[5] = kP5 * w;
+  if (valid) {
+    A.atomJ[q] = A.eps * L * m;
+    A.atomD[q] = m * exp(-L);
+    A.cntd[q] = c == 0 ? 1.0 : static_cast<double>(c);
+    A.emptyd[q] = c == 0 ? 1.0 : 0.0;
+    if (DEBUG) {
+      A.dbg_cnt[q] = c == 0 ? 1u : c;
+      A.dbg_hash[q] = hash;
+      A.dbg_logs[q] = L;
+    }
+  }
+}
+
+template <bool DEBUG>
+__global__ void __launch_bounds__(kT, 3)
+trunc_fused(FusedArgs A) {
+  __shared__ FusedSmem sm;
+  load_exp2_table(sm.tbl);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qa = blockIdx.x * kFA + warp * 64 + lane, qb = qa + 32;
+  FusedAtoms at;
+  at.va = qa < A.nq;
+  at.vb = qb < A.nq;
+  const double4 pa = at.va ? A.xs[qa] : make_double4(0, 0, 0, 0);
+  const double4 pb = at.vb ? A.xs[qb] : make_double4(0, 0, 0, 0);
+  at.xa[0] = pa.x; at.xa[1] = pa.y; at.xa[2] = pa.z;
+  at.xb[0] = pb.x; at.xb[1] = pb.y; at.xb[2] = pb.z;
+  double lo[3], hi[3];
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = fmin(at.va ? at.xa[d] : INFINITY, at.vb ? at.xb[d] : INFINITY);
+    hi[d] = fmax(at.va ? at.xa[d] : -INFINITY, at.vb ? at.xb[d] : -INFINITY);
+  }
+  Region R;
+  setup_region(A.g, lo, hi, A.r2, A.r_scan, A.c2, sm.sh, R);
+  double xl[3], yl[3];
+  for (int d = 0; d < 3; ++d) {
+    xl[d] = at.xa[d] - R.o[d];
+    yl[d] = at.xb[d] - R.o[d];
+    at.Xa[d] = 2.0 * A.c2 * xl[d];
+    at.Xb[d] = 2.0 * A.c2 * yl[d];
+  }
+  at.xsqa = A.c2 * fma(xl[2], xl[2], fma(xl[1], xl[1], xl[0] * xl[0]));
+  at.xsqb = A.c2 * fma(yl[2], yl[2], fma(yl[1], yl[1], yl[0] * yl[0]));
+  const float big = 1e30f;
+  at.F0 = make_float2(at.va ? static_cast<float>(xl[0]) : big, at.vb ? static_cast<float>(yl[0]) : big);
+  at.F1 = make_float2(at.va ? static_cast<float>(xl[1]) : big, at.vb ? static_cast<float>(yl[1]) : big);
+  at.F2 = make_float2(at.va ? static_cast<float>(xl[2]) : big, at.vb ? static_cast<float>(yl[2]) : big);
+  at.Sa = at.Sb = 0.0;
+  at.ca = at.cb = 0;
+  at.ha = at.hb = 0;
+  // warp box over both atoms of every lane
+  WarpBox wb;
+  {
+    const WarpBox w1 = warp_box(at.va, at.F0.x, at.F1.x, at.F2.x);
+    const WarpBox w2 = warp_box(at.vb, at.F0.y, at.F1.y, at.F2.y);
+    wb.lo0 = fminf(w1.lo0, w2.lo0); wb.lo1 = fminf(w1.lo1, w2.lo1); wb.lo2 = fminf(w1.lo2, w2.lo2);
+    wb.hi0 = fmaxf(w1.hi0, w2.hi0); wb.hi1 = fmaxf(w1.hi1, w2.hi1); wb.hi2 = fmaxf(w1.hi2, w2.hi2);
+  }
+  const float cull_thr = R.hi_thr * 1.0001f;
+  const double B = A.scal[kSlotB];
+
+  // ---- phase 1: S~ ----
+  if (R.wide)
+    fused_scan<1, true, DEBUG>(sm, A, R, wb, cull_thr, B, at);
+  else
+    fused_scan<1, false, DEBUG>(sm, A, R, wb, cull_thr, B, at);
+
+  // ---- finalise atoms; empty sets and flagged sums (warp cooperative) ----
+  fused_finalize<DEBUG>(A, R, B, at.va, at.ca, at.Sa, at.xsqa, pa, at.xa, at.ha, qa, at.wa);
+  fused_finalize<DEBUG>(A, R, B, at.vb, at.cb, at.Sb, at.xsqb, pb, at.xb, at.hb, qb, at.wb);
+
+  // ---- phase 2: gradient ----
+  if (R.wide)
+    fused_scan<2, true, DEBUG>(sm, A, R, wb, cull_thr, B, at);
+  else
+    fused_scan<2, false, DEBUG>(sm, A, R, wb, cull_thr, B, at);
+}
+
+__global__ void trunc_assemble_fp(const unsigned long long* __restrict__ gacc, int n,
+                                  double* __restrict__ res) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) res[j] = fp_to_double(gacc + 3 * static_cast<size_t>(j));
+}
+
 __global__ void trunc_assemble(const double* __restrict__ G, const int* __restrict__ tperm,
                                int n, const unsigned long long* __restrict__ empty_fp,
                                double* __restrict__ res) {
@@ -846,6 +1299,14 @@ __global__ void max_cost_kernel(const double* __restrict__ d2, int m, double* __
   if (threadIdx.x == 0) *out = mx;
 }
 
+
+bool use_fused() {
+  static const bool v = [] {
+    const char* e = std::getenv("RSOT_TRUNC_PATH");
+    return !(e && std::string(e) == "split");
+  }();
+  return v;
+}
 
 double cells_per_radius() {
   static const double v = [] {
@@ -1100,7 +1561,40 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
   TCK(cudaMemsetAsync(ws.empty_fp, 0, sizeof(unsigned long long) * 3 * static_cast<size_t>(n), s));
   (note_launch(), gather_d_kernel<<<(n + 255) / 256, 256, 0, s>>>(b.b2, tc.perm_c, n, ws.b2s));
   (note_launch(), gather_d_kernel<<<(n + 255) / 256, 256, 0, s>>>(b.b2, tc.perm_h, n, ws.b2h));
-  if (nq > 0) {
+  if (nq > 0 && use_fused()) {
+    FusedArgs A;
+    A.xs = ac.ph; A.nq = nq; A.ys = tc.pc; A.b2s = ws.b2s; A.tperm = tc.perm_c;
+    A.cell_start = tc.cell_start; A.g = g; A.scal = b.scal; A.psi = b.psi;
+    A.c2 = c2; A.r2 = r2; A.r_scan = r_scan; A.eps = eps;
+    A.atomJ = ws.atomJ; A.atomD = ws.atomD; A.cntd = ws.cntd; A.emptyd = ws.emptyd;
+    A.gacc = ws.empty_fp;
+    A.dbg_cnt = ws.cnt; A.dbg_hash = ws.hash; A.dbg_logs = ws.atomL;
+    const int nblk = (nq + kFA - 1) / kFA;
+    if (b.timing) cudaEventRecord(b.timing[1], s);
+    if (dbg)
+      (note_launch(), trunc_fused<true><<<nblk, kT, 0, s>>>(A));
+    else
+      (note_launch(), trunc_fused<false><<<nblk, kT, 0, s>>>(A));
+    if (b.timing) {
+      cudaEventRecord(b.timing[2], s);
+      cudaEventRecord(b.timing[3], s);
+      cudaEventRecord(b.timing[4], s);
+    }
+    (note_launch(), trunc_assemble_fp<<<(n + 255) / 256, 256, 0, s>>>(ws.empty_fp, n, b.res));
+    launch_det_sum(ws.atomJ, nq, ws.red, b.res + n + kResJ, s);
+    launch_det_sum(ws.atomD, nq, ws.red + 1024, b.res + n + kResD, s);
+    launch_det_sum(ws.cntd, nq, ws.red + 2048, b.res + n + kResPairs, s);
+    launch_det_sum(ws.emptyd, nq, ws.red + 3072, b.res + n + kResEmpty, s);
+    if (dbg) {
+      (note_launch(), scatter_debug<uint32_t><<<(nq + 255) / 256, 256, 0, s>>>(ws.cnt, ac.perm_h, nq,
+                                                                           dbg->count));
+      (note_launch(), scatter_debug<unsigned long long><<<(nq + 255) / 256, 256, 0, s>>>(
+          reinterpret_cast<unsigned long long*>(ws.hash), ac.perm_h, nq,
+          reinterpret_cast<unsigned long long*>(dbg->hash)));
+      (note_launch(), scatter_debug<double><<<(nq + 255) / 256, 256, 0, s>>>(ws.atomL, ac.perm_h, nq,
+                                                                          dbg->log_s));
+    }
+  } else if (nq > 0) {
     const int nblk = (nq + kT - 1) / kT;
     if (b.timing) cudaEventRecord(b.timing[1], s);
     if (scan) {

@@ -54,41 +54,47 @@ __global__ void prologue_blocks(const double4* __restrict__ tgt,
   __shared__ double sh[256];
   const int lo = blockIdx.x * chunk;
   const int hi = min(n, lo + chunk);
-  double mx = -INFINITY, s = 0.0, bad = 0.0;
+  double mx = -INFINITY, mn = INFINITY, s = 0.0, bad = 0.0;
   for (int j = lo + threadIdx.x; j < hi; j += blockDim.x) {
     const double p = psi[j];
     if (!isfinite(p)) bad = 1.0;
     const double v = kLog2e * fma(p, inv_eps, tgt[j].w);
     b2[j] = v;
     mx = fmax(mx, v);
+    mn = fmin(mn, v);
     s = fma(p, nu[j], s);
   }
   mx = block_max<256>(mx, sh);
+  mn = -block_max<256>(-mn, sh);
   s = block_sum<256>(s, sh);
   bad = block_max<256>(bad, sh);
   if (threadIdx.x == 0) {
     part[blockIdx.x] = mx;
     part[kRedBlocks + blockIdx.x] = s;
     part[2 * kRedBlocks + blockIdx.x] = bad;
+    part[3 * kRedBlocks + blockIdx.x] = mn;
   }
 }
 
 __global__ void prologue_final(const double* __restrict__ part, int nblk,
                                double* __restrict__ scal) {
   __shared__ double sh[256];
-  double mx = -INFINITY, s = 0.0, bad = 0.0;
+  double mx = -INFINITY, mn = INFINITY, s = 0.0, bad = 0.0;
   for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
     mx = fmax(mx, part[i]);
     s += part[kRedBlocks + i];
     bad = fmax(bad, part[2 * kRedBlocks + i]);
+    mn = fmin(mn, part[3 * kRedBlocks + i]);
   }
   mx = block_max<256>(mx, sh);
+  mn = -block_max<256>(-mn, sh);
   s = block_sum<256>(s, sh);
   bad = block_max<256>(bad, sh);
   if (threadIdx.x == 0) {
     scal[kSlotB] = mx;
     scal[kSlotPsiNu] = s;
     scal[kSlotNonFinite] = bad;
+    scal[kSlotBmin] = mn;
   }
 }
 

@@ -75,12 +75,16 @@ __device__ __forceinline__ double exp2_acc(double s, double acc,
   return fma(p, scale, acc);
 }
 
-// acc + (take ? 2^s : 0) without a branch (the scale is zeroed on the INT
-// pipe for lanes that do not take the pair).
+// acc + (take ? 2^s : 0) without a branch.  Lanes that do not take the
+// pair get n = -16368 = 16 * (-1023), whose scale word pattern is exactly
+// +0.0 (one SEL on the INT pipe).  CLAMP = false is used when the caller has
+// proven every taken s lies in [-1020, 1000].
+template <bool CLAMP = true>
 __device__ __forceinline__ double exp2_acc_masked(double s, double acc,
                                                   const int2* __restrict__ tbl, bool take) {
   const double kk = __dadd_rn(s, kExpMagic);
-  const int n = min(max(__double2loint(kk), -16320), 16000);
+  int n = __double2loint(kk);
+  if (CLAMP) n = min(max(n, -16320), 16000);
   const double kd = __dadd_rn(kk, -kExpMagic);
   const double r = __dadd_rn(s, -kd);
   double p = fma(kP5, r, kP4);
@@ -88,10 +92,9 @@ __device__ __forceinline__ double exp2_acc_masked(double s, double acc,
   p = fma(p, r, kP2);
   p = fma(p, r, kP1);
   p = fma(p, r, kP0);
+  n = take ? n : -16368;
   const int2 t = tbl[n & 15];
-  const int hi = take ? t.y + n * 65536 : 0;
-  const int lo = take ? t.x : 0;
-  return fma(p, __hiloint2double(hi, lo), acc);
+  return fma(p, __hiloint2double(t.y + n * 65536, t.x), acc);
 }
 
 // Exact reference predicate (point.hpp:35-40, spatial_index.cpp:54):

@@ -27,6 +27,7 @@ enum ScalarSlot : int {
   kSlotPsiNu = 1,      // sum_j psi_j nu_j (fixed-order)
   kSlotNonFinite = 2,  // > 0 when psi had a non-finite entry
   kSlotFlagCount = 3,  // u64 count of atoms needing the exact fallback
+  kSlotBmin = 4,       // min_j b2_j (exponent range check)
   kNumSlots = 8
 };
 

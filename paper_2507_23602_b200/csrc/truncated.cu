@@ -794,17 +794,18 @@ struct FusedSmem {
   int rowPref[kT + 1];
   unsigned char wlist[kT / 32][kTileT];
   double colW[kT / 32][kTileT];
+  Region R;                            // CTA-uniform scan region (kept out of registers)
   int2 tbl[16];
   double sh[200];
   int shi[40];
 };
 
 struct FusedAtoms {
-  double xa[3], xb[3];       // global coordinates
   double Xa[3], Xb[3];       // 2 c2 x'
   double xsqa, xsqb;         // c2 |x'|^2
   float2 F0, F1, F2;         // local FP32 coordinates of (a, b)
-  bool va, vb;               // valid atoms
+  float lo_thr, hi_thr;      // FP32 decision thresholds
+  int qa, qb;                // Hilbert positions of the two atoms
   double Sa, Sb;             // phase 1 sums
   uint32_t ca, cb;           // candidate counts
   uint64_t ha, hb;           // candidate hashes (debug)
@@ -828,14 +829,19 @@ __device__ __forceinline__ double chain3(const double (&X)[3], const double4& y)
 }
 
 // w_a 2^sa [ta] + w_b 2^sb [tb] with per-atom scaled polynomials.
+template <bool CLAMP>
 __device__ __forceinline__ double exp2_pair_weighted(double sa, double sb, const double (&pa)[6],
                                                      const double (&pb)[6],
                                                      const int2* __restrict__ tbl, bool ta,
                                                      bool tb) {
   const double kka = __dadd_rn(sa, kExpMagic);
   const double kkb = __dadd_rn(sb, kExpMagic);
-  int na = min(max(__double2loint(kka), -16320), 16000);
-  int nb = min(max(__double2loint(kkb), -16320), 16000);
+  int na = __double2loint(kka);
+  int nb = __double2loint(kkb);
+  if (CLAMP) {
+    na = min(max(na, -16320), 16000);
+    nb = min(max(nb, -16320), 16000);
+  }
   const double ra = __dadd_rn(sa, -__dadd_rn(kka, -kExpMagic));
   const double rb = __dadd_rn(sb, -__dadd_rn(kkb, -kExpMagic));
   double qa = fma(pa[5], ra, pa[4]);
@@ -848,7 +854,7 @@ __device__ __forceinline__ double exp2_pair_weighted(double sa, double sb, const
   qb = fma(qb, rb, pb[1]);
   qa = fma(qa, ra, pa[0]);
   qb = fma(qb, rb, pb[0]);
-  na = ta ? na : -16368;  // -16368 = 16*(-1023): scale word pattern 0 -> +0.0
+  na = ta ? na : -16368;  // scale word pattern 0 -> +0.0
   nb = tb ? nb : -16368;
   const int2 Ta = tbl[na & 15];
   const int2 Tb = tbl[nb & 15];
@@ -858,7 +864,7 @@ __device__ __forceinline__ double exp2_pair_weighted(double sa, double sb, const
 }
 
 // Transposed butterfly: v[i] (this lane's contribution to item i of the
-// batch) -> lane l returns the warp total of item (l >> 1).
+// batch of 16) -> lane l returns the warp total of item (l >> 1).
 __device__ __forceinline__ double butterfly16(double (&v)[16]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -875,14 +881,15 @@ __device__ __forceinline__ double butterfly16(double (&v)[16]) {
 }
 
 // Stages tile [base, base + cnt) of the current row batch.
-__device__ __forceinline__ void fused_stage(FusedSmem& sm, const FusedArgs& A, const Region& R,
-                                            double B, int base, int cnt) {
+__device__ __forceinline__ void fused_stage(FusedSmem& sm, const FusedArgs& A, double B,
+                                            int base, int cnt) {
+  const double o0 = sm.R.o[0], o1 = sm.R.o[1], o2 = sm.R.o[2];
   for (int t = threadIdx.x; t < cnt; t += kT) {
     const int s = base + t;
     const int r = find_row(sm.rowPref, s);
     const int k = sm.rowStart[r] + (s - sm.rowPref[r]);
     const double4 y = A.ys[k];
-    const double y0 = y.x - R.o[0], y1 = y.y - R.o[1], y2 = y.z - R.o[2];
+    const double y0 = y.x - o0, y1 = y.y - o1, y2 = y.z - o2;
     const double yy = fma(y2, y2, fma(y1, y1, y0 * y0));
     const double w = fmax(fma(-A.c2, yy, A.b2s[k]) - B, -1.0e5);
     sm.tD[t] = make_double4(y0, y1, y2, w);
@@ -919,10 +926,10 @@ __device__ __forceinline__ int fused_cull(const FusedSmem& sm, int cnt, const Wa
   return nsel;
 }
 
-// Packed FP32x2 pre-test of one item against both atoms + exact band test.
-__device__ __forceinline__ void fused_test(const FusedSmem& sm, const FusedArgs& A, const Region& R,
-                                          const FusedAtoms& at, int t, bool valid_item, bool& ina,
-                                          bool& inb, bool& bda, bool& bdb) {
+// Packed FP32x2 pre-test of one item against both atoms.
+__device__ __forceinline__ void fused_test(const FusedSmem& sm, const FusedAtoms& at, int t,
+                                          bool valid_item, bool& ina, bool& inb, bool& bda,
+                                          bool& bdb) {
   const float4 n01 = sm.tN0[t];
   const float2 n2 = sm.tN1[t];
   const float2 dx = __fadd2_rn(at.F0, make_float2(n01.x, n01.y));
@@ -931,30 +938,42 @@ __device__ __forceinline__ void fused_test(const FusedSmem& sm, const FusedArgs&
   float2 d2 = __fmul2_rn(dx, dx);
   d2 = __ffma2_rn(dy, dy, d2);
   d2 = __ffma2_rn(dz, dz, d2);
-  ina = valid_item && d2.x < R.lo_thr;
-  inb = valid_item && d2.y < R.lo_thr;
-  bda = valid_item && !ina && d2.x <= R.hi_thr;
-  bdb = valid_item && !inb && d2.y <= R.hi_thr;
+  ina = valid_item && d2.x < at.lo_thr;
+  inb = valid_item && d2.y < at.lo_thr;
+  bda = valid_item && !ina && d2.x <= at.hi_thr;
+  bdb = valid_item && !inb && d2.y <= at.hi_thr;
 }
 
+// Exact reference predicate for pairs inside the FP32 error band (rare).
 __device__ __forceinline__ void fused_exact(const FusedSmem& sm, const FusedArgs& A,
-                                           const FusedAtoms& at, int t, bool bda, bool bdb,
-                                           bool& ina, bool& inb) {
+                                         const FusedAtoms& at, int t, bool bda, bool bdb,
+                                         bool& ina, bool& inb) {
   const double4 yg = A.ys[sm.tK[t]];
-  if (bda) ina = exact_inside(at.xa[0], at.xa[1], at.xa[2], yg.x, yg.y, yg.z, A.r2);
-  if (bdb) inb = exact_inside(at.xb[0], at.xb[1], at.xb[2], yg.x, yg.y, yg.z, A.r2);
+  if (bda) {
+    const double4 x = A.xs[at.qa];
+    ina = exact_inside(x.x, x.y, x.z, yg.x, yg.y, yg.z, A.r2);
+  }
+  if (bdb) {
+    const double4 x = A.xs[at.qb];
+    inb = exact_inside(x.x, x.y, x.z, yg.x, yg.y, yg.z, A.r2);
+  }
 }
 
-template <int PHASE, bool WIDE, bool DEBUG>
-__device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const Region& R, const WarpBox& wb,
-                           float cull_thr, double B, FusedAtoms& at) {
+// SAFE: CTA whose exponents may leave [-1020, 1000] (spread chunk or huge
+// psi range): per-atom shift carried in every exponent when R.wide, and the
+// exponent split clamped.
+template <int PHASE, bool SAFE, bool DEBUG>
+__device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb, float cull_thr,
+                           double B, FusedAtoms& at) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* const list = sm.wlist[warp];
-  const int ny = R.c_hi[1] - R.c_lo[1] + 1;
-  const int nrows = ny * (R.c_hi[2] - R.c_lo[2] + 1);
+  const bool wide = SAFE && sm.R.wide;
+  const int ny = sm.R.c_hi[1] - sm.R.c_lo[1] + 1;
+  const int nrows = ny * (sm.R.c_hi[2] - sm.R.c_lo[2] + 1);
   for (int rb = 0; rb < nrows; rb += kT) {
     int st = 0, ln = 0;
-    if (rb + threadIdx.x < nrows) row_range(A.g, R, A.r_scan, A.cell_start, rb + threadIdx.x, st, ln);
+    if (rb + threadIdx.x < nrows)
+      row_range(A.g, sm.R, A.r_scan, A.cell_start, rb + threadIdx.x, st, ln);
     int total = 0;
     const int pre = block_exclusive_scan<kT>(ln, sm.shi, &total);
     sm.rowStart[threadIdx.x] = st;
@@ -963,7 +982,7 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const Region& R, c
     for (int base = 0; base < total; base += kTileT) {
       const int cnt = min(kTileT, total - base);
       __syncthreads();
-      fused_stage(sm, A, R, B, base, cnt);
+      fused_stage(sm, A, B, base, cnt);
       __syncthreads();
       const int nsel = fused_cull(sm, cnt, wb, cull_thr, list);
       if (PHASE == 1) {
@@ -972,8 +991,8 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const Region& R, c
           const int t0 = list[i];
           const int t1 = v1 ? list[i + 1] : t0;
           bool a0, b0, a1, b1, da0, db0, da1, db1;
-          fused_test(sm, A, R, at, t0, true, a0, b0, da0, db0);
-          fused_test(sm, A, R, at, t1, v1, a1, b1, da1, db1);
+          fused_test(sm, at, t0, true, a0, b0, da0, db0);
+          fused_test(sm, at, t1, v1, a1, b1, da1, db1);
           if (__any_sync(0xffffffffu, da0 || db0 || da1 || db1)) {
             if (da0 || db0) fused_exact(sm, A, at, t0, da0, db0, a0, b0);
             if (da1 || db1) fused_exact(sm, A, at, t1, da1, db1, a1, b1);
@@ -983,14 +1002,14 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const Region& R, c
             const double4 y1 = sm.tD[t1];
             double sa0 = chain3(at.Xa, y0), sb0 = chain3(at.Xb, y0);
             double sa1 = chain3(at.Xa, y1), sb1 = chain3(at.Xb, y1);
-            if (WIDE) {
+            if (wide) {
               sa0 -= at.xsqa; sa1 -= at.xsqa;
               sb0 -= at.xsqb; sb1 -= at.xsqb;
             }
-            at.Sa = exp2_acc_masked(sa0, at.Sa, sm.tbl, a0);
-            at.Sb = exp2_acc_masked(sb0, at.Sb, sm.tbl, b0);
-            at.Sa = exp2_acc_masked(sa1, at.Sa, sm.tbl, a1);
-            at.Sb = exp2_acc_masked(sb1, at.Sb, sm.tbl, b1);
+            at.Sa = exp2_acc_masked<SAFE>(sa0, at.Sa, sm.tbl, a0);
+            at.Sb = exp2_acc_masked<SAFE>(sb0, at.Sb, sm.tbl, b0);
+            at.Sa = exp2_acc_masked<SAFE>(sa1, at.Sa, sm.tbl, a1);
+            at.Sb = exp2_acc_masked<SAFE>(sb1, at.Sb, sm.tbl, b1);
             at.ca += static_cast<uint32_t>(a0) + static_cast<uint32_t>(a1);
             at.cb += static_cast<uint32_t>(b0) + static_cast<uint32_t>(b1);
             if (DEBUG) {
@@ -1014,8 +1033,8 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const Region& R, c
             const int t0 = v0 ? list[i] : list[0];
             const int t1 = v1 ? list[i + 1] : t0;
             bool a0, bb0, a1, bb1, da0, db0, da1, db1;
-            fused_test(sm, A, R, at, t0, v0, a0, bb0, da0, db0);
-            fused_test(sm, A, R, at, t1, v1, a1, bb1, da1, db1);
+            fused_test(sm, at, t0, v0, a0, bb0, da0, db0);
+            fused_test(sm, at, t1, v1, a1, bb1, da1, db1);
             if (__any_sync(0xffffffffu, da0 || db0 || da1 || db1)) {
               if (da0 || db0) fused_exact(sm, A, at, t0, da0, db0, a0, bb0);
               if (da1 || db1) fused_exact(sm, A, at, t1, da1, db1, a1, bb1);
@@ -1027,12 +1046,12 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const Region& R, c
               const double4 y1 = sm.tD[t1];
               double sa0 = chain3(at.Xa, y0), sb0 = chain3(at.Xb, y0);
               double sa1 = chain3(at.Xa, y1), sb1 = chain3(at.Xb, y1);
-              if (WIDE) {
+              if (wide) {
                 sa0 -= at.xsqa; sa1 -= at.xsqa;
                 sb0 -= at.xsqb; sb1 -= at.xsqb;
               }
-              v[2 * p] = exp2_pair_weighted(sa0, sb0, at.wa, at.wb, sm.tbl, a0, bb0);
-              v[2 * p + 1] = exp2_pair_weighted(sa1, sb1, at.wa, at.wb, sm.tbl, a1, bb1);
+              v[2 * p] = exp2_pair_weighted<SAFE>(sa0, sb0, at.wa, at.wb, sm.tbl, a0, bb0);
+              v[2 * p + 1] = exp2_pair_weighted<SAFE>(sa1, sb1, at.wa, at.wb, sm.tbl, a1, bb1);
             }
           }
           const double tot = butterfly16(v);
@@ -1054,8 +1073,10 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const Region& R, c
 
 // Exact LSE (reference per-atom max shift) of one atom by the whole warp,
 // and, for the gradient, its exact contributions p_qj m_q into gacc.
-__device__ void warp_exact_atom(const FusedArgs& A, const double x[3], double m, double& L) {
+__device__ __noinline__ void warp_exact_atom(const FusedArgs& A, double x0, double x1, double x2,
+                                             double m, double* L_out) {
   const int lane = threadIdx.x & 31;
+  const double x[3] = {x0, x1, x2};
   int c_lo[3], c_hi[3];
   for (int d = 0; d < 3; ++d) {
     c_lo[d] = cell_of(A.g, d, x[d] - A.r_scan);
@@ -1070,7 +1091,7 @@ __device__ void warp_exact_atom(const FusedArgs& A, const double x[3], double m,
         const int b = A.cell_start[row + c_lo[0]], e = A.cell_start[row + c_hi[0] + 1];
         for (int k = b + lane; k < e; k += 32) {
           const double4 y = A.ys[k];
-          const double d2 = exact_sqdist(x[0], x[1], x[2], y.x, y.y, y.z);
+          const double d2 = exact_sqdist(x0, x1, x2, y.x, y.y, y.z);
           if (!(d2 < A.r2)) continue;
           const int j = A.tperm[k];
           const double ex = reference_exponent(A.psi[j], d2, A.eps, y.w);
@@ -1082,18 +1103,29 @@ __device__ void warp_exact_atom(const FusedArgs& A, const double x[3], double m,
     if (pass == 0) mx = warp_max(acc);
     else if (pass == 1) sum = warp_sum(acc);
   }
-  L = mx + log(sum);
+  *L_out = mx + log(sum);
+}
+
+__device__ __noinline__ void warp_nearest_fallback(const FusedArgs& A, double px, double py,
+                                                   double pz, double pm, double* L_out,
+                                                   int* j_out) {
+  double bd;
+  int bj, bk;
+  warp_nearest(A.g, A.ys, A.tperm, A.cell_start, px, py, pz, bd, bj, bk);
+  *L_out = reference_exponent(A.psi[bj], bd, A.eps, A.ys[bk].w);
+  *j_out = bj;
+  if ((threadIdx.x & 31) == 0) fp_add(A.gacc + 3 * static_cast<size_t>(bj), pm);
 }
 
 // Per-atom finalisation between the phases (all lanes of the warp call it:
 // empty and flagged atoms are resolved warp-cooperatively).
 template <bool DEBUG>
-__device__ __forceinline__ void fused_finalize(const FusedArgs& A, const Region& R, double B,
-                                               bool valid, uint32_t c, double S, double xsq,
-                                               const double4& p, const double (&x)[3],
-                                               uint64_t hash, int q, double (&W)[6]) {
+__device__ __forceinline__ void fused_finalize(const FusedArgs& A, double B, bool wide, bool valid,
+                                               uint32_t c, double S, double xsq, int q,
+                                               uint64_t hash, double (&W)[6]) {
   const int lane = threadIdx.x & 31;
-  const double shift = R.wide ? 0.0 : xsq;
+  const double4 p = valid ? A.xs[q] : make_double4(0, 0, 0, 0);
+  const double shift = wide ? 0.0 : xsq;
   const double m = p.w;
   const bool empty = valid && c == 0;
   const bool flag = valid && c > 0 && (!(S >= 0x1p-960) || !(S <= 0x1p960));
@@ -1103,30 +1135,23 @@ __device__ __forceinline__ void fused_finalize(const FusedArgs& A, const Region&
   while (me) {
     const int l = __ffs(me) - 1;
     me &= me - 1;
-    const double px = __shfl_sync(0xffffffffu, x[0], l);
-    const double py = __shfl_sync(0xffffffffu, x[1], l);
-    const double pz = __shfl_sync(0xffffffffu, x[2], l);
-    const double pm = __shfl_sync(0xffffffffu, m, l);
-    double bd;
-    int bj, bk;
-    warp_nearest(A.g, A.ys, A.tperm, A.cell_start, px, py, pz, bd, bj, bk);
+    double Lx;
+    int bj;
+    warp_nearest_fallback(A, __shfl_sync(0xffffffffu, p.x, l), __shfl_sync(0xffffffffu, p.y, l),
+                          __shfl_sync(0xffffffffu, p.z, l), __shfl_sync(0xffffffffu, m, l), &Lx,
+                          &bj);
     if (lane == l) {
-      L = reference_exponent(A.psi[bj], bd, A.eps, A.ys[bk].w);
+      L = Lx;
       if (DEBUG) hash = candidate_hash_term(static_cast<uint64_t>(bj));
     }
-    if (lane == 0) fp_add(A.gacc + 3 * static_cast<size_t>(bj), pm);
   }
   unsigned mf = __ballot_sync(0xffffffffu, flag);
   while (mf) {
     const int l = __ffs(mf) - 1;
     mf &= mf - 1;
-    double px[3];
-    px[0] = __shfl_sync(0xffffffffu, x[0], l);
-    px[1] = __shfl_sync(0xffffffffu, x[1], l);
-    px[2] = __shfl_sync(0xffffffffu, x[2], l);
-    const double pm = __shfl_sync(0xffffffffu, m, l);
     double Lx;
-    warp_exact_atom(A, px, pm, Lx);
+    warp_exact_atom(A, __shfl_sync(0xffffffffu, p.x, l), __shfl_sync(0xffffffffu, p.y, l),
+                    __shfl_sync(0xffffffffu, p.z, l), __shfl_sync(0xffffffffu, m, l), &Lx);
     if (lane == l) {
       L = Lx;
       w = 0.0;  // its gradient contributions are already in gacc
@@ -1153,63 +1178,68 @@ trunc_fused(FusedArgs A) {
   __shared__ FusedSmem sm;
   load_exp2_table(sm.tbl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qa = blockIdx.x * kFA + warp * 64 + lane, qb = qa + 32;
   FusedAtoms at;
-  at.va = qa < A.nq;
-  at.vb = qb < A.nq;
-  const double4 pa = at.va ? A.xs[qa] : make_double4(0, 0, 0, 0);
-  const double4 pb = at.vb ? A.xs[qb] : make_double4(0, 0, 0, 0);
-  at.xa[0] = pa.x; at.xa[1] = pa.y; at.xa[2] = pa.z;
-  at.xb[0] = pb.x; at.xb[1] = pb.y; at.xb[2] = pb.z;
-  double lo[3], hi[3];
-  for (int d = 0; d < 3; ++d) {
-    lo[d] = fmin(at.va ? at.xa[d] : INFINITY, at.vb ? at.xb[d] : INFINITY);
-    hi[d] = fmax(at.va ? at.xa[d] : -INFINITY, at.vb ? at.xb[d] : -INFINITY);
+  at.qa = blockIdx.x * kFA + warp * 64 + lane;
+  at.qb = at.qa + 32;
+  const bool va = at.qa < A.nq, vb = at.qb < A.nq;
+  double4 pa = va ? A.xs[at.qa] : make_double4(0, 0, 0, 0);
+  double4 pb = vb ? A.xs[at.qb] : make_double4(0, 0, 0, 0);
+  {
+    double lo[3], hi[3];
+    lo[0] = fmin(va ? pa.x : INFINITY, vb ? pb.x : INFINITY);
+    lo[1] = fmin(va ? pa.y : INFINITY, vb ? pb.y : INFINITY);
+    lo[2] = fmin(va ? pa.z : INFINITY, vb ? pb.z : INFINITY);
+    hi[0] = fmax(va ? pa.x : -INFINITY, vb ? pb.x : -INFINITY);
+    hi[1] = fmax(va ? pa.y : -INFINITY, vb ? pb.y : -INFINITY);
+    hi[2] = fmax(va ? pa.z : -INFINITY, vb ? pb.z : -INFINITY);
+    Region R;
+    setup_region(A.g, lo, hi, A.r2, A.r_scan, A.c2, sm.sh, R);
+    if (threadIdx.x == 0) sm.R = R;
+    __syncthreads();
   }
-  Region R;
-  setup_region(A.g, lo, hi, A.r2, A.r_scan, A.c2, sm.sh, R);
-  double xl[3], yl[3];
-  for (int d = 0; d < 3; ++d) {
-    xl[d] = at.xa[d] - R.o[d];
-    yl[d] = at.xb[d] - R.o[d];
-    at.Xa[d] = 2.0 * A.c2 * xl[d];
-    at.Xb[d] = 2.0 * A.c2 * yl[d];
-  }
-  at.xsqa = A.c2 * fma(xl[2], xl[2], fma(xl[1], xl[1], xl[0] * xl[0]));
-  at.xsqb = A.c2 * fma(yl[2], yl[2], fma(yl[1], yl[1], yl[0] * yl[0]));
+  const double o0 = sm.R.o[0], o1 = sm.R.o[1], o2 = sm.R.o[2];
+  const double ax = pa.x - o0, ay = pa.y - o1, az = pa.z - o2;
+  const double bx = pb.x - o0, by = pb.y - o1, bz = pb.z - o2;
+  const double c2x2 = 2.0 * A.c2;
+  at.Xa[0] = c2x2 * ax; at.Xa[1] = c2x2 * ay; at.Xa[2] = c2x2 * az;
+  at.Xb[0] = c2x2 * bx; at.Xb[1] = c2x2 * by; at.Xb[2] = c2x2 * bz;
+  at.xsqa = A.c2 * fma(az, az, fma(ay, ay, ax * ax));
+  at.xsqb = A.c2 * fma(bz, bz, fma(by, by, bx * bx));
   const float big = 1e30f;
-  at.F0 = make_float2(at.va ? static_cast<float>(xl[0]) : big, at.vb ? static_cast<float>(yl[0]) : big);
-  at.F1 = make_float2(at.va ? static_cast<float>(xl[1]) : big, at.vb ? static_cast<float>(yl[1]) : big);
-  at.F2 = make_float2(at.va ? static_cast<float>(xl[2]) : big, at.vb ? static_cast<float>(yl[2]) : big);
+  at.F0 = make_float2(va ? static_cast<float>(ax) : big, vb ? static_cast<float>(bx) : big);
+  at.F1 = make_float2(va ? static_cast<float>(ay) : big, vb ? static_cast<float>(by) : big);
+  at.F2 = make_float2(va ? static_cast<float>(az) : big, vb ? static_cast<float>(bz) : big);
+  at.lo_thr = sm.R.lo_thr;
+  at.hi_thr = sm.R.hi_thr;
   at.Sa = at.Sb = 0.0;
   at.ca = at.cb = 0;
   at.ha = at.hb = 0;
-  // warp box over both atoms of every lane
   WarpBox wb;
   {
-    const WarpBox w1 = warp_box(at.va, at.F0.x, at.F1.x, at.F2.x);
-    const WarpBox w2 = warp_box(at.vb, at.F0.y, at.F1.y, at.F2.y);
+    const WarpBox w1 = warp_box(va, at.F0.x, at.F1.x, at.F2.x);
+    const WarpBox w2 = warp_box(vb, at.F0.y, at.F1.y, at.F2.y);
     wb.lo0 = fminf(w1.lo0, w2.lo0); wb.lo1 = fminf(w1.lo1, w2.lo1); wb.lo2 = fminf(w1.lo2, w2.lo2);
     wb.hi0 = fmaxf(w1.hi0, w2.hi0); wb.hi1 = fmaxf(w1.hi1, w2.hi1); wb.hi2 = fmaxf(w1.hi2, w2.hi2);
   }
-  const float cull_thr = R.hi_thr * 1.0001f;
+  const float cull_thr = sm.R.hi_thr * 1.0001f;
   const double B = A.scal[kSlotB];
+  // Exponents of taken pairs lie in [bmin - B - c2 r^2, c2 |x'|^2] (shifted)
+  // or [bmin - B - c2 r^2, 0] (wide); outside [-1000, 400] use the safe path.
+  const bool wide = sm.R.wide;
+  const bool safe = wide || (A.scal[kSlotBmin] - B) - A.c2 * A.r2 < -1000.0;
 
-  // ---- phase 1: S~ ----
-  if (R.wide)
-    fused_scan<1, true, DEBUG>(sm, A, R, wb, cull_thr, B, at);
+  if (safe)
+    fused_scan<1, true, DEBUG>(sm, A, wb, cull_thr, B, at);
   else
-    fused_scan<1, false, DEBUG>(sm, A, R, wb, cull_thr, B, at);
+    fused_scan<1, false, DEBUG>(sm, A, wb, cull_thr, B, at);
 
-  // ---- finalise atoms; empty sets and flagged sums (warp cooperative) ----
-  fused_finalize<DEBUG>(A, R, B, at.va, at.ca, at.Sa, at.xsqa, pa, at.xa, at.ha, qa, at.wa);
-  fused_finalize<DEBUG>(A, R, B, at.vb, at.cb, at.Sb, at.xsqb, pb, at.xb, at.hb, qb, at.wb);
+  fused_finalize<DEBUG>(A, B, wide, va, at.ca, at.Sa, at.xsqa, at.qa, at.ha, at.wa);
+  fused_finalize<DEBUG>(A, B, wide, vb, at.cb, at.Sb, at.xsqb, at.qb, at.hb, at.wb);
 
-  // ---- phase 2: gradient ----
-  if (R.wide)
-    fused_scan<2, true, DEBUG>(sm, A, R, wb, cull_thr, B, at);
+  if (safe)
+    fused_scan<2, true, DEBUG>(sm, A, wb, cull_thr, B, at);
   else
-    fused_scan<2, false, DEBUG>(sm, A, R, wb, cull_thr, B, at);
+    fused_scan<2, false, DEBUG>(sm, A, wb, cull_thr, B, at);
 }
 
 __global__ void trunc_assemble_fp(const unsigned long long* __restrict__ gacc, int n,

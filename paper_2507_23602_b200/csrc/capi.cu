@@ -129,6 +129,16 @@ struct rsot_cuda_atoms {
 
 namespace {
 
+DeviceTargets make_dt(const rsot_cuda_targets* t) {
+  DeviceTargets d;
+  d.y = t->y;
+  d.nu = t->nu;
+  d.n = static_cast<int>(t->n);
+  d.lo = make_double3(t->cells.bbox_lo[0], t->cells.bbox_lo[1], t->cells.bbox_lo[2]);
+  d.hi = make_double3(t->cells.bbox_hi[0], t->cells.bbox_hi[1], t->cells.bbox_hi[2]);
+  return d;
+}
+
 int set_device(rsot_cuda_ctx* ctx) {
   RSOT_CK(cudaSetDevice(ctx->device));
   return RSOT_CUDA_OK;
@@ -179,7 +189,7 @@ EvalBuffers buffers(rsot_cuda_ctx* c, double* g_out, double* scalars_out) {
 int enqueue_eval(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
                  EvalBuffers& b, double eps, double cutoff, DebugOut* dbg) {
   const cudaStream_t s = c->stream;
-  DeviceTargets dt{t->y, t->nu, static_cast<int>(t->n)};
+  const DeviceTargets dt = make_dt(t);
   DeviceAtoms da{a->x, static_cast<int>(a->nq)};
   if (b.timing) cudaEventRecord(b.timing[0], s);
   launch_prologue(dt, b, eps, s);
@@ -540,7 +550,7 @@ int rsot_cuda_nearest(rsot_cuda_ctx* c, rsot_cuda_targets* t, const double* xyz,
   int rc = set_device(c);
   if (rc) return rc;
   if (m == 0) return RSOT_CUDA_OK;
-  rc = run_nearest_points(c->trunc, DeviceTargets{t->y, t->nu, static_cast<int>(t->n)},
+  rc = run_nearest_points(c->trunc, make_dt(t),
                           t->cells, xyz, m, out, c->stream, g_last_error);
   return rc ? fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error) : RSOT_CUDA_OK;
 }
@@ -552,7 +562,7 @@ int rsot_cuda_covering_cost(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targ
   if (!out) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
   double c0 = 0.0;
   rc = run_covering_cost(c->trunc, DeviceAtoms{a->x, static_cast<int>(a->nq)},
-                         DeviceTargets{t->y, t->nu, static_cast<int>(t->n)}, t->cells,
+                         make_dt(t), t->cells,
                          &c0, c->stream, g_last_error);
   if (rc) return fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error);
   if (c->comm) {

@@ -105,7 +105,7 @@ __global__ void prologue_final(const double* __restrict__ part, int nblk,
 // the per-atom shift -c2|x'|^2 to every exponent (one extra DADD per pair);
 // it is used only when the CTA's atoms are spread so widely that the
 // shifted exponent could overflow (c2 * half-diagonal^2 > 400).
-template <int APT, bool WIDE>
+template <int APT, bool WIDE, bool CLAMP>
 __device__ __forceinline__ void passA_tile(const double4* __restrict__ tile, int cnt,
                                            const double (&X)[APT][3], const double (&sub)[APT],
                                            double (&S)[APT], const int2* __restrict__ tbl) {
@@ -116,7 +116,7 @@ __device__ __forceinline__ void passA_tile(const double4* __restrict__ tile, int
     for (int k = 0; k < APT; ++k) {
       double s = fma(X[k][0], y.x, fma(X[k][1], y.y, fma(X[k][2], y.z, y.w)));
       if (WIDE) s -= sub[k];
-      S[k] = exp2_acc(s, S[k], tbl);
+      S[k] = exp2_acc<CLAMP>(s, S[k], tbl);
     }
   }
 }
@@ -126,8 +126,9 @@ __global__ void __launch_bounds__(kThreads)
 dense_passA(const double4* __restrict__ atoms, int nq,
             const double4* __restrict__ tgt, const double* __restrict__ b2,
             int n, int per_split, const double* __restrict__ scal, double c2,
-            double* __restrict__ partS, double* __restrict__ shiftA) {
+            double* __restrict__ partS, double* __restrict__ shiftA, double3 tlo, double3 thi) {
   __shared__ double4 tile[kTile];
+  __shared__ double4 tile2[kTile];
   __shared__ int2 tbl[16];
   __shared__ double sh[200];
   load_exp2_table(tbl);
@@ -160,6 +161,13 @@ dense_passA(const double4* __restrict__ atoms, int nq,
   }
   const bool wide = c2 * hd2 > 400.0;
   const double B = scal[kSlotB];
+  // Exponents lie in [bmin - B - c2 maxd2, c2 hd2]; clamp only if that can
+  // leave [-1000, 400] (maxd2: farthest target-bbox corner from the box).
+  const double mx0 = fmax(thi.x - box[0], box[3] - tlo.x);
+  const double mx1 = fmax(thi.y - box[1], box[4] - tlo.y);
+  const double mx2 = fmax(thi.z - box[2], box[5] - tlo.z);
+  const double maxd2 = fma(mx2, mx2, fma(mx1, mx1, mx0 * mx0));
+  const bool safe = wide || (scal[kSlotBmin] - B) - c2 * maxd2 < -1000.0;
   const double c2x2 = 2.0 * c2;
   double X[APT][3], S[APT], sub[APT];
 #pragma unroll
@@ -176,22 +184,56 @@ dense_passA(const double4* __restrict__ atoms, int nq,
 
   const int j0 = blockIdx.y * per_split;
   const int j1 = min(n, j0 + per_split);
+  // Double-buffered target tiles: the next tile's global loads are issued
+  // before the current tile's compute and staged after it (one barrier per
+  // tile, load latency hidden behind FP64 work).
+  constexpr int kPer = kTile / kThreads;
+  double4 pre_y[kPer];
+  double pre_b[kPer];
+  auto fetch = [&](int base) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int j = base + threadIdx.x + u * kThreads;
+      if (j < j1) {
+        pre_y[u] = tgt[j];
+        pre_b[u] = b2[j];
+      }
+    }
+  };
+  auto stage = [&](double4* dst, int base) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int t = threadIdx.x + u * kThreads;
+      if (base + t < j1) {
+        const double y0 = pre_y[u].x - o[0], y1 = pre_y[u].y - o[1], y2 = pre_y[u].z - o[2];
+        const double yy = fma(y2, y2, fma(y1, y1, y0 * y0));
+        const double w = fmax(fma(-c2, yy, pre_b[u]) - B, -1.0e5);  // nu_j = 0 => 0
+        dst[t] = make_double4(y0, y1, y2, w);
+      }
+    }
+  };
+  if (j0 < j1) {
+    fetch(j0);
+    stage(tile, j0);
+  }
+  __syncthreads();
+  int buf = 0;
   for (int base = j0; base < j1; base += kTile) {
     const int cnt = min(kTile, j1 - base);
-    __syncthreads();
-    for (int t = threadIdx.x; t < cnt; t += kThreads) {
-      const double4 y = tgt[base + t];
-      const double y0 = y.x - o[0], y1 = y.y - o[1], y2 = y.z - o[2];
-      const double yy = fma(y2, y2, fma(y1, y1, y0 * y0));
-      double w = fma(-c2, yy, b2[base + t]) - B;
-      w = fmax(w, -1.0e5);  // nu_j = 0 => b2 = -inf: contributes 0
-      tile[t] = make_double4(y0, y1, y2, w);
+    const bool more = base + kTile < j1;
+    if (more) fetch(base + kTile);
+    const double4* cur = buf ? tile2 : tile;
+    if (safe) {
+      if (wide)
+        passA_tile<APT, true, true>(cur, cnt, X, sub, S, tbl);
+      else
+        passA_tile<APT, false, true>(cur, cnt, X, sub, S, tbl);
+    } else {
+      passA_tile<APT, false, false>(cur, cnt, X, sub, S, tbl);
     }
+    if (more) stage(buf ? tile : tile2, base + kTile);
+    buf ^= 1;
     __syncthreads();
-    if (wide)
-      passA_tile<APT, true>(tile, cnt, X, sub, S, tbl);
-    else
-      passA_tile<APT, false>(tile, cnt, X, sub, S, tbl);
   }
 #pragma unroll
   for (int k = 0; k < APT; ++k) {
@@ -287,6 +329,7 @@ dense_passB(const double4* __restrict__ atoms, const double* __restrict__ atomLa
             const double* __restrict__ b2, int n, double c2,
             double* __restrict__ partG) {
   __shared__ double4 tile[kTile];
+  __shared__ double4 tile2[kTile];
   __shared__ int2 tbl[16];
   __shared__ double sh[200];
   load_exp2_table(tbl);
@@ -321,26 +364,53 @@ dense_passB(const double4* __restrict__ atoms, const double* __restrict__ atomLa
   const double c2x2 = 2.0 * c2;
   const int q0 = blockIdx.y * per_split;
   const int q1 = min(nq, q0 + per_split);
+  constexpr int kPer = kTile / kThreads;
+  double4 pre_x[kPer];
+  double pre_l[kPer];
+  auto fetch = [&](int base) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int q = base + threadIdx.x + u * kThreads;
+      if (q < q1) {
+        pre_x[u] = atoms[q];
+        pre_l[u] = atomLam[q];
+      }
+    }
+  };
+  auto stage = [&](double4* dst, int base) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int t = threadIdx.x + u * kThreads;
+      if (base + t < q1) {
+        const double x0 = pre_x[u].x - o[0], x1 = pre_x[u].y - o[1], x2 = pre_x[u].z - o[2];
+        const double xx = fma(x2, x2, fma(x1, x1, x0 * x0));
+        dst[t] = make_double4(c2x2 * x0, c2x2 * x1, c2x2 * x2, fma(-c2, xx, pre_l[u]));
+      }
+    }
+  };
+  if (q0 < q1) {
+    fetch(q0);
+    stage(tile, q0);
+  }
+  __syncthreads();
+  int buf = 0;
   for (int base = q0; base < q1; base += kTile) {
     const int cnt = min(kTile, q1 - base);
-    __syncthreads();
-    for (int t = threadIdx.x; t < cnt; t += kThreads) {
-      const double4 a = atoms[base + t];
-      const double x0 = a.x - o[0], x1 = a.y - o[1], x2 = a.z - o[2];
-      const double xx = fma(x2, x2, fma(x1, x1, x0 * x0));
-      const double A = fma(-c2, xx, atomLam[base + t]);
-      tile[t] = make_double4(c2x2 * x0, c2x2 * x1, c2x2 * x2, A);
-    }
-    __syncthreads();
+    const bool more = base + kTile < q1;
+    if (more) fetch(base + kTile);
+    const double4* cur = buf ? tile2 : tile;
 #pragma unroll 4
     for (int t = 0; t < cnt; ++t) {
-      const double4 X = tile[t];
+      const double4 X = cur[t];
 #pragma unroll
       for (int k = 0; k < TPT; ++k) {
         const double s = fma(X.x, y[k][0], fma(X.y, y[k][1], fma(X.z, y[k][2], T[k] + X.w)));
         G[k] = exp2_acc(s, G[k], tbl);
       }
     }
+    if (more) stage(buf ? tile : tile2, base + kTile);
+    buf ^= 1;
+    __syncthreads();
   }
 #pragma unroll
   for (int k = 0; k < TPT; ++k) {
@@ -475,10 +545,10 @@ void launch_dense(const DeviceAtoms& a, const DeviceTargets& t, EvalBuffers& b,
     if (b.timing) cudaEventRecord(b.timing[1], s);
     if (p.apt == 2)
       (note_launch(), dense_passA<2><<<gA, kThreads, 0, s>>>(a.x, nq, t.y, b.b2, n, per_split,
-                                              b.scal, c2, b.partS, b.shiftA));
+                                              b.scal, c2, b.partS, b.shiftA, t.lo, t.hi));
     else
       (note_launch(), dense_passA<1><<<gA, kThreads, 0, s>>>(a.x, nq, t.y, b.b2, n, per_split,
-                                              b.scal, c2, b.partS, b.shiftA));
+                                              b.scal, c2, b.partS, b.shiftA, t.lo, t.hi));
     if (b.timing) cudaEventRecord(b.timing[2], s);
     (note_launch(), dense_finalizeA<<<(nq + 255) / 256, 256, 0, s>>>(
         a.x, nq, b.partS, splitsA, b.shiftA, b.scal, eps, b.atomL, b.atomLam,

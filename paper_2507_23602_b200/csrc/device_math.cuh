@@ -59,10 +59,12 @@ __device__ __forceinline__ void load_exp2_table(int2* smem_tbl) {
 // (the reference would add a subnormal or zero); s above 1000 yields at least
 // 2^999, which the callers detect (sum > 2^960) and route to the exact
 // per-atom path.  FP64 pipe: 3 DADD + 6 DFMA; INT: 2 IMNMX, LOP3, LEA, IMAD.
+template <bool CLAMP = true>
 __device__ __forceinline__ double exp2_acc(double s, double acc,
                                            const int2* __restrict__ tbl) {
   const double kk = __dadd_rn(s, kExpMagic);
-  const int n = min(max(__double2loint(kk), -16320), 16000);  // round(16 s)
+  int n = __double2loint(kk);  // round(16 s)
+  if (CLAMP) n = min(max(n, -16320), 16000);
   const double kd = __dadd_rn(kk, -kExpMagic);
   const double r = __dadd_rn(s, -kd);        // |r| <= 1/32
   double p = fma(kP5, r, kP4);

@@ -45,6 +45,7 @@ struct DeviceTargets {
   const double4* y;   // {y0, y1, y2, ln nu}
   const double* nu;
   int n;
+  double3 lo, hi;     // bounding box of the target points
 };
 
 struct DeviceAtoms {

@@ -11,7 +11,7 @@ import os
 from ctypes import POINTER, c_char_p, c_double, c_int, c_size_t, c_uint8, c_uint32, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "librsot_b200.so")
+LIB_PATH = os.environ.get("RSOT_LIB_PATH") or os.path.join(_HERE, "lib", "librsot_b200.so")
 
 RSOT_CUDA_OK = 0
 RSOT_CUDA_INVALID_ARGUMENT = -1

@@ -809,7 +809,7 @@ struct FusedAtoms {
   double Sa, Sb;             // phase 1 sums
   uint32_t ca, cb;           // candidate counts
   uint64_t ha, hb;           // candidate hashes (debug)
-  double wa[6], wb[6];       // phase 2: polynomial coefficients x m/S~
+  double wa, wb;             // phase 2: m_q / S~_q (0 for empty / exact-path atoms)
 };
 
 struct FusedArgs {
@@ -828,10 +828,10 @@ __device__ __forceinline__ double chain3(const double (&X)[3], const double4& y)
   return fma(X[0], y.x, fma(X[1], y.y, fma(X[2], y.z, y.w)));
 }
 
-// w_a 2^sa [ta] + w_b 2^sb [tb] with per-atom scaled polynomials.
+// w_a 2^sa [ta] + w_b 2^sb [tb] (the weights multiply the table scales:
+// one DMUL each, fewer live registers than per-atom scaled polynomials).
 template <bool CLAMP>
-__device__ __forceinline__ double exp2_pair_weighted(double sa, double sb, const double (&pa)[6],
-                                                     const double (&pb)[6],
+__device__ __forceinline__ double exp2_pair_weighted(double sa, double sb, double wa, double wb,
                                                      const int2* __restrict__ tbl, bool ta,
                                                      bool tb) {
   const double kka = __dadd_rn(sa, kExpMagic);
@@ -844,22 +844,22 @@ __device__ __forceinline__ double exp2_pair_weighted(double sa, double sb, const
   }
   const double ra = __dadd_rn(sa, -__dadd_rn(kka, -kExpMagic));
   const double rb = __dadd_rn(sb, -__dadd_rn(kkb, -kExpMagic));
-  double qa = fma(pa[5], ra, pa[4]);
-  double qb = fma(pb[5], rb, pb[4]);
-  qa = fma(qa, ra, pa[3]);
-  qb = fma(qb, rb, pb[3]);
-  qa = fma(qa, ra, pa[2]);
-  qb = fma(qb, rb, pb[2]);
-  qa = fma(qa, ra, pa[1]);
-  qb = fma(qb, rb, pb[1]);
-  qa = fma(qa, ra, pa[0]);
-  qb = fma(qb, rb, pb[0]);
+  double qa = fma(kP5, ra, kP4);
+  double qb = fma(kP5, rb, kP4);
+  qa = fma(qa, ra, kP3);
+  qb = fma(qb, rb, kP3);
+  qa = fma(qa, ra, kP2);
+  qb = fma(qb, rb, kP2);
+  qa = fma(qa, ra, kP1);
+  qb = fma(qb, rb, kP1);
+  qa = fma(qa, ra, kP0);
+  qb = fma(qb, rb, kP0);
   na = ta ? na : -16368;  // scale word pattern 0 -> +0.0
   nb = tb ? nb : -16368;
   const int2 Ta = tbl[na & 15];
   const int2 Tb = tbl[nb & 15];
-  const double sca = __hiloint2double(Ta.y + na * 65536, Ta.x);
-  const double scb = __hiloint2double(Tb.y + nb * 65536, Tb.x);
+  const double sca = __hiloint2double(Ta.y + na * 65536, Ta.x) * wa;
+  const double scb = __hiloint2double(Tb.y + nb * 65536, Tb.x) * wb;
   return fma(qa, sca, qb * scb);
 }
 
@@ -1122,7 +1122,7 @@ __device__ __noinline__ void warp_nearest_fallback(const FusedArgs& A, double px
 template <bool DEBUG>
 __device__ __forceinline__ void fused_finalize(const FusedArgs& A, double B, bool wide, bool valid,
                                                uint32_t c, double S, double xsq, int q,
-                                               uint64_t hash, double (&W)[6]) {
+                                               uint64_t hash, double& W) {
   const int lane = threadIdx.x & 31;
   const double4 p = valid ? A.xs[q] : make_double4(0, 0, 0, 0);
   const double shift = wide ? 0.0 : xsq;
@@ -1157,8 +1157,7 @@ __device__ __forceinline__ void fused_finalize(const FusedArgs& A, double B, boo
       w = 0.0;  // its gradient contributions are already in gacc
     }
   }
-  W[0] = kP0 * w; W[1] = kP1 * w; W[2] = kP2 * w;
-  W[3] = kP3 * w; W[4] = kP4 * w; W[5] = kP5 * w;
+  W = w;
   if (valid) {
     A.atomJ[q] = A.eps * L * m;
     A.atomD[q] = m * exp(-L);
@@ -1173,7 +1172,7 @@ __device__ __forceinline__ void fused_finalize(const FusedArgs& A, double B, boo
 }
 
 template <bool DEBUG>
-__global__ void __launch_bounds__(kT, 3)
+__global__ void __launch_bounds__(kT, 4)
 trunc_fused(FusedArgs A) {
   __shared__ FusedSmem sm;
   load_exp2_table(sm.tbl);

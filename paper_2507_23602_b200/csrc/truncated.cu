@@ -807,7 +807,9 @@ struct FusedAtoms {
   float lo_thr, hi_thr;      // FP32 decision thresholds
   int qa, qb;                // Hilbert positions of the two atoms
   double Sa, Sb;             // phase 1 sums
-  uint32_t ca, cb;           // candidate counts
+  uint32_t tot;              // accepted pairs of both atoms
+  unsigned anyf;             // OR of the pair masks (bits 0/2: atom a, 1/3: atom b)
+  uint32_t ca, cb;           // per-atom candidate counts (debug builds)
   uint64_t ha, hb;           // candidate hashes (debug)
   double wa, wb;             // phase 2: m_q / S~_q (0 for empty / exact-path atoms)
 };
@@ -926,10 +928,8 @@ __device__ __forceinline__ int fused_cull(const FusedSmem& sm, int cnt, const Wa
   return nsel;
 }
 
-// Packed FP32x2 pre-test of one item against both atoms.
-__device__ __forceinline__ void fused_test(const FusedSmem& sm, const FusedAtoms& at, int t,
-                                          bool valid_item, bool& ina, bool& inb, bool& bda,
-                                          bool& bdb) {
+// Packed FP32x2 squared distances of item t to the thread's atoms (a, b).
+__device__ __forceinline__ float2 fused_d2(const FusedSmem& sm, const FusedAtoms& at, int t) {
   const float4 n01 = sm.tN0[t];
   const float2 n2 = sm.tN1[t];
   const float2 dx = __fadd2_rn(at.F0, make_float2(n01.x, n01.y));
@@ -937,25 +937,33 @@ __device__ __forceinline__ void fused_test(const FusedSmem& sm, const FusedAtoms
   const float2 dz = __fadd2_rn(at.F2, n2);
   float2 d2 = __fmul2_rn(dx, dx);
   d2 = __ffma2_rn(dy, dy, d2);
-  d2 = __ffma2_rn(dz, dz, d2);
-  ina = valid_item && d2.x < at.lo_thr;
-  inb = valid_item && d2.y < at.lo_thr;
-  bda = valid_item && !ina && d2.x <= at.hi_thr;
-  bdb = valid_item && !inb && d2.y <= at.hi_thr;
+  return __ffma2_rn(dz, dz, d2);
 }
 
-// Exact reference predicate for pairs inside the FP32 error band (rare).
-__device__ __forceinline__ void fused_exact(const FusedSmem& sm, const FusedArgs& A,
-                                         const FusedAtoms& at, int t, bool bda, bool bdb,
-                                         bool& ina, bool& inb) {
-  const double4 yg = A.ys[sm.tK[t]];
-  if (bda) {
-    const double4 x = A.xs[at.qa];
-    ina = exact_inside(x.x, x.y, x.z, yg.x, yg.y, yg.z, A.r2);
-  }
-  if (bdb) {
-    const double4 x = A.xs[at.qb];
-    inb = exact_inside(x.x, x.y, x.z, yg.x, yg.y, yg.z, A.r2);
+__device__ __forceinline__ unsigned sign4(float2 u0, float2 u1) {
+  return (__float_as_uint(u0.x) >> 31) | ((__float_as_uint(u0.y) >> 31) << 1) |
+         ((__float_as_uint(u1.x) >> 31) << 2) | ((__float_as_uint(u1.y) >> 31) << 3);
+}
+
+// 4-bit pair masks for items (t0, t1) x atoms (a, b): bit 2i = atom a,
+// bit 2i+1 = atom b.  in: d2 < lo (sign of d2 - lo is exact); border:
+// lo <= d2 < hi (decided by the exact fp64 predicate).
+__device__ __forceinline__ void fused_masks(float2 d0, float2 d1, float2 nlo, float2 nhi, bool v1,
+                                            unsigned& in, unsigned& border) {
+  const unsigned keep = v1 ? 0xFu : 0x3u;
+  in = sign4(__fadd2_rn(d0, nlo), __fadd2_rn(d1, nlo)) & keep;
+  border = sign4(__fadd2_rn(d0, nhi), __fadd2_rn(d1, nhi)) & keep & ~in;
+}
+
+// Exact reference predicate for the pairs inside the FP32 error band (rare).
+__device__ __noinline__ void fused_exact(const FusedSmem& sm, const FusedArgs& A,
+                                         const FusedAtoms& at, int t0, int t1, unsigned border,
+                                         unsigned* in) {
+  for (int bit = 0; bit < 4; ++bit) {
+    if (!((border >> bit) & 1u)) continue;
+    const double4 yg = A.ys[sm.tK[bit < 2 ? t0 : t1]];
+    const double4 x = A.xs[(bit & 1) ? at.qb : at.qa];
+    if (exact_inside(x.x, x.y, x.z, yg.x, yg.y, yg.z, A.r2)) *in |= 1u << bit;
   }
 }
 
@@ -968,6 +976,8 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* const list = sm.wlist[warp];
   const bool wide = SAFE && sm.R.wide;
+  const float2 nlo = make_float2(-at.lo_thr, -at.lo_thr);
+  const float2 nhi = make_float2(-at.hi_thr, -at.hi_thr);
   const int ny = sm.R.c_hi[1] - sm.R.c_lo[1] + 1;
   const int nrows = ny * (sm.R.c_hi[2] - sm.R.c_lo[2] + 1);
   for (int rb = 0; rb < nrows; rb += kT) {
@@ -990,14 +1000,12 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
           const bool v1 = i + 1 < nsel;
           const int t0 = list[i];
           const int t1 = v1 ? list[i + 1] : t0;
-          bool a0, b0, a1, b1, da0, db0, da1, db1;
-          fused_test(sm, at, t0, true, a0, b0, da0, db0);
-          fused_test(sm, at, t1, v1, a1, b1, da1, db1);
-          if (__any_sync(0xffffffffu, da0 || db0 || da1 || db1)) {
-            if (da0 || db0) fused_exact(sm, A, at, t0, da0, db0, a0, b0);
-            if (da1 || db1) fused_exact(sm, A, at, t1, da1, db1, a1, b1);
+          unsigned in, bd;
+          fused_masks(fused_d2(sm, at, t0), fused_d2(sm, at, t1), nlo, nhi, v1, in, bd);
+          if (__any_sync(0xffffffffu, bd != 0u)) {
+            if (bd) fused_exact(sm, A, at, t0, t1, bd, &in);
           }
-          if (__any_sync(0xffffffffu, a0 || b0 || a1 || b1)) {
+          if (__any_sync(0xffffffffu, in != 0u)) {
             const double4 y0 = sm.tD[t0];
             const double4 y1 = sm.tD[t1];
             double sa0 = chain3(at.Xa, y0), sb0 = chain3(at.Xb, y0);
@@ -1006,17 +1014,19 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
               sa0 -= at.xsqa; sa1 -= at.xsqa;
               sb0 -= at.xsqb; sb1 -= at.xsqb;
             }
-            at.Sa = exp2_acc_masked<SAFE>(sa0, at.Sa, sm.tbl, a0);
-            at.Sb = exp2_acc_masked<SAFE>(sb0, at.Sb, sm.tbl, b0);
-            at.Sa = exp2_acc_masked<SAFE>(sa1, at.Sa, sm.tbl, a1);
-            at.Sb = exp2_acc_masked<SAFE>(sb1, at.Sb, sm.tbl, b1);
-            at.ca += static_cast<uint32_t>(a0) + static_cast<uint32_t>(a1);
-            at.cb += static_cast<uint32_t>(b0) + static_cast<uint32_t>(b1);
+            at.Sa = exp2_acc_masked<SAFE>(sa0, at.Sa, sm.tbl, in & 1u);
+            at.Sb = exp2_acc_masked<SAFE>(sb0, at.Sb, sm.tbl, in & 2u);
+            at.Sa = exp2_acc_masked<SAFE>(sa1, at.Sa, sm.tbl, in & 4u);
+            at.Sb = exp2_acc_masked<SAFE>(sb1, at.Sb, sm.tbl, in & 8u);
+            at.tot += __popc(in);
+            at.anyf |= in;
             if (DEBUG) {
-              if (a0) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
-              if (a1) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
-              if (b0) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
-              if (b1) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
+              at.ca += __popc(in & 5u);
+              at.cb += __popc(in & 10u);
+              if (in & 1u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
+              if (in & 4u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
+              if (in & 2u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
+              if (in & 8u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
             }
           }
         }
@@ -1032,16 +1042,15 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
             const bool v0 = i < nsel, v1 = i + 1 < nsel;
             const int t0 = v0 ? list[i] : list[0];
             const int t1 = v1 ? list[i + 1] : t0;
-            bool a0, bb0, a1, bb1, da0, db0, da1, db1;
-            fused_test(sm, at, t0, v0, a0, bb0, da0, db0);
-            fused_test(sm, at, t1, v1, a1, bb1, da1, db1);
-            if (__any_sync(0xffffffffu, da0 || db0 || da1 || db1)) {
-              if (da0 || db0) fused_exact(sm, A, at, t0, da0, db0, a0, bb0);
-              if (da1 || db1) fused_exact(sm, A, at, t1, da1, db1, a1, bb1);
+            unsigned in, bd;
+            fused_masks(fused_d2(sm, at, t0), fused_d2(sm, at, t1), nlo, nhi, v1, in, bd);
+            if (!v0) in = bd = 0u;
+            if (__any_sync(0xffffffffu, bd != 0u)) {
+              if (bd) fused_exact(sm, A, at, t0, t1, bd, &in);
             }
             v[2 * p] = 0.0;
             v[2 * p + 1] = 0.0;
-            if (__any_sync(0xffffffffu, a0 || bb0 || a1 || bb1)) {
+            if (__any_sync(0xffffffffu, in != 0u)) {
               const double4 y0 = sm.tD[t0];
               const double4 y1 = sm.tD[t1];
               double sa0 = chain3(at.Xa, y0), sb0 = chain3(at.Xb, y0);
@@ -1050,8 +1059,8 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
                 sa0 -= at.xsqa; sa1 -= at.xsqa;
                 sb0 -= at.xsqb; sb1 -= at.xsqb;
               }
-              v[2 * p] = exp2_pair_weighted<SAFE>(sa0, sb0, at.wa, at.wb, sm.tbl, a0, bb0);
-              v[2 * p + 1] = exp2_pair_weighted<SAFE>(sa1, sb1, at.wa, at.wb, sm.tbl, a1, bb1);
+              v[2 * p] = exp2_pair_weighted<SAFE>(sa0, sb0, at.wa, at.wb, sm.tbl, in & 1u, in & 2u);
+              v[2 * p + 1] = exp2_pair_weighted<SAFE>(sa1, sb1, at.wa, at.wb, sm.tbl, in & 4u, in & 8u);
             }
           }
           const double tot = butterfly16(v);
@@ -1121,16 +1130,17 @@ __device__ __noinline__ void warp_nearest_fallback(const FusedArgs& A, double px
 // empty and flagged atoms are resolved warp-cooperatively).
 template <bool DEBUG>
 __device__ __forceinline__ void fused_finalize(const FusedArgs& A, double B, bool wide, bool valid,
-                                               uint32_t c, double S, double xsq, int q,
-                                               uint64_t hash, double& W) {
+                                               bool nonempty, double cnt_contrib, uint32_t dbg_count,
+                                               double S, double xsq, int q, uint64_t hash,
+                                               double& W) {
   const int lane = threadIdx.x & 31;
   const double4 p = valid ? A.xs[q] : make_double4(0, 0, 0, 0);
   const double shift = wide ? 0.0 : xsq;
   const double m = p.w;
-  const bool empty = valid && c == 0;
-  const bool flag = valid && c > 0 && (!(S >= 0x1p-960) || !(S <= 0x1p960));
+  const bool empty = valid && !nonempty;
+  const bool flag = valid && nonempty && (!(S >= 0x1p-960) || !(S <= 0x1p960));
   double L = (B - shift + log2(S)) * kLn2;
-  double w = valid && c > 0 ? m / S : 0.0;
+  double w = valid && nonempty ? m / S : 0.0;
   unsigned me = __ballot_sync(0xffffffffu, empty);
   while (me) {
     const int l = __ffs(me) - 1;
@@ -1161,10 +1171,10 @@ __device__ __forceinline__ void fused_finalize(const FusedArgs& A, double B, boo
   if (valid) {
     A.atomJ[q] = A.eps * L * m;
     A.atomD[q] = m * exp(-L);
-    A.cntd[q] = c == 0 ? 1.0 : static_cast<double>(c);
-    A.emptyd[q] = c == 0 ? 1.0 : 0.0;
+    A.cntd[q] = empty ? 1.0 + cnt_contrib : cnt_contrib;
+    A.emptyd[q] = empty ? 1.0 : 0.0;
     if (DEBUG) {
-      A.dbg_cnt[q] = c == 0 ? 1u : c;
+      A.dbg_cnt[q] = empty ? 1u : dbg_count;
       A.dbg_hash[q] = hash;
       A.dbg_logs[q] = L;
     }
@@ -1211,6 +1221,8 @@ trunc_fused(FusedArgs A) {
   at.lo_thr = sm.R.lo_thr;
   at.hi_thr = sm.R.hi_thr;
   at.Sa = at.Sb = 0.0;
+  at.tot = 0;
+  at.anyf = 0;
   at.ca = at.cb = 0;
   at.ha = at.hb = 0;
   WarpBox wb;
@@ -1232,8 +1244,11 @@ trunc_fused(FusedArgs A) {
   else
     fused_scan<1, false, DEBUG>(sm, A, wb, cull_thr, B, at);
 
-  fused_finalize<DEBUG>(A, B, wide, va, at.ca, at.Sa, at.xsqa, at.qa, at.ha, at.wa);
-  fused_finalize<DEBUG>(A, B, wide, vb, at.cb, at.Sb, at.xsqb, at.qb, at.hb, at.wb);
+  // pair counter: the lane's accepted pairs are booked on atom a
+  fused_finalize<DEBUG>(A, B, wide, va, (at.anyf & 5u) != 0u, static_cast<double>(at.tot), at.ca,
+                        at.Sa, at.xsqa, at.qa, at.ha, at.wa);
+  fused_finalize<DEBUG>(A, B, wide, vb, (at.anyf & 10u) != 0u, 0.0, at.cb, at.Sb, at.xsqb, at.qb,
+                        at.hb, at.wb);
 
   if (safe)
     fused_scan<2, true, DEBUG>(sm, A, wb, cull_thr, B, at);

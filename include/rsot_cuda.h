@@ -146,6 +146,18 @@ int rsot_cuda_nearest(rsot_cuda_ctx* ctx, rsot_cuda_targets* targets,
 int rsot_cuda_covering_cost(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
                             rsot_cuda_targets* targets, double* out);
 
+/* ---- softmax_refine (multilevel prolongation) -----------------------------
+ * rsot::softmax_refine (proj/src/solve.cpp:62-142): psi on the n_fine points
+ * fine_xyz (host, AoS double[3]) from the coarse potential coarse_psi (host,
+ * length = coarse target count) of `coarse`, using all atoms of `atoms`
+ * (single GPU; the atom handle must hold every atom).  cutoff = +inf ->
+ * untruncated phase 1; finite -> the reference's brute-force cost test.
+ * psi_out (host, n_fine) receives the initial fine potential. */
+int rsot_cuda_softmax_refine(rsot_cuda_ctx* ctx, rsot_cuda_targets* coarse,
+                             const double* coarse_psi, const double* fine_xyz,
+                             size_t n_fine, rsot_cuda_atoms* atoms, double eps,
+                             double cutoff, double* psi_out);
+
 /* ---- measurement ----------------------------------------------------------
  * Enables CUDA-event timing of the hot kernels inside each evaluation
  * (events on the launching stream); rsot_cuda_last_kernel_ms returns the

@@ -62,6 +62,9 @@ class COracle:
                                            POINTER(Scalars), c_void_p, c_void_p, c_void_p]
         L.oracle_covering_cost.restype = c_int
         L.oracle_covering_cost.argtypes = [c_size_t, c_void_p, c_size_t, c_void_p, POINTER(c_double)]
+        L.oracle_softmax_refine.restype = c_int
+        L.oracle_softmax_refine.argtypes = [c_size_t, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p,
+                                            c_size_t, c_void_p, c_void_p, c_double, c_double, c_void_p]
         L.oracle_ball_radius.restype = c_double
         L.oracle_ball_radius.argtypes = [c_double]
         L.oracle_cutoff_pointwise.restype = c_double
@@ -96,6 +99,19 @@ class COracle:
                    candidate_pairs=sc.candidate_pairs, empty_candidate_atoms=sc.empty_candidate_atoms)
         if per_atom:
             out.update(count=cnt, hash=hsh, log_s=logs)
+        return out
+
+    def softmax_refine(self, coarse_xyz, coarse_nu, coarse_psi, fine_xyz, atoms, masses, eps,
+                       cutoff=math.inf):
+        cy, fy, ax = _pts(coarse_xyz), _pts(fine_xyz), _pts(atoms)
+        cnu = np.ascontiguousarray(coarse_nu, dtype=np.float64)
+        cpsi = np.ascontiguousarray(coarse_psi, dtype=np.float64)
+        am = np.ascontiguousarray(masses, dtype=np.float64)
+        out = np.empty(len(fy))
+        rc = self.L.oracle_softmax_refine(len(cy), _p(cy), _p(cnu), _p(cpsi), len(fy), _p(fy), len(ax), _p(ax),
+                                          _p(am), float(eps), float(cutoff), _p(out))
+        if rc != 0:
+            raise ValueError(self.L.oracle_last_error().decode())
         return out
 
     def hash_term(self, j: int) -> int:
@@ -147,6 +163,9 @@ class RefLib:
         L.ref_evaluate_dual.restype = c_int
         L.ref_evaluate_dual.argtypes = [c_void_p, c_void_p, c_size_t, c_double, c_double, c_int,
                                         c_void_p, POINTER(Scalars)]
+        L.ref_softmax_refine.restype = c_int
+        L.ref_softmax_refine.argtypes = [c_void_p, c_void_p, c_void_p, c_size_t, c_double, c_double, c_int,
+                                         c_void_p]
         L.ref_covering_cost.restype = c_int
         L.ref_covering_cost.argtypes = [c_void_p, POINTER(c_double)]
         self.L = L
@@ -178,6 +197,16 @@ class RefProblem:
             raise RuntimeError(self.lib.L.ref_last_error().decode())
         return dict(J=sc.J, D=sc.D, gradient=g, atoms_visited=sc.atoms_visited,
                     candidate_pairs=sc.candidate_pairs, empty_candidate_atoms=sc.empty_candidate_atoms)
+
+    def softmax_refine(self, coarse_psi, fine_xyz, eps, cutoff=math.inf, workers=1):
+        cpsi = np.ascontiguousarray(coarse_psi, dtype=np.float64)
+        fy = _pts(fine_xyz)
+        out = np.empty(len(fy))
+        rc = self.lib.L.ref_softmax_refine(self.h, _p(cpsi), _p(fy), len(fy), float(eps), float(cutoff),
+                                           int(workers), _p(out))
+        if rc != 0:
+            raise ValueError(self.lib.L.ref_last_error().decode())
+        return out
 
     def covering_cost(self):
         v = c_double()

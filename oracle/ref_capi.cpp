@@ -13,6 +13,7 @@
 
 #include "rsot/evaluate.hpp"
 #include "rsot/measures.hpp"
+#include "rsot/solve.hpp"
 #include "rsot/spatial_index.hpp"
 
 namespace {
@@ -112,6 +113,29 @@ int ref_covering_cost(void* prob, double* out) {
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;
+  }
+}
+
+// rsot::softmax_refine (solve.cpp:62-142): prob's targets are the coarse
+// level, prob's atoms the atoms; fine points given separately.
+int ref_softmax_refine(void* prob, const double* coarse_psi, const double* fine_xyz,
+                       size_t n_fine, double eps, double cutoff, int workers,
+                       double* psi_out) {
+  auto* p = static_cast<RefProblem*>(prob);
+  try {
+    const std::vector<double> cpsi(coarse_psi, coarse_psi + p->target.size());
+    const rsot::PointList fine = to_points(fine_xyz, n_fine);
+    const std::vector<double> out =
+        rsot::softmax_refine(p->target, cpsi, fine, p->atoms, eps,
+                             rsot::CostKind::SqEuclidean, cutoff, workers);
+    std::memcpy(psi_out, out.data(), sizeof(double) * n_fine);
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return -1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -2;
   }
 }
 

@@ -427,6 +427,78 @@ int oracle_evaluate_dual(size_t nq, const double* ax, const double* am,
   return ORACLE_OK;
 }
 
+/* solve.cpp:62-142, SqEuclidean cost, one worker (parallel_blocks with
+ * workers = 1 runs the same loops in order). */
+int oracle_softmax_refine(size_t n_coarse, const double* cy, const double* cnu,
+                          const double* cpsi, size_t n_fine, const double* fy,
+                          size_t nq, const double* ax, const double* am,
+                          double eps, double cutoff, double* psi_out) {
+  for (size_t j = 0; j < n_coarse; ++j)
+    if (!isfinite(cpsi[j])) {
+      g_last_error = "potential has non-finite entries";
+      return ORACLE_INVALID_ARGUMENT;
+    }
+  const int truncated = isfinite(cutoff);
+  double* log_nu = (double*)malloc(sizeof(double) * (n_coarse ? n_coarse : 1));
+  for (size_t j = 0; j < n_coarse; ++j) log_nu[j] = log(cnu[j]);
+  double* log_S = (double*)malloc(sizeof(double) * (nq ? nq : 1));
+  double* expo = (double*)malloc(sizeof(double) * (n_coarse ? n_coarse : 1));
+  size_t* cand = (size_t*)malloc(sizeof(size_t) * (n_coarse ? n_coarse : 1));
+  for (size_t q = 0; q < nq; ++q) { /* :79-118 */
+    const double* x = ax + 3 * q;
+    size_t nc = 0;
+    if (truncated) {
+      for (size_t j = 0; j < n_coarse; ++j)
+        if (0.5 * sqdist(x, cy + 3 * j) < cutoff) cand[nc++] = j;
+      if (nc == 0) {
+        size_t best = 0;
+        double best_c = 0.5 * sqdist(x, cy);
+        for (size_t j = 1; j < n_coarse; ++j) {
+          const double c = 0.5 * sqdist(x, cy + 3 * j);
+          if (c < best_c) {
+            best_c = c;
+            best = j;
+          }
+        }
+        cand[nc++] = best;
+      }
+    } else {
+      for (size_t j = 0; j < n_coarse; ++j) cand[nc++] = j;
+    }
+    double emax = -INFINITY;
+    for (size_t i = 0; i < nc; ++i) {
+      const size_t j = cand[i];
+      expo[i] = (cpsi[j] - 0.5 * sqdist(x, cy + 3 * j)) / eps + log_nu[j];
+      emax = (emax < expo[i]) ? expo[i] : emax;
+    }
+    double sum = 0.0;
+    for (size_t i = 0; i < nc; ++i) sum += exp(expo[i] - emax);
+    log_S[q] = emax + log(sum);
+  }
+  int rc = ORACLE_OK;
+  for (size_t k = 0; k < n_fine; ++k) { /* :120-139 */
+    const double* y = fy + 3 * k;
+    double emax = -INFINITY;
+    for (size_t q = 0; q < nq; ++q) {
+      const double t = -(0.5 * sqdist(ax + 3 * q, y)) / eps - log_S[q] + log(am[q]);
+      emax = (emax < t) ? t : emax;
+    }
+    double sum = 0.0;
+    for (size_t q = 0; q < nq; ++q) {
+      const double t = -(0.5 * sqdist(ax + 3 * q, y)) / eps - log_S[q] + log(am[q]);
+      sum += exp(t - emax);
+    }
+    psi_out[k] = -eps * (emax + log(sum));
+    if (!isfinite(psi_out[k])) rc = ORACLE_INVALID_ARGUMENT;
+  }
+  if (rc) g_last_error = "potential has non-finite entries";
+  free(log_nu);
+  free(log_S);
+  free(expo);
+  free(cand);
+  return rc;
+}
+
 /* spatial_index.cpp:101-121 (SqEuclidean branch) */
 int oracle_covering_cost(size_t nq, const double* ax, size_t n,
                          const double* ty, double* out) {

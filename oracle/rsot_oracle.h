@@ -92,6 +92,15 @@ int oracle_evaluate_dual(size_t nq, const double* atom_xyz,
                          oracle_scalars* out, uint32_t* cand_count,
                          uint64_t* cand_hash, double* log_s);
 
+/* rsot::softmax_refine (proj/src/solve.cpp:62-142), SqEuclidean, single
+ * worker: psi_out[n_fine] from the coarse potential.  Returns
+ * ORACLE_INVALID_ARGUMENT on non-finite input or output (require_finite). */
+int oracle_softmax_refine(size_t n_coarse, const double* coarse_xyz,
+                          const double* coarse_nu, const double* coarse_psi,
+                          size_t n_fine, const double* fine_xyz, size_t nq,
+                          const double* atom_xyz, const double* atom_mass,
+                          double eps, double cutoff, double* psi_out);
+
 /* rsot::covering_cost, SqEuclidean: max_q min_j 0.5*|x_q - y_j|^2. */
 int oracle_covering_cost(size_t nq, const double* atom_xyz, size_t n,
                          const double* target_xyz, double* out);

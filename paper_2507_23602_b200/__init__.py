@@ -30,4 +30,5 @@ from .rsot import (  # noqa: F401
     gauge_fixed,
     refresh_truncation,
     require_finite,
+    softmax_refine,
 )

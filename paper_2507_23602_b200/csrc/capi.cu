@@ -20,6 +20,7 @@
 
 #include "../../include/rsot_cuda.h"
 #include "kernels.cuh"
+#include "refine.cuh"
 #include "truncated.cuh"
 
 using namespace rsot_cuda;
@@ -106,6 +107,7 @@ struct rsot_cuda_ctx {
       atomD, partG, res, g_out, scalars_out;
   DevBuf<int> flagged;
   TruncWorkspace trunc;
+  RefineWorkspace refine;
   double* h_pinned = nullptr;  // small pinned staging for scalars
   bool timing = false;
   cudaEvent_t ev[8] = {};
@@ -304,6 +306,7 @@ int rsot_cuda_ctx_destroy(rsot_cuda_ctx* c) {
   c->partG.release(); c->res.release(); c->g_out.release();
   c->scalars_out.release(); c->flagged.release();
   c->trunc.release();
+  c->refine.release();
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
@@ -579,6 +582,36 @@ int rsot_cuda_covering_cost(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targ
   }
   *out = c0;
   return RSOT_CUDA_OK;
+}
+
+int rsot_cuda_softmax_refine(rsot_cuda_ctx* c, rsot_cuda_targets* coarse,
+                             const double* coarse_psi, const double* fine_xyz, size_t n_fine,
+                             rsot_cuda_atoms* a, double eps, double cutoff, double* psi_out) {
+  int rc = check_ready(c, a, coarse);
+  if (rc) return rc;
+  if (!coarse_psi || (n_fine && (!fine_xyz || !psi_out)))
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  if (!(eps > 0.0)) return fail(RSOT_CUDA_INVALID_ARGUMENT, "epsilon must be > 0");
+  for (size_t j = 0; j < coarse->n; ++j)
+    if (!std::isfinite(coarse_psi[j]))
+      return fail(RSOT_CUDA_INVALID_ARGUMENT, "potential has non-finite entries");
+  if (a->nq == 0)  // the reference's phase 2 yields -eps*(-inf) -> require_finite throws
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "potential has non-finite entries");
+  if (n_fine == 0) return RSOT_CUDA_OK;
+  if (std::isnan(cutoff)) cutoff = INFINITY;
+  const DenseLaunch plan = plan_dense(static_cast<int>(a->nq), static_cast<int>(coarse->n), c->num_sms);
+  rc = ensure_workspace(c, a->nq, coarse->n, plan);
+  if (rc) return rc;
+  EvalBuffers b = buffers(c, nullptr, nullptr);
+  b.timing = nullptr;
+  RSOT_CK(cudaMemcpyAsync(b.psi, coarse_psi, sizeof(double) * coarse->n, cudaMemcpyHostToDevice,
+                          c->stream));
+  const DeviceTargets dt = make_dt(coarse);
+  launch_prologue(dt, b, eps, c->stream);
+  rc = run_softmax_refine(c->refine, DeviceAtoms{a->x, static_cast<int>(a->nq)}, dt, b, fine_xyz,
+                          static_cast<int>(n_fine), eps, cutoff, c->num_sms, psi_out, c->stream,
+                          g_last_error);
+  return rc ? fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error) : RSOT_CUDA_OK;
 }
 
 int rsot_cuda_ctx_set_timing(rsot_cuda_ctx* c, int enable) {

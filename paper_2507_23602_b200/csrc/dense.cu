@@ -576,6 +576,27 @@ void launch_dense(const DeviceAtoms& a, const DeviceTargets& t, EvalBuffers& b,
   (note_launch(), set_dense_counts<<<1, 1, 0, s>>>(b.res, n, static_cast<double>(nq)));
 }
 
+// Generic target-major gather (dense pass B) used by softmax_refine phase 2:
+// G[j] = sum_q 2^(T_j + A_q + X_q . y'_j) with T_j = b2[j] - c2|y'|^2 and
+// A_q = lam[q] - c2|x'|^2, split over atoms and reduced in fixed order.
+void launch_dense_gather(const double4* atoms, const double* lam, int nq, const double4* ty,
+                         const double* b2, int n, double c2, int num_sms, double* partG,
+                         size_t partG_cap, double* G, cudaStream_t s) {
+  const DenseLaunch p = plan_dense(nq, n, num_sms);
+  int per_splitB = (((nq + p.splitsB - 1) / p.splitsB) + kTile - 1) / kTile * kTile;
+  int splitsB = (nq + per_splitB - 1) / per_splitB;
+  while (static_cast<size_t>(splitsB) * n > partG_cap && splitsB > 1) {
+    per_splitB *= 2;
+    splitsB = (nq + per_splitB - 1) / per_splitB;
+  }
+  dim3 gB((n + kThreads * p.tpt - 1) / (kThreads * p.tpt), splitsB);
+  if (p.tpt == 2)
+    (note_launch(), dense_passB<2><<<gB, kThreads, 0, s>>>(atoms, lam, nq, per_splitB, ty, b2, n, c2, partG));
+  else
+    (note_launch(), dense_passB<1><<<gB, kThreads, 0, s>>>(atoms, lam, nq, per_splitB, ty, b2, n, c2, partG));
+  (note_launch(), reduce_partG<<<(n + 255) / 256, 256, 0, s>>>(partG, splitsB, n, G));
+}
+
 void launch_finalize(const DeviceTargets& t, EvalBuffers& b, cudaStream_t s) {
   (note_launch(), finalize_kernel<<<(t.n + 255) / 256, 256, 0, s>>>(b.res, t.nu, t.n, b.scal,
                                                     b.g_out, b.scalars_out));

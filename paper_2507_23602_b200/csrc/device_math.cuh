@@ -39,13 +39,18 @@ __device__ __constant__ int2 kExp2Table[16] = {
     {(int)0xa2a490da, 0x3fefa4af}};
 
 // Near-minimax degree-5 fit of 2^r on [-1/32, 1/32] (mpmath chebyfit),
-// coefficients rounded to double; worst relative error 4.61e-15.
-constexpr double kP5 = 0x1.5d897e525c216p-10;
-constexpr double kP4 = 0x1.3b2c9b8a6caeap-7;
-constexpr double kP3 = 0x1.c6b08d6f2a289p-5;
-constexpr double kP2 = 0x1.ebfbdff555824p-3;
-constexpr double kP1 = 0x1.62e42fefa39f3p-1;
-constexpr double kP0 = 0x1.0000000000014p+0;
+// coefficients rounded to double; worst relative error 4.61e-15.  Kept in
+// constant memory so the DFMAs take them as c[][] operands (no per-loop
+// uniform-register materialisation).
+__device__ __constant__ double kPoly[6] = {0x1.0000000000014p+0, 0x1.62e42fefa39f3p-1,
+                                           0x1.ebfbdff555824p-3, 0x1.c6b08d6f2a289p-5,
+                                           0x1.3b2c9b8a6caeap-7, 0x1.5d897e525c216p-10};
+#define kP0 (kPoly[0])
+#define kP1 (kPoly[1])
+#define kP2 (kPoly[2])
+#define kP3 (kPoly[3])
+#define kP4 (kPoly[4])
+#define kP5 (kPoly[5])
 
 // Copies the exp2 table into shared memory (16 x 8 B = 128 B: a half-warp
 // LDS.64 with any index pattern is one conflict-free wavefront).

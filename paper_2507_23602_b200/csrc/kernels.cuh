@@ -99,6 +99,11 @@ void launch_finalize(const DeviceTargets& t, EvalBuffers& b, cudaStream_t s);
 void launch_det_sum(const double* x, size_t n, double* partials, double* out,
                     cudaStream_t s);
 
+// Dense target-major gather (softmax_refine phase 2), see dense.cu.
+void launch_dense_gather(const double4* atoms, const double* lam, int nq, const double4* ty,
+                         const double* b2, int n, double c2, int num_sms, double* partG,
+                         size_t partG_cap, double* G, cudaStream_t s);
+
 // FP64 DFMA peak probe (roofline denominator), returns DFMA/s.
 double measure_dfma_rate(cudaStream_t s);
 

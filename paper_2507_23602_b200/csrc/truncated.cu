@@ -996,18 +996,28 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
       __syncthreads();
       const int nsel = fused_cull(sm, cnt, wb, cull_thr, list);
       if (PHASE == 1) {
+        // software-pipelined: the next step's list entries and distances are
+        // loaded before this step's exponentials (hides LDS latency).
+        int t0 = nsel > 0 ? list[0] : 0;
+        int t1 = nsel > 1 ? list[1] : t0;
+        float2 d0 = fused_d2(sm, at, t0), d1 = fused_d2(sm, at, t1);
         for (int i = 0; i < nsel; i += 2) {
           const bool v1 = i + 1 < nsel;
-          const int t0 = list[i];
-          const int t1 = v1 ? list[i + 1] : t0;
           unsigned in, bd;
-          fused_masks(fused_d2(sm, at, t0), fused_d2(sm, at, t1), nlo, nhi, v1, in, bd);
+          fused_masks(d0, d1, nlo, nhi, v1, in, bd);
+          const int c0 = t0, c1 = t1;
+          if (i + 2 < nsel) {
+            t0 = list[i + 2];
+            t1 = (i + 3 < nsel) ? list[i + 3] : t0;
+            d0 = fused_d2(sm, at, t0);
+            d1 = fused_d2(sm, at, t1);
+          }
           if (__any_sync(0xffffffffu, bd != 0u)) {
-            if (bd) fused_exact(sm, A, at, t0, t1, bd, &in);
+            if (bd) fused_exact(sm, A, at, c0, c1, bd, &in);
           }
           if (__any_sync(0xffffffffu, in != 0u)) {
-            const double4 y0 = sm.tD[t0];
-            const double4 y1 = sm.tD[t1];
+            const double4 y0 = sm.tD[c0];
+            const double4 y1 = sm.tD[c1];
             double sa0 = chain3(at.Xa, y0), sb0 = chain3(at.Xb, y0);
             double sa1 = chain3(at.Xa, y1), sb1 = chain3(at.Xb, y1);
             if (wide) {
@@ -1023,10 +1033,10 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
             if (DEBUG) {
               at.ca += __popc(in & 5u);
               at.cb += __popc(in & 10u);
-              if (in & 1u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
-              if (in & 4u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
-              if (in & 2u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
-              if (in & 8u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
+              if (in & 1u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[c0]));
+              if (in & 4u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[c1]));
+              if (in & 2u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[c0]));
+              if (in & 8u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[c1]));
             }
           }
         }

@@ -446,6 +446,29 @@ def evaluate_dual(atoms: SourceAtoms, target: TargetMeasure, psi: DualPotential,
                       empty_candidate_atoms=int(sc.empty_candidate_atoms))
 
 
+def softmax_refine(coarse: TargetMeasure, coarse_psi, fine_points, atoms: SourceAtoms, eps: float,
+                   kind: CostKind = CostKind.SqEuclidean, cutoff: float = math.inf, workers: int = 1,
+                   ctx: Optional[Context] = None) -> np.ndarray:
+    """rsot::softmax_refine (solve.hpp, solve.cpp:62-142) on the GPU: the
+    initial fine-level potential from a coarse one (multilevel prolongation).
+    `workers` (a CPU thread count in the reference) is ignored."""
+    cpsi = np.ascontiguousarray(np.asarray(coarse_psi, dtype=np.float64))
+    if len(cpsi) != coarse.size():
+        raise ValueError("softmax refine: psi/coarse size mismatch")
+    require_finite(cpsi)
+    if kind != CostKind.SqEuclidean:
+        raise NotImplementedError("SqGeodesicSphere is out of scope for the B200 evaluator")
+    ctx = ctx or Context.default()
+    fine = _points3(fine_points)
+    out = np.empty(len(fine), dtype=np.float64)
+    dev_t = _device_targets(coarse, ctx)
+    dev_a = _device_atoms(atoms, ctx) if ctx.world == 1 else DeviceAtoms(ctx, atoms.points, atoms.masses,
+                                                                          shard=False)
+    _lib.check(ctx.lib.rsot_cuda_softmax_refine(ctx.handle, dev_t.handle, _ptr(cpsi), _ptr(fine), len(fine),
+                                                dev_a.handle, float(eps), float(cutoff), _ptr(out)))
+    return out
+
+
 def evaluate_dual_debug(atoms: SourceAtoms, target: TargetMeasure, psi, eps: float, cutoff: float,
                         ctx: Optional[Context] = None):
     """evaluate_dual plus per-atom candidate counts, candidate hashes and ln S_q

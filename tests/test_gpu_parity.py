@@ -249,3 +249,40 @@ def test_full_size_properties(ctx, name):
     else:
         assert p.nq <= r1.candidate_pairs < p.nq * p.n
     assert math.isfinite(r1.J) and r1.D > 0
+
+
+# ---- softmax_refine -------------------------------------
+
+@pytest.mark.parametrize("nc,nf,nq,eps,cut", [(50, 300, 4000, 0.05, math.inf), (80, 500, 6000, 0.02, 0.01),
+                                              (40, 200, 3000, 0.01, 0.001), (30, 100, 2000, 0.02, -1.0),
+                                              (600, 900, 20000, 0.005, 0.002)])
+def test_softmax_refine_parity(ctx, nc, nf, nq, eps, cut):
+    rng = np.random.default_rng(nc * 7 + nf)
+    cy = rng.uniform(size=(nc, 3))
+    cnu = rng.uniform(size=nc) + 0.1
+    cnu /= cnu.sum()
+    cpsi = rng.normal(0, 0.02, nc)
+    fy = rng.uniform(size=(nf, 3))
+    ax = rng.uniform(size=(nq, 3))
+    am = rng.uniform(size=nq) + 0.1
+    am /= am.sum()
+    want = C.softmax_refine(cy, cnu, cpsi, fy, ax, am, eps, cut)
+    coarse = rs.TargetMeasure(dim=3, points=cy, weights=cnu)
+    atoms = rs.SourceAtoms(dim=3, points=ax, masses=am)
+    got = rs.softmax_refine(coarse, cpsi, fy, atoms, eps, cutoff=cut, ctx=ctx)
+    scale = np.max(np.abs(want))
+    assert np.max(np.abs(got - want)) <= 1e-10 * scale
+
+
+def test_softmax_refine_cfg4_subsample(ctx):
+    """cfg4 shapes: coarse 8192 mixture targets, fine points, fine atoms (subset)."""
+    co = synth.make("cfg4_coarse")
+    fi = synth.make("cfg4_fine")
+    sub = synth.subsample_atoms(fi, 3000)
+    cpsi = np.random.default_rng(5).normal(0, 1e-3, co.n)
+    fine_pts = fi.targets[:400]
+    cut = float(np.max(cpsi)) + 1e-3 * math.log(float(np.max(co.nu)) / 1e-12)
+    want = C.softmax_refine(co.targets, co.nu, cpsi, fine_pts, sub.atoms, sub.masses, 1e-3, cut)
+    got = rs.softmax_refine(rs.TargetMeasure(dim=3, points=co.targets, weights=co.nu), cpsi, fine_pts,
+                            rs.SourceAtoms(dim=3, points=sub.atoms, masses=sub.masses), 1e-3, cutoff=cut, ctx=ctx)
+    assert np.max(np.abs(got - want)) <= 1e-10 * np.max(np.abs(want))

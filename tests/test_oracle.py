@@ -199,3 +199,41 @@ def test_reference_doctest_suites(suite):
     p = subprocess.run([exe], capture_output=True, text=True, timeout=600, cwd="/tmp")
     failed = [ln.split('TEST_CASE("', 1)[1].rstrip('")') for ln in p.stderr.splitlines() if "in TEST_CASE(" in ln]
     assert set(failed) <= KNOWN_REFERENCE_FAILURES, p.stderr[-2000:]
+
+
+@pytest.mark.skipif(not have_ref, reason="reference library not built here")
+def test_softmax_refine_oracle_matches_reference_bitwise():
+    """rsot::softmax_refine (solve.cpp:62-142): C restatement vs the reference."""
+    from oracle.oracle import RefLib
+    ref = RefLib()
+    rng = np.random.default_rng(17)
+    for (nc, nf, nq, eps, cut) in [(50, 120, 1500, 0.05, math.inf), (80, 150, 2000, 0.02, 0.01),
+                                   (40, 60, 800, 0.01, 0.001), (30, 40, 500, 0.02, -1.0)]:
+        cy = rng.uniform(size=(nc, 3))
+        cnu = rng.uniform(size=nc) + 0.1
+        cnu /= cnu.sum()
+        cpsi = rng.normal(0, 0.02, nc)
+        fy = rng.uniform(size=(nf, 3))
+        ax = rng.uniform(size=(nq, 3))
+        am = rng.uniform(size=nq) + 0.1
+        am /= am.sum()
+        o = C.softmax_refine(cy, cnu, cpsi, fy, ax, am, eps, cut)
+        r = ref.problem(3, ax, am, cy, cnu).softmax_refine(cpsi, fy, eps, cut, 1)
+        assert np.array_equal(o, r)
+
+
+def test_softmax_refine_identity_cases():
+    """test_core.cpp:370-397 analogue: a single coarse target refines to a
+    potential whose gauge-fixed values are the closed form."""
+    rng = np.random.default_rng(2)
+    ax = rng.uniform(size=(300, 3))
+    am = np.full(300, 1 / 300)
+    fy = rng.uniform(size=(20, 3))
+    out = C.softmax_refine(np.array([[0.5, 0.5, 0.5]]), np.array([1.0]), np.array([0.3]), fy, ax, am, 0.1)
+    # ln S_q = (0.3 - c(x_q, y0)) / eps  ->  psi_k = -eps LSE_q(-c_qk/eps - ln S_q + ln m_q)
+    c0 = 0.5 * ((ax - 0.5) ** 2).sum(axis=1)
+    logS = (0.3 - c0) / 0.1
+    for k in range(5):
+        t = -0.5 * ((ax - fy[k]) ** 2).sum(axis=1) / 0.1 - logS + np.log(am)
+        m = t.max()
+        assert out[k] == pytest.approx(-0.1 * (m + np.log(np.exp(t - m).sum())), rel=1e-12, abs=1e-14)

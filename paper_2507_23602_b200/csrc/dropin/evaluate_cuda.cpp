@@ -24,6 +24,7 @@
 #include <string>
 
 #include "rsot/evaluate.hpp"
+#include "rsot/solve.hpp"
 #include "rsot_cuda.h"
 #include "rsot_cuda_context.hpp"
 
@@ -182,16 +183,18 @@ struct State {
     return h;
   }
 
-  rsot_cuda_atoms* get_atoms(const SourceAtoms& a) {
+  rsot_cuda_atoms* get_atoms(const SourceAtoms& a, bool full = false) {
+    const int world_eff = full ? 1 : world;
     Key k = make_key(a.points, a.masses);
-    k.h ^= static_cast<uint64_t>(world) * 0x9E3779B97F4A7C15ull + static_cast<uint64_t>(rank);
+    k.h ^= static_cast<uint64_t>(world_eff) * 0x9E3779B97F4A7C15ull +
+           static_cast<uint64_t>(full ? 0 : rank);
     for (auto it = atoms.begin(); it != atoms.end(); ++it)
       if (it->first == k) {
         atoms.splice(atoms.begin(), atoms, it);
         return atoms.front().second;
       }
     size_t lo = 0, hi = a.points.size();
-    if (world > 1) rsot_cuda_shard_range(a.points.size(), rank, world, &lo, &hi);
+    if (world_eff > 1) rsot_cuda_shard_range(a.points.size(), rank, world, &lo, &hi);
     rsot_cuda_atoms* h = nullptr;
     const double* xyz = a.points.empty() ? nullptr : a.points[lo].data();
     const double* m = a.masses.empty() ? nullptr : a.masses.data() + lo;
@@ -246,6 +249,34 @@ EvalResult evaluate_dual(const SourceAtoms& atoms, const TargetMeasure& target,
   result.candidate_pairs = sc.candidate_pairs;
   result.empty_candidate_atoms = sc.empty_candidate_atoms;
   return result;
+}
+
+// ---- solve.cpp:62-142 on the GPU ----------------------------------------------
+// The reference defines softmax_refine in solve.cpp next to solve_multilevel;
+// the drop-in build weakens that definition (objcopy --weaken-symbol, see
+// csrc/dropin/Makefile) so this one serves both direct callers and the
+// reference's own solve_multilevel (its call goes through the PLT).
+std::vector<double> softmax_refine(const TargetMeasure& coarse,
+                                   const std::vector<double>& coarse_psi,
+                                   const PointList& fine_points, const SourceAtoms& atoms,
+                                   double eps, CostKind kind, double cutoff, int workers) {
+  (void)workers;  // CPU thread count in the reference
+  if (coarse_psi.size() != coarse.size())
+    throw std::invalid_argument("softmax refine: psi/coarse size mismatch");
+  require_finite(coarse_psi);
+  if (kind != CostKind::SqEuclidean)
+    throw std::invalid_argument(
+        "softmax_refine (B200): SqGeodesicSphere is out of scope for the GPU path");
+  auto& st = cuda_detail::state();
+  std::lock_guard<std::mutex> lock(st.mu);
+  rsot_cuda_targets* dt = st.get_targets(coarse);
+  rsot_cuda_atoms* da = st.get_atoms(atoms, /*full=*/true);
+  std::vector<double> out(fine_points.size());
+  const int rc = rsot_cuda_softmax_refine(st.context(), dt, coarse_psi.data(),
+                                          fine_points.empty() ? nullptr : fine_points.data()->data(),
+                                          fine_points.size(), da, eps, cutoff, out.data());
+  if (rc) cuda_detail::raise(rc, "rsot_cuda_softmax_refine");
+  return out;
 }
 
 namespace cuda {

@@ -163,6 +163,23 @@ def make(name: str, seed: Optional[int] = None) -> Problem:
     raise ValueError(f"unknown config {name}")
 
 
+def make_cfg4_small(level: str, seed: int = 4) -> Problem:
+    """cfg4 at reduced size (8^3 -> 16^3 hexes, 512 -> 4096 targets) for
+    solve-level comparisons against the CPU reference."""
+    cells, n = (8, 512) if level == "coarse" else (16, 4096)
+    means = mixture_means(seed)
+    atoms = tensor_atoms(cells, 3)
+    masses = _masses(mixture_density(atoms, means))
+    fine = mixture_samples(4096, means, seed)
+    if level == "coarse":
+        sel = np.sort(np.random.default_rng([seed, 13]).choice(4096, size=512, replace=False))
+        tg = np.ascontiguousarray(fine[sel])
+    else:
+        tg = fine
+    return Problem("cfg4_small_" + level, 3, atoms, masses, tg, np.full(len(tg), 1.0 / len(tg)), 1e-3, 0.0,
+                   "pointwise", seed=seed)
+
+
 def subsample_atoms(p: Problem, count: int, seed: int = 99) -> Problem:
     """A seeded subset of the atoms (masses kept as is) for bounded oracle runs."""
     rng = np.random.default_rng([seed, p.seed])

@@ -555,7 +555,43 @@ __device__ double fp_to_double(const unsigned long long* acc) {
          static_cast<double>(acc[0]) * 0x1p-150;
 }
 
-// Warp-cooperative exact nearest target (lexicographic (d^2, j) argmin).
+// Warp-cooperative exact nearest target (lexicographic (d^2, j) argmin) by
+// expanding Chebyshev rings of cells.  A ring is a set of cell rows; the
+// cells of a row are contiguous in the cell-sorted targets, so each row (or
+// the two end cells of an inner row) is one target range.  Lanes fetch the
+// ranges of 32 rows at once and drop rows whose box lies farther than the
+// best distance so far; the surviving ranges are then scanned by the whole
+// warp, lanes over targets.  The search stops once the scanned box provably
+// contains the minimum.
+__device__ __forceinline__ double range_lb2(const GridDev& g, const double* v, int cy, int cz,
+                                            int a0, int a1) {
+  const double dx = slab_dist(g, 0, a0, v[0], v[0]);
+  const double dx1 = slab_dist(g, 0, a1, v[0], v[0]);
+  const double ddx = (a0 <= cell_of(g, 0, v[0]) && cell_of(g, 0, v[0]) <= a1) ? 0.0 : fmin(dx, dx1);
+  const double dy = slab_dist(g, 1, cy, v[1], v[1]);
+  const double dz = slab_dist(g, 2, cz, v[2], v[2]);
+  return fma(ddx, ddx, fma(dy, dy, dz * dz));
+}
+
+__device__ __forceinline__ void scan_range(int b, int e, double x0, double x1, double x2,
+                                           const double4* __restrict__ ys,
+                                           const int* __restrict__ tperm, double& bd, int& bj,
+                                           int& bk) {
+  const int lane = threadIdx.x & 31;
+  unsigned m = __ballot_sync(0xffffffffu, e > b);
+  while (m) {
+    const int l = __ffs(m) - 1;
+    m &= m - 1;
+    const int rb = __shfl_sync(0xffffffffu, b, l), re = __shfl_sync(0xffffffffu, e, l);
+    for (int t = rb + lane; t < re; t += 32) {
+      const double4 y = ys[t];
+      const double d2 = exact_sqdist(x0, x1, x2, y.x, y.y, y.z);
+      const int j = tperm[t];
+      if (d2 < bd || (d2 == bd && j < bj)) { bd = d2; bj = j; bk = t; }
+    }
+  }
+}
+
 __device__ void warp_nearest(const GridDev& g, const double4* __restrict__ ys,
                              const int* __restrict__ tperm,
                              const int* __restrict__ cell_start, double x0,
@@ -572,24 +608,37 @@ __device__ void warp_nearest(const GridDev& g, const double4* __restrict__ ys,
     const int zlo = max(0, cc[2] - k), zhi = min(g.dims[2] - 1, cc[2] + k);
     const int ylo = max(0, cc[1] - k), yhi = min(g.dims[1] - 1, cc[1] + k);
     const int xlo = max(0, cc[0] - k), xhi = min(g.dims[0] - 1, cc[0] + k);
-    for (int cz = zlo; cz <= zhi; ++cz)
-      for (int cy = ylo; cy <= yhi; ++cy) {
+    const int ny = yhi - ylo + 1;
+    const int nrows = ny * (zhi - zlo + 1);
+    // rows whose box is beyond the warp's best so far cannot improve it
+    const double prune = bd * (1.0 + 1e-9);
+    for (int r0 = 0; r0 < nrows; r0 += 32) {
+      const int ri = r0 + lane;
+      int b0 = 0, e0 = 0, b1 = 0, e1 = 0;
+      if (ri < nrows) {
+        const int cy = ylo + ri % ny, cz = zlo + ri / ny;
         const bool full = (abs(cz - cc[2]) == k) || (abs(cy - cc[1]) == k);
         const long long row = (static_cast<long long>(cz) * g.dims[1] + cy) * g.dims[0];
-        for (int part = 0; part < (full ? 1 : 2); ++part) {
-          int a0, a1;
-          if (full) { a0 = xlo; a1 = xhi; }
-          else if (part == 0) { a0 = cc[0] - k; a1 = a0; if (a0 < 0) continue; }
-          else { a0 = cc[0] + k; a1 = a0; if (a0 > g.dims[0] - 1 || k == 0) continue; }
-          const int b = cell_start[row + a0], e = cell_start[row + a1 + 1];
-          for (int t = b + lane; t < e; t += 32) {
-            const double4 y = ys[t];
-            const double d2 = exact_sqdist(x0, x1, x2, y.x, y.y, y.z);
-            const int j = tperm[t];
-            if (d2 < bd || (d2 == bd && j < bj)) { bd = d2; bj = j; bk = t; }
+        if (full) {
+          if (!(range_lb2(g, v, cy, cz, xlo, xhi) > prune)) {
+            b0 = cell_start[row + xlo];
+            e0 = cell_start[row + xhi + 1];
+          }
+        } else {
+          const int a = cc[0] - k, c = cc[0] + k;
+          if (a >= 0 && !(range_lb2(g, v, cy, cz, a, a) > prune)) {
+            b0 = cell_start[row + a];
+            e0 = cell_start[row + a + 1];
+          }
+          if (c <= g.dims[0] - 1 && !(range_lb2(g, v, cy, cz, c, c) > prune)) {
+            b1 = cell_start[row + c];
+            e1 = cell_start[row + c + 1];
           }
         }
       }
+      scan_range(b0, e0, x0, x1, x2, ys, tperm, bd, bj, bk);
+      scan_range(b1, e1, x0, x1, x2, ys, tperm, bd, bj, bk);
+    }
     // warp lexicographic min
     for (int o = 16; o > 0; o >>= 1) {
       const double od = __shfl_xor_sync(0xffffffffu, bd, o);
@@ -824,6 +873,7 @@ struct FusedArgs {
   double* atomJ; double* atomD; double* cntd; double* emptyd;
   unsigned long long* gacc;              // [3 N] fixed point, original index
   uint32_t* dbg_cnt; uint64_t* dbg_hash; double* dbg_logs;  // Hilbert order
+  uint32_t* cnt_out;                     // 0 = empty candidate set (Hilbert order)
 };
 
 __device__ __forceinline__ double chain3(const double (&X)[3], const double4& y) {
@@ -1125,17 +1175,6 @@ __device__ __noinline__ void warp_exact_atom(const FusedArgs& A, double x0, doub
   *L_out = mx + log(sum);
 }
 
-__device__ __noinline__ void warp_nearest_fallback(const FusedArgs& A, double px, double py,
-                                                   double pz, double pm, double* L_out,
-                                                   int* j_out) {
-  double bd;
-  int bj, bk;
-  warp_nearest(A.g, A.ys, A.tperm, A.cell_start, px, py, pz, bd, bj, bk);
-  *L_out = reference_exponent(A.psi[bj], bd, A.eps, A.ys[bk].w);
-  *j_out = bj;
-  if ((threadIdx.x & 31) == 0) fp_add(A.gacc + 3 * static_cast<size_t>(bj), pm);
-}
-
 // Per-atom finalisation between the phases (all lanes of the warp call it:
 // empty and flagged atoms are resolved warp-cooperatively).
 template <bool DEBUG>
@@ -1151,20 +1190,10 @@ __device__ __forceinline__ void fused_finalize(const FusedArgs& A, double B, boo
   const bool flag = valid && nonempty && (!(S >= 0x1p-960) || !(S <= 0x1p960));
   double L = (B - shift + log2(S)) * kLn2;
   double w = valid && nonempty ? m / S : 0.0;
-  unsigned me = __ballot_sync(0xffffffffu, empty);
-  while (me) {
-    const int l = __ffs(me) - 1;
-    me &= me - 1;
-    double Lx;
-    int bj;
-    warp_nearest_fallback(A, __shfl_sync(0xffffffffu, p.x, l), __shfl_sync(0xffffffffu, p.y, l),
-                          __shfl_sync(0xffffffffu, p.z, l), __shfl_sync(0xffffffffu, m, l), &Lx,
-                          &bj);
-    if (lane == l) {
-      L = Lx;
-      if (DEBUG) hash = candidate_hash_term(static_cast<uint64_t>(bj));
-    }
-  }
+  // Empty candidate sets: resolved after this kernel by trunc_nearest_empty
+  // (warp per empty atom over the whole GPU, no CTA barrier in the way);
+  // their phase-2 weight is 0 and their J/D/L are written there.
+  if (valid) A.cnt_out[q] = empty ? 0u : 1u;
   unsigned mf = __ballot_sync(0xffffffffu, flag);
   while (mf) {
     const int l = __ffs(mf) - 1;
@@ -1596,7 +1625,6 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
                   const DeviceTargets& t, TargetCells& tc, EvalBuffers& b,
                   double eps, double cutoff, int num_sms, DebugOut* dbg,
                   cudaStream_t s, std::string& err) {
-  (void)num_sms;
   // cost.hpp:38-42 and spatial_index.cpp:50,54, evaluated on the host exactly
   // as the reference does.
   const double radius = cutoff < 0.0 ? 0.0 : std::sqrt(2.0 * cutoff);
@@ -1622,15 +1650,25 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
     A.c2 = c2; A.r2 = r2; A.r_scan = r_scan; A.eps = eps;
     A.atomJ = ws.atomJ; A.atomD = ws.atomD; A.cntd = ws.cntd; A.emptyd = ws.emptyd;
     A.gacc = ws.empty_fp;
-    A.dbg_cnt = ws.cnt; A.dbg_hash = ws.hash; A.dbg_logs = ws.atomL;
+    A.dbg_cnt = reinterpret_cast<uint32_t*>(ws.S); A.dbg_hash = ws.hash; A.dbg_logs = ws.atomL;
+    A.cnt_out = ws.cnt;
     const int nblk = (nq + kFA - 1) / kFA;
     if (b.timing) cudaEventRecord(b.timing[1], s);
     if (dbg)
       (note_launch(), trunc_fused<true><<<nblk, kT, 0, s>>>(A));
     else
       (note_launch(), trunc_fused<false><<<nblk, kT, 0, s>>>(A));
+    if (b.timing) cudaEventRecord(b.timing[2], s);
+    const int nb_near = std::min(4 * num_sms, (nq + 255) / 256 * 8 + 1);
+    if (dbg)
+      (note_launch(), trunc_nearest_empty<true><<<nb_near, 256, 0, s>>>(ac.ph, nq, ws.cnt, tc.pc, tc.perm_c,
+                                                        tc.cell_start, g, b.psi, eps, ws.atomL,
+                                                        ws.atomJ, ws.atomD, ws.empty_fp, ws.hash));
+    else
+      (note_launch(), trunc_nearest_empty<false><<<nb_near, 256, 0, s>>>(ac.ph, nq, ws.cnt, tc.pc, tc.perm_c,
+                                                         tc.cell_start, g, b.psi, eps, ws.atomL,
+                                                         ws.atomJ, ws.atomD, ws.empty_fp, ws.hash));
     if (b.timing) {
-      cudaEventRecord(b.timing[2], s);
       cudaEventRecord(b.timing[3], s);
       cudaEventRecord(b.timing[4], s);
     }
@@ -1640,8 +1678,8 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
     launch_det_sum(ws.cntd, nq, ws.red + 2048, b.res + n + kResPairs, s);
     launch_det_sum(ws.emptyd, nq, ws.red + 3072, b.res + n + kResEmpty, s);
     if (dbg) {
-      (note_launch(), scatter_debug<uint32_t><<<(nq + 255) / 256, 256, 0, s>>>(ws.cnt, ac.perm_h, nq,
-                                                                           dbg->count));
+      (note_launch(), scatter_debug<uint32_t><<<(nq + 255) / 256, 256, 0, s>>>(
+          reinterpret_cast<uint32_t*>(ws.S), ac.perm_h, nq, dbg->count));
       (note_launch(), scatter_debug<unsigned long long><<<(nq + 255) / 256, 256, 0, s>>>(
           reinterpret_cast<unsigned long long*>(ws.hash), ac.perm_h, nq,
           reinterpret_cast<unsigned long long*>(dbg->hash)));

@@ -126,7 +126,7 @@ struct rsot_cuda_atoms {
   rsot_cuda_ctx* ctx = nullptr;
   size_t nq = 0;
   double4* x = nullptr;  // {x0, x1, x2, m}
-  AtomCells cells;       // cell order (built on demand)
+  AtomCells cells;       // Hilbert order (built on first truncated use)
 };
 
 namespace {

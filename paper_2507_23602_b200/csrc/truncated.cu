@@ -148,17 +148,6 @@ __global__ void hilbert_keys_kernel(const double4* __restrict__ pts, int n, doub
   idx[i] = i;
 }
 
-__global__ void invert_perm_kernel(const int* __restrict__ perm, int n, int* __restrict__ inv) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) inv[perm[i]] = i;
-}
-
-__global__ void compose_kernel(const int* __restrict__ inv_h, const int* __restrict__ perm_c,
-                               int n, int* __restrict__ c2h) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) c2h[i] = inv_h[perm_c[i]];
-}
-
 __global__ void gather_d_kernel(const double* __restrict__ src, const int* __restrict__ idx,
                                 int n, double* __restrict__ dst) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -267,262 +256,6 @@ __device__ __forceinline__ WarpBox warp_box(bool valid, float a, float b, float 
     w.hi2 = fmaxf(w.hi2, __shfl_xor_sync(0xffffffffu, w.hi2, o));
   }
   return w;
-}
-
-// Compacts the indices of the staged points of a tile that can be within
-// the (conservative) FP32 threshold of ANY point of the warp's box into the
-// warp's list; returns the list length.  Never drops a point some lane
-// would accept or send to the exact test: for x in the box the box distance
-// is <= |x - y| (the threshold carries a relative margin for rounding).
-__device__ __forceinline__ int warp_cull(const float4* __restrict__ tF, int cnt, const WarpBox& w,
-                                         float thr, unsigned char* __restrict__ list) {
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
-  int nsel = 0;
-  for (int g = 0; g < cnt; g += 32) {
-    const int t = g + lane;
-    bool keep = false;
-    if (t < cnt) {
-      const float4 y = tF[t];
-      const float dx = fmaxf(fmaxf(w.lo0 - y.x, y.x - w.hi0), 0.f);
-      const float dy = fmaxf(fmaxf(w.lo1 - y.y, y.y - w.hi1), 0.f);
-      const float dz = fmaxf(fmaxf(w.lo2 - y.z, y.z - w.hi2), 0.f);
-      keep = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= thr;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (keep) list[nsel + __popc(m & lt)] = static_cast<unsigned char>(t);
-    nsel += __popc(m);
-  }
-  __syncwarp();
-  return nsel;
-}
-
-// ---------------------------------------------------------------------------
-// Pass A: atom-major truncated LSE.
-
-template <bool DEBUG>
-__global__ void __launch_bounds__(kT)
-trunc_passA(const double4* __restrict__ xs, int nq,
-            const double4* __restrict__ ys, const double* __restrict__ b2s,
-            const int* __restrict__ tperm, const int* __restrict__ cell_start,
-            GridDev g, const double* __restrict__ scal, double c2, double r2,
-            double r_scan, double* __restrict__ S_out,
-            double* __restrict__ shift_out, uint32_t* __restrict__ cnt_out,
-            uint64_t* __restrict__ hash_out) {
-  __shared__ double4 tD[kTileT];
-  __shared__ float4 tF[kTileT];
-  __shared__ int tK[kTileT];
-  __shared__ int rowStart[kT];
-  __shared__ int rowPref[kT + 1];
-  __shared__ int2 tbl[16];
-  __shared__ double sh[200];
-  __shared__ int shi[40];
-  __shared__ unsigned char wlist[kT / 32][kTileT];
-  load_exp2_table(tbl);
-
-  const int q = blockIdx.x * kT + threadIdx.x;
-  const bool valid = q < nq;
-  double4 xa = valid ? xs[q] : make_double4(0, 0, 0, 0);
-  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  if (valid) {
-    lo[0] = hi[0] = xa.x;
-    lo[1] = hi[1] = xa.y;
-    lo[2] = hi[2] = xa.z;
-  }
-  Region R;
-  setup_region(g, lo, hi, r2, r_scan, c2, sh, R);
-  const double x0 = xa.x - R.o[0], x1 = xa.y - R.o[1], x2 = xa.z - R.o[2];
-  const float xf0 = valid ? static_cast<float>(x0) : 1e30f;
-  const float xf1 = valid ? static_cast<float>(x1) : 1e30f;
-  const float xf2 = valid ? static_cast<float>(x2) : 1e30f;
-  const double X0 = 2.0 * c2 * x0, X1 = 2.0 * c2 * x1, X2 = 2.0 * c2 * x2;
-  const double xsq = c2 * fma(x2, x2, fma(x1, x1, x0 * x0));
-  // Spread chunk: carry the per-atom shift in every exponent (see dense.cu).
-  const bool wide = R.wide;
-  const WarpBox wb = warp_box(valid, xf0, xf1, xf2);
-  const float cull_thr = R.hi_thr * 1.0001f;
-  unsigned char* const mylist = wlist[threadIdx.x >> 5];
-  const double B = scal[kSlotB];
-  double S = 0.0;
-  uint32_t cnt = 0;
-  uint64_t hash = 0;
-
-  const int ny = R.c_hi[1] - R.c_lo[1] + 1;
-  const int nrows = ny * (R.c_hi[2] - R.c_lo[2] + 1);
-  for (int rb = 0; rb < nrows; rb += kT) {
-    int st = 0, ln = 0;
-    if (rb + threadIdx.x < nrows) row_range(g, R, r_scan, cell_start, rb + threadIdx.x, st, ln);
-    int total = 0;
-    const int pre = block_exclusive_scan<kT>(ln, shi, &total);
-    rowStart[threadIdx.x] = st;
-    rowPref[threadIdx.x] = pre;
-    if (threadIdx.x == 0) rowPref[kT] = total;
-    for (int base = 0; base < total; base += kTileT) {
-      const int cntT = min(kTileT, total - base);
-      __syncthreads();
-      for (int t = threadIdx.x; t < cntT; t += kT) {
-        const int s = base + t;
-        const int r = find_row(rowPref, s);
-        const int k = rowStart[r] + (s - rowPref[r]);
-        const double4 y = ys[k];
-        const double y0 = y.x - R.o[0], y1 = y.y - R.o[1], y2 = y.z - R.o[2];
-        const double yy = fma(y2, y2, fma(y1, y1, y0 * y0));
-        const double w = fmax(fma(-c2, yy, b2s[k]) - B, -1.0e5);
-        tD[t] = make_double4(y0, y1, y2, w);
-        tF[t] = make_float4(static_cast<float>(y0), static_cast<float>(y1),
-                            static_cast<float>(y2), 0.f);
-        tK[t] = k;
-      }
-      __syncthreads();
-      const int nsel = warp_cull(tF, cntT, wb, cull_thr, mylist);
-      // Two list items per step: the selection is resolved per lane (FP32
-      // test; exact fp64 reference predicate only inside the error band),
-      // then the exponentials run branch-free for the whole warp with the
-      // accumulation masked per lane, so there is no divergent code and
-      // the two items' FP64 chains interleave.
-      for (int i = 0; i < nsel; i += 2) {
-        const int t0 = mylist[i];
-        const int t1 = (i + 1 < nsel) ? mylist[i + 1] : t0;
-        const bool has1 = i + 1 < nsel;
-        const float4 ya = tF[t0];
-        const float4 yb = tF[t1];
-        const float ax = xf0 - ya.x, ay = xf1 - ya.y, az = xf2 - ya.z;
-        const float bx = xf0 - yb.x, by = xf1 - yb.y, bz = xf2 - yb.z;
-        const float d2a = fmaf(az, az, fmaf(ay, ay, ax * ax));
-        const float d2b = fmaf(bz, bz, fmaf(by, by, bx * bx));
-        bool in0 = d2a < R.lo_thr;
-        bool in1 = has1 && d2b < R.lo_thr;
-        const bool bd0 = !in0 && d2a <= R.hi_thr;
-        const bool bd1 = has1 && !in1 && d2b <= R.hi_thr;
-        if (__any_sync(0xffffffffu, bd0 || bd1)) {
-          if (bd0) {
-            const double4 yg = ys[tK[t0]];
-            in0 = exact_inside(xa.x, xa.y, xa.z, yg.x, yg.y, yg.z, r2);
-          }
-          if (bd1) {
-            const double4 yg = ys[tK[t1]];
-            in1 = exact_inside(xa.x, xa.y, xa.z, yg.x, yg.y, yg.z, r2);
-          }
-        }
-        if (__any_sync(0xffffffffu, in0 || in1)) {
-          const double4 y0 = tD[t0];
-          const double4 y1 = tD[t1];
-          double s0 = fma(X0, y0.x, fma(X1, y0.y, fma(X2, y0.z, y0.w)));
-          double s1 = fma(X0, y1.x, fma(X1, y1.y, fma(X2, y1.z, y1.w)));
-          if (wide) {
-            s0 -= xsq;
-            s1 -= xsq;
-          }
-          S = exp2_acc_masked(s0, S, tbl, in0);
-          S = exp2_acc_masked(s1, S, tbl, in1);
-          cnt += static_cast<uint32_t>(in0) + static_cast<uint32_t>(in1);
-          if (DEBUG) {
-            if (in0) hash += candidate_hash_term(static_cast<uint64_t>(tperm[tK[t0]]));
-            if (in1) hash += candidate_hash_term(static_cast<uint64_t>(tperm[tK[t1]]));
-          }
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (valid) {
-    S_out[q] = S;
-    shift_out[q] = wide ? 0.0 : xsq;
-    cnt_out[q] = cnt;
-    if (DEBUG) hash_out[q] = hash;
-  }
-}
-
-// Per-atom finalisation for atoms with a non-empty candidate set.
-__global__ void trunc_finalizeA(const double4* __restrict__ xs, int nq,
-                                const double* __restrict__ S_in,
-                                const double* __restrict__ shiftA,
-                                const uint32_t* __restrict__ cnt,
-                                double* __restrict__ scal, double eps,
-                                double* __restrict__ atomL,
-                                double* __restrict__ atomLam,
-                                double* __restrict__ atomJ,
-                                double* __restrict__ atomD,
-                                double* __restrict__ cntd,
-                                double* __restrict__ emptyd,
-                                int* __restrict__ flagged) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= nq) return;
-  const uint32_t c = cnt[q];
-  cntd[q] = c == 0 ? 1.0 : static_cast<double>(c);
-  emptyd[q] = c == 0 ? 1.0 : 0.0;
-  if (c == 0) {  // handled by the nearest kernel; never inside in pass B
-    atomLam[q] = -1.0e5;
-    return;
-  }
-  double S = S_in[q];
-  const double m = xs[q].w;
-  if (!(S >= 0x1p-960) || !(S <= 0x1p960)) {
-    unsigned long long* n = reinterpret_cast<unsigned long long*>(&scal[kSlotFlagCount]);
-    flagged[atomicAdd(n, 1ull)] = q;
-    S = 1.0;
-  }
-  const double L2 = (scal[kSlotB] - shiftA[q]) + log2(S);
-  const double L = L2 * kLn2;
-  atomL[q] = L;
-  atomJ[q] = eps * L * m;
-  atomD[q] = m * exp(-L);
-  atomLam[q] = fmax(log2(m) - L2, -1.0e5);
-}
-
-// Exact per-atom LSE (reference per-atom max shift) for flagged atoms.
-__global__ void trunc_exact_fallback(const double4* __restrict__ xs,
-                                     const double4* __restrict__ ys,
-                                     const int* __restrict__ tperm,
-                                     const int* __restrict__ cell_start, GridDev g,
-                                     const double* __restrict__ psi, double eps,
-                                     double r2, double r_scan,
-                                     const double* __restrict__ scal,
-                                     const int* __restrict__ flagged,
-                                     double* __restrict__ atomL,
-                                     double* __restrict__ atomLam,
-                                     double* __restrict__ atomJ,
-                                     double* __restrict__ atomD) {
-  __shared__ double sh[256];
-  const unsigned long long nflag =
-      *reinterpret_cast<const unsigned long long*>(&scal[kSlotFlagCount]);
-  for (unsigned long long f = blockIdx.x; f < nflag; f += gridDim.x) {
-    const int q = flagged[f];
-    const double4 a = xs[q];
-    int c_lo[3], c_hi[3];
-    const double v[3] = {a.x, a.y, a.z};
-    for (int d = 0; d < 3; ++d) {
-      c_lo[d] = cell_of(g, d, v[d] - r_scan);
-      c_hi[d] = cell_of(g, d, v[d] + r_scan);
-    }
-    double mx = -INFINITY, sum = 0.0;
-    for (int pass = 0; pass < 2; ++pass) {
-      double acc = pass == 0 ? -INFINITY : 0.0;
-      for (int cz = c_lo[2]; cz <= c_hi[2]; ++cz)
-        for (int cy = c_lo[1]; cy <= c_hi[1]; ++cy) {
-          const long long row = (static_cast<long long>(cz) * g.dims[1] + cy) * g.dims[0];
-          const int b = cell_start[row + c_lo[0]], e = cell_start[row + c_hi[0] + 1];
-          for (int k = b + threadIdx.x; k < e; k += blockDim.x) {
-            const double4 y = ys[k];
-            const double d2 = exact_sqdist(a.x, a.y, a.z, y.x, y.y, y.z);
-            if (!(d2 < r2)) continue;
-            const int j = tperm[k];
-            const double ex = reference_exponent(psi[j], d2, eps, y.w);
-            if (pass == 0) acc = fmax(acc, ex); else acc += exp(ex - mx);
-          }
-        }
-      if (pass == 0) mx = block_max<256>(acc, sh);
-      else sum = block_sum<256>(acc, sh);
-    }
-    if (threadIdx.x == 0) {
-      const double L = mx + log(sum);
-      atomL[q] = L;
-      atomJ[q] = eps * L * a.w;
-      atomD[q] = a.w * exp(-L);
-      atomLam[q] = fmax(log2(a.w) - L * kLog2e, -1.0e5);
-    }
-    __syncthreads();
-  }
 }
 
 // 192-bit fixed point (scale 2^150) accumulation of a non-negative double.
@@ -704,114 +437,6 @@ __global__ void trunc_nearest_empty(const double4* __restrict__ xs, int nq,
       }
     }
   }
-}
-
-// ---------------------------------------------------------------------------
-// Pass B: target-major truncated gather.
-
-__global__ void __launch_bounds__(kT)
-trunc_passB(const double4* __restrict__ ys, const double* __restrict__ b2s, int n,
-            const double4* __restrict__ xs, const double* __restrict__ atomLam,
-            const int* __restrict__ acell_start, GridDev g, double c2, double r2,
-            double r_scan, double* __restrict__ G_out) {
-  __shared__ double4 tD[kTileT];
-  __shared__ float4 tF[kTileT];
-  __shared__ int tK[kTileT];
-  __shared__ int rowStart[kT];
-  __shared__ int rowPref[kT + 1];
-  __shared__ int2 tbl[16];
-  __shared__ double sh[200];
-  __shared__ int shi[40];
-  __shared__ unsigned char wlist[kT / 32][kTileT];
-  load_exp2_table(tbl);
-
-  const int j = blockIdx.x * kT + threadIdx.x;
-  const bool valid = j < n;
-  const double4 yg = valid ? ys[j] : make_double4(0, 0, 0, 0);
-  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  if (valid) {
-    lo[0] = hi[0] = yg.x;
-    lo[1] = hi[1] = yg.y;
-    lo[2] = hi[2] = yg.z;
-  }
-  Region R;
-  setup_region(g, lo, hi, r2, r_scan, c2, sh, R);
-  const double y0 = yg.x - R.o[0], y1 = yg.y - R.o[1], y2 = yg.z - R.o[2];
-  const float yf0 = valid ? static_cast<float>(y0) : 1e30f;
-  const float yf1 = valid ? static_cast<float>(y1) : 1e30f;
-  const float yf2 = valid ? static_cast<float>(y2) : 1e30f;
-  const double T = valid ? fmax(fma(-c2, fma(y2, y2, fma(y1, y1, y0 * y0)), b2s[j]), -1.0e5) : -1.0e5;
-  double G = 0.0;
-  const WarpBox wb = warp_box(valid, yf0, yf1, yf2);
-  const float cull_thr = R.hi_thr * 1.0001f;
-  unsigned char* const mylist = wlist[threadIdx.x >> 5];
-
-  const int ny = R.c_hi[1] - R.c_lo[1] + 1;
-  const int nrows = ny * (R.c_hi[2] - R.c_lo[2] + 1);
-  const double c2x2 = 2.0 * c2;
-  for (int rb = 0; rb < nrows; rb += kT) {
-    int st = 0, ln = 0;
-    if (rb + threadIdx.x < nrows) row_range(g, R, r_scan, acell_start, rb + threadIdx.x, st, ln);
-    int total = 0;
-    const int pre = block_exclusive_scan<kT>(ln, shi, &total);
-    rowStart[threadIdx.x] = st;
-    rowPref[threadIdx.x] = pre;
-    if (threadIdx.x == 0) rowPref[kT] = total;
-    for (int base = 0; base < total; base += kTileT) {
-      const int cntT = min(kTileT, total - base);
-      __syncthreads();
-      for (int t = threadIdx.x; t < cntT; t += kT) {
-        const int s = base + t;
-        const int r = find_row(rowPref, s);
-        const int k = rowStart[r] + (s - rowPref[r]);
-        const double4 a = xs[k];
-        const double x0 = a.x - R.o[0], x1 = a.y - R.o[1], x2 = a.z - R.o[2];
-        const double xx = fma(x2, x2, fma(x1, x1, x0 * x0));
-        const double A = fma(-c2, xx, atomLam[k]);
-        tD[t] = make_double4(c2x2 * x0, c2x2 * x1, c2x2 * x2, A);
-        tF[t] = make_float4(static_cast<float>(x0), static_cast<float>(x1),
-                            static_cast<float>(x2), 0.f);
-        tK[t] = k;
-      }
-      __syncthreads();
-      const int nsel = warp_cull(tF, cntT, wb, cull_thr, mylist);
-      for (int i = 0; i < nsel; i += 2) {  // see pass A
-        const int t0 = mylist[i];
-        const int t1 = (i + 1 < nsel) ? mylist[i + 1] : t0;
-        const bool has1 = i + 1 < nsel;
-        const float4 xa = tF[t0];
-        const float4 xb = tF[t1];
-        const float ax = xa.x - yf0, ay = xa.y - yf1, az = xa.z - yf2;
-        const float bx = xb.x - yf0, by = xb.y - yf1, bz = xb.z - yf2;
-        const float d2a = fmaf(az, az, fmaf(ay, ay, ax * ax));
-        const float d2b = fmaf(bz, bz, fmaf(by, by, bx * bx));
-        bool in0 = d2a < R.lo_thr;
-        bool in1 = has1 && d2b < R.lo_thr;
-        const bool bd0 = !in0 && d2a <= R.hi_thr;
-        const bool bd1 = has1 && !in1 && d2b <= R.hi_thr;
-        if (__any_sync(0xffffffffu, bd0 || bd1)) {
-          if (bd0) {
-            const double4 xg = xs[tK[t0]];
-            in0 = exact_inside(xg.x, xg.y, xg.z, yg.x, yg.y, yg.z, r2);
-          }
-          if (bd1) {
-            const double4 xg = xs[tK[t1]];
-            in1 = exact_inside(xg.x, xg.y, xg.z, yg.x, yg.y, yg.z, r2);
-          }
-        }
-        if (__any_sync(0xffffffffu, in0 || in1)) {
-          const double4 Xa = tD[t0];
-          const double4 Xb = tD[t1];
-          const double s0 = fma(Xa.x, y0, fma(Xa.y, y1, fma(Xa.z, y2, T + Xa.w)));
-          const double s1 = fma(Xb.x, y0, fma(Xb.y, y1, fma(Xb.z, y2, T + Xb.w)));
-          G = exp2_acc_masked(s0, G, tbl, in0);
-          G = exp2_acc_masked(s1, G, tbl, in1);
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (valid) G_out[j] = G;
 }
 
 // ---------------------------------------------------------------------------
@@ -1301,15 +926,6 @@ __global__ void trunc_assemble_fp(const unsigned long long* __restrict__ gacc, i
   if (j < n) res[j] = fp_to_double(gacc + 3 * static_cast<size_t>(j));
 }
 
-__global__ void trunc_assemble(const double* __restrict__ G, const int* __restrict__ tperm,
-                               int n, const unsigned long long* __restrict__ empty_fp,
-                               double* __restrict__ res) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const int j = tperm[k];
-  res[j] = G[k] + fp_to_double(empty_fp + 3 * static_cast<size_t>(j));
-}
-
 __global__ void set_visited(double* __restrict__ res, int n, double nq) {
   res[n + kResVisited] = nq;
 }
@@ -1319,12 +935,6 @@ __global__ void scatter_debug(const T* __restrict__ src, const int* __restrict__
                               int nq, T* __restrict__ dst) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nq) dst[perm[i]] = src[i];
-}
-
-__global__ void cnt_fix_kernel(const uint32_t* __restrict__ cnt, int nq,
-                               uint32_t* __restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nq) out[i] = cnt[i] == 0 ? 1u : cnt[i];
 }
 
 __global__ void dense_debug_kernel(const double* __restrict__ atomL, int nq, int n,
@@ -1382,14 +992,6 @@ __global__ void max_cost_kernel(const double* __restrict__ d2, int m, double* __
   if (threadIdx.x == 0) *out = mx;
 }
 
-
-bool use_fused() {
-  static const bool v = [] {
-    const char* e = std::getenv("RSOT_TRUNC_PATH");
-    return !(e && std::string(e) == "split");
-  }();
-  return v;
-}
 
 double cells_per_radius() {
   static const double v = [] {
@@ -1464,7 +1066,6 @@ int build_hilbert(TruncWorkspace& ws, const double4* pts, int n, PointOrders& po
   if (ensure_key_buffers(ws, n, err)) return 1;
   TCK(realloc_exact(po.ph, n));
   TCK(realloc_exact(po.perm_h, n));
-  TCK(realloc_exact(po.inv_h, n));
   if (n > 0) {
     double sc[3];
     for (int d = 0; d < 3; ++d) {
@@ -1477,23 +1078,20 @@ int build_hilbert(TruncWorkspace& ws, const double4* pts, int n, PointOrders& po
     if (radix_sort(ws, n, 3 * kHilBits, s, err)) return 1;
     (note_launch(), gather4_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, ws.idx2, n, po.ph));
     TCK(cudaMemcpyAsync(po.perm_h, ws.idx2, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
-    (note_launch(), invert_perm_kernel<<<(n + 255) / 256, 256, 0, s>>>(po.perm_h, n, po.inv_h));
   }
   TCK(cudaGetLastError());
   po.n = n;
   po.hil_valid = true;
-  po.cell_valid = false;
   return 0;
 }
 
-// Cell order for grid g (requires the Hilbert order for c2h).
+// Cell order for grid g.
 int build_cells(TruncWorkspace& ws, const double4* pts, int n, const GridDesc& g,
                 PointOrders& po, cudaStream_t s, std::string& err) {
-  if (po.cell_valid && po.grid_id == g.id && po.n == n) return 0;
+  if (po.cell_valid && po.grid_id == g.id && po.ncell_pts == n) return 0;
   if (ensure_key_buffers(ws, n, err)) return 1;
   TCK(realloc_exact(po.pc, n));
   TCK(realloc_exact(po.perm_c, n));
-  TCK(realloc_exact(po.c2h, n));
   TCK(realloc_exact(po.cell_start, g.ncells + 1));
   const GridDev gd = to_dev(g);
   if (n > 0) {
@@ -1503,11 +1101,11 @@ int build_cells(TruncWorkspace& ws, const double4* pts, int n, const GridDesc& g
     if (radix_sort(ws, n, end_bit, s, err)) return 1;
     (note_launch(), gather4_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, ws.idx2, n, po.pc));
     TCK(cudaMemcpyAsync(po.perm_c, ws.idx2, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
-    (note_launch(), compose_kernel<<<(n + 255) / 256, 256, 0, s>>>(po.inv_h, po.perm_c, n, po.c2h));
   }
   (note_launch(), cell_start_kernel<<<(n + 1 + 255) / 256, 256, 0, s>>>(ws.keys2, n, g.ncells, po.cell_start));
   TCK(cudaGetLastError());
   po.grid_id = g.id;
+  po.ncell_pts = n;
   po.cell_valid = true;
   return 0;
 }
@@ -1547,17 +1145,17 @@ GridDesc plan_grid(const double blo[3], const double bhi[3], int n, double r) {
 }  // namespace
 
 void PointOrders::release() {
-  void* ptrs[] = {ph, perm_h, inv_h, pc, perm_c, c2h, cell_start};
+  void* ptrs[] = {ph, perm_h, pc, perm_c, cell_start};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   ph = pc = nullptr;
-  perm_h = inv_h = perm_c = c2h = cell_start = nullptr;
+  perm_h = perm_c = cell_start = nullptr;
   hil_valid = cell_valid = false;
 }
 
 void TruncWorkspace::release() {
-  void* ptrs[] = {cub_tmp, keys, keys2, idx, idx2, b2s, b2h, lamc, S, shiftA, atomL, atomLam,
-                  atomJ, atomD, cntd, emptyd, cnt, hash, flagged, empty_fp, G, pts, near_out, red};
+  void* ptrs[] = {cub_tmp, keys, keys2, idx, idx2, b2s, S, atomL, atomJ, atomD, cntd, emptyd, cnt,
+                  hash, empty_fp, pts, near_out, red};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   *this = TruncWorkspace();
@@ -1569,7 +1167,6 @@ static int ensure_target_cells(TruncWorkspace& ws, const DeviceTargets& t, Targe
     err = "target bounding box not set";
     return 1;
   }
-  if (build_hilbert(ws, t.y, t.n, tc, s, err)) return 1;
   const double want = std::max(r / cells_per_radius(), tc.hmin);
   if (tc.cell_valid && tc.g.h >= 0.75 * want && tc.g.h <= 1.35 * want) return 0;
   GridDesc g = plan_grid(tc.bbox_lo, tc.bbox_hi, t.n, r);
@@ -1582,38 +1179,31 @@ static int ensure_target_cells(TruncWorkspace& ws, const DeviceTargets& t, Targe
   return 0;
 }
 
-static int ensure_atom_cells(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
-                             const TargetCells& tc, cudaStream_t s, std::string& err) {
+static int ensure_atom_order(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
+                             cudaStream_t s, std::string& err) {
   if (!ac.bbox_set) {
     err = "atom bounding box not set";
     return 1;
   }
-  if (build_hilbert(ws, a.x, a.nq, ac, s, err)) return 1;
-  return build_cells(ws, a.x, a.nq, tc.g, ac, s, err);
+  return build_hilbert(ws, a.x, a.nq, ac, s, err);
 }
 
 static int ensure_trunc_ws(TruncWorkspace& ws, int nq, int n, std::string& err) {
   if (static_cast<size_t>(nq) > ws.atom_cap || !ws.S) {
     const size_t c = std::max<size_t>(nq, 1);
     TCK(realloc_exact(ws.S, c));
-    TCK(realloc_exact(ws.shiftA, c));
     TCK(realloc_exact(ws.atomL, c));
-    TCK(realloc_exact(ws.atomLam, c));
-    TCK(realloc_exact(ws.lamc, c));
     TCK(realloc_exact(ws.atomJ, c));
     TCK(realloc_exact(ws.atomD, c));
     TCK(realloc_exact(ws.cntd, c));
     TCK(realloc_exact(ws.emptyd, c));
     TCK(realloc_exact(ws.cnt, c));
     TCK(realloc_exact(ws.hash, c));
-    TCK(realloc_exact(ws.flagged, c));
     ws.atom_cap = c;
   }
-  if (static_cast<size_t>(n) > ws.tgt_cap || !ws.G) {
+  if (static_cast<size_t>(n) > ws.tgt_cap || !ws.b2s) {
     const size_t c = std::max<size_t>(n, 1);
-    TCK(realloc_exact(ws.G, c));
     TCK(realloc_exact(ws.b2s, c));
-    TCK(realloc_exact(ws.b2h, c));
     TCK(realloc_exact(ws.empty_fp, 3 * c));
     ws.tgt_cap = c;
   }
@@ -1634,7 +1224,7 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
   const double r_scan = r_use * (1.0 + 1e-9) + 1e-300;
   const int n = t.n, nq = a.nq;
   if (ensure_target_cells(ws, t, tc, r_use, s, err)) return 1;
-  if (ensure_atom_cells(ws, a, ac, tc, s, err)) return 1;
+  if (ensure_atom_order(ws, a, ac, s, err)) return 1;
   if (ensure_trunc_ws(ws, nq, n, err)) return 1;
   const GridDev g = to_dev(tc.g);
   const double c2 = kLog2e / (2.0 * eps);
@@ -1642,8 +1232,7 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
   TCK(cudaMemsetAsync(b.scal + kSlotFlagCount, 0, sizeof(double), s));
   TCK(cudaMemsetAsync(ws.empty_fp, 0, sizeof(unsigned long long) * 3 * static_cast<size_t>(n), s));
   (note_launch(), gather_d_kernel<<<(n + 255) / 256, 256, 0, s>>>(b.b2, tc.perm_c, n, ws.b2s));
-  (note_launch(), gather_d_kernel<<<(n + 255) / 256, 256, 0, s>>>(b.b2, tc.perm_h, n, ws.b2h));
-  if (nq > 0 && use_fused()) {
+  if (nq > 0) {
     FusedArgs A;
     A.xs = ac.ph; A.nq = nq; A.ys = tc.pc; A.b2s = ws.b2s; A.tperm = tc.perm_c;
     A.cell_start = tc.cell_start; A.g = g; A.scal = b.scal; A.psi = b.psi;
@@ -1685,60 +1274,6 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
           reinterpret_cast<unsigned long long*>(dbg->hash)));
       (note_launch(), scatter_debug<double><<<(nq + 255) / 256, 256, 0, s>>>(ws.atomL, ac.perm_h, nq,
                                                                           dbg->log_s));
-    }
-  } else if (nq > 0) {
-    const int nblk = (nq + kT - 1) / kT;
-    if (b.timing) cudaEventRecord(b.timing[1], s);
-    if (scan) {
-      if (dbg)
-        (note_launch(), trunc_passA<true><<<nblk, kT, 0, s>>>(ac.ph, nq, tc.pc, ws.b2s, tc.perm_c, tc.cell_start,
-                                              g, b.scal, c2, r2, r_scan, ws.S, ws.shiftA,
-                                              ws.cnt, ws.hash));
-      else
-        (note_launch(), trunc_passA<false><<<nblk, kT, 0, s>>>(ac.ph, nq, tc.pc, ws.b2s, tc.perm_c, tc.cell_start,
-                                               g, b.scal, c2, r2, r_scan, ws.S, ws.shiftA,
-                                               ws.cnt, ws.hash));
-    } else {
-      // radius <= 0: every candidate set is empty (spatial_index.cpp:50).
-      TCK(cudaMemsetAsync(ws.cnt, 0, sizeof(uint32_t) * nq, s));
-    }
-    if (b.timing) cudaEventRecord(b.timing[2], s);
-    (note_launch(), trunc_finalizeA<<<(nq + 255) / 256, 256, 0, s>>>(ac.ph, nq, ws.S, ws.shiftA, ws.cnt, b.scal,
-                                                     eps, ws.atomL, ws.atomLam, ws.atomJ,
-                                                     ws.atomD, ws.cntd, ws.emptyd, ws.flagged));
-    (note_launch(), trunc_exact_fallback<<<64, 256, 0, s>>>(ac.ph, tc.pc, tc.perm_c, tc.cell_start, g, b.psi, eps,
-                                            r2, r_scan, b.scal, ws.flagged, ws.atomL,
-                                            ws.atomLam, ws.atomJ, ws.atomD));
-    const int nb_near = std::min(4 * 148, (nq + 255) / 256 * 8 + 1);
-    if (dbg)
-      (note_launch(), trunc_nearest_empty<true><<<nb_near, 256, 0, s>>>(ac.ph, nq, ws.cnt, tc.pc, tc.perm_c,
-                                                        tc.cell_start, g, b.psi, eps, ws.atomL,
-                                                        ws.atomJ, ws.atomD, ws.empty_fp, ws.hash));
-    else
-      (note_launch(), trunc_nearest_empty<false><<<nb_near, 256, 0, s>>>(ac.ph, nq, ws.cnt, tc.pc, tc.perm_c,
-                                                         tc.cell_start, g, b.psi, eps, ws.atomL,
-                                                         ws.atomJ, ws.atomD, ws.empty_fp, ws.hash));
-    (note_launch(), gather_d_kernel<<<(nq + 255) / 256, 256, 0, s>>>(ws.atomLam, ac.c2h, nq, ws.lamc));
-    if (b.timing) cudaEventRecord(b.timing[3], s);
-    if (scan)
-      (note_launch(), trunc_passB<<<(n + kT - 1) / kT, kT, 0, s>>>(tc.ph, ws.b2h, n, ac.pc, ws.lamc,
-                                                   ac.cell_start, g, c2, r2, r_scan, ws.G));
-    else
-      TCK(cudaMemsetAsync(ws.G, 0, sizeof(double) * n, s));
-    if (b.timing) cudaEventRecord(b.timing[4], s);
-    (note_launch(), trunc_assemble<<<(n + 255) / 256, 256, 0, s>>>(ws.G, tc.perm_h, n, ws.empty_fp, b.res));
-    launch_det_sum(ws.atomJ, nq, ws.red, b.res + n + kResJ, s);
-    launch_det_sum(ws.atomD, nq, ws.red + 1024, b.res + n + kResD, s);
-    launch_det_sum(ws.cntd, nq, ws.red + 2048, b.res + n + kResPairs, s);
-    launch_det_sum(ws.emptyd, nq, ws.red + 3072, b.res + n + kResEmpty, s);
-    if (dbg) {
-      (note_launch(), cnt_fix_kernel<<<(nq + 255) / 256, 256, 0, s>>>(ws.cnt, nq, reinterpret_cast<uint32_t*>(ws.S)));
-      (note_launch(), scatter_debug<uint32_t><<<(nq + 255) / 256, 256, 0, s>>>(
-          reinterpret_cast<uint32_t*>(ws.S), ac.perm_h, nq, dbg->count));
-      (note_launch(), scatter_debug<unsigned long long><<<(nq + 255) / 256, 256, 0, s>>>(
-          reinterpret_cast<unsigned long long*>(ws.hash), ac.perm_h, nq,
-          reinterpret_cast<unsigned long long*>(dbg->hash)));
-      (note_launch(), scatter_debug<double><<<(nq + 255) / 256, 256, 0, s>>>(ws.atomL, ac.perm_h, nq, dbg->log_s));
     }
   } else {
     TCK(cudaMemsetAsync(b.res, 0, sizeof(double) * (n + kResTail), s));

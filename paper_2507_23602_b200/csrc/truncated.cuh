@@ -28,24 +28,23 @@ struct GridDesc {
   uint64_t id = 0;      // unique id of this grid build
 };
 
-// Two orders per point set:
-//   Hilbert order (radius independent, built once): consecutive runs of 128
-//     points are spatially compact CTA chunks (no long jumps, unlike
+// Point orders:
+//   Hilbert order (atoms; radius independent, built once): consecutive runs
+//     of kFA points are spatially compact CTA chunks (no long jumps, unlike
 //     Morton or row-major orders);
-//   cell order (per grid): rows of cells are contiguous scan ranges.
+//   cell order (targets; per grid): rows of cells are contiguous scan ranges.
 struct PointOrders {
   bool bbox_set = false;     // set once from the host data at creation
   double bbox_lo[3] = {0, 0, 0}, bbox_hi[3] = {0, 0, 0};
-  int n = 0;
+  int n = 0;                 // points in the Hilbert order
   bool hil_valid = false;
   double4* ph = nullptr;     // Hilbert-sorted copy
   int* perm_h = nullptr;     // Hilbert position -> original index
-  int* inv_h = nullptr;      // original index -> Hilbert position
   bool cell_valid = false;
   uint64_t grid_id = 0;      // grid the cell order was built for
+  int ncell_pts = 0;         // points in the cell order
   double4* pc = nullptr;     // cell-sorted copy
   int* perm_c = nullptr;     // cell position -> original index
-  int* c2h = nullptr;        // cell position -> Hilbert position
   int* cell_start = nullptr; // [ncells + 1]
   void release();
 };
@@ -70,13 +69,11 @@ struct TruncWorkspace {
   uint64_t* keys = nullptr; uint64_t* keys2 = nullptr; size_t keys_cap = 0;
   int* idx = nullptr; int* idx2 = nullptr; size_t idx_cap = 0;
   double* b2s = nullptr; size_t b2s_cap = 0;        // b2 in target cell order
-  double* b2h = nullptr;                              // b2 in target Hilbert order
-  double* lamc = nullptr;                             // atom Lam in cell order
-  double* S = nullptr; double* shiftA = nullptr; double* atomL = nullptr;
-  double* atomLam = nullptr; double* atomJ = nullptr; double* atomD = nullptr;
+  double* S = nullptr; double* atomL = nullptr;
+  double* atomJ = nullptr; double* atomD = nullptr;
   double* cntd = nullptr; double* emptyd = nullptr; uint32_t* cnt = nullptr;
-  uint64_t* hash = nullptr; int* flagged = nullptr; size_t atom_cap = 0;
-  unsigned long long* empty_fp = nullptr; double* G = nullptr; size_t tgt_cap = 0;
+  uint64_t* hash = nullptr; size_t atom_cap = 0;
+  unsigned long long* empty_fp = nullptr; size_t tgt_cap = 0;
   double* pts = nullptr; unsigned long long* near_out = nullptr; size_t pts_cap = 0;
   double* red = nullptr;  // reduction partials
   void release();

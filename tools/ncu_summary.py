@@ -88,6 +88,8 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--out", required=True)
     ap.add_argument("--note", default="")
+    ap.add_argument("--traffic-out", help="write {dram_bytes_per_eval} here (the --set full capture "
+                    "must hold exactly one evaluation's hot kernels)")
     a = ap.parse_args()
     summary = {"note": a.note}
     lines = [f"# ncu summary: {a.out}", "", a.note, ""]
@@ -110,6 +112,11 @@ def main():
             lines.append(f"- top stalls (warps per issue): {d['stalls_per_issue']}")
             lines.append("")
     json.dump(summary, open(a.out + ".json", "w"), indent=1)
+    if a.traffic_out and a.rep:
+        tb = sum(d.get("dram_read_bytes", 0.0) + d.get("dram_write_bytes", 0.0) for d in summary["kernels"]
+                 if d.get("dram_read_bytes") == d.get("dram_read_bytes"))
+        json.dump({"source": a.out + ".json", "kernels": [d["kernel"] for d in summary["kernels"]],
+                   "dram_bytes_per_eval": tb, "note": a.note}, open(a.traffic_out, "w"), indent=1)
     open(a.out + ".md", "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 

@@ -158,6 +158,18 @@ int rsot_cuda_softmax_refine(rsot_cuda_ctx* ctx, rsot_cuda_targets* coarse,
                              size_t n_fine, rsot_cuda_atoms* atoms, double eps,
                              double cutoff, double* psi_out);
 
+/* ---- precision ------------------------------------------------------------
+ * RSOT_CUDA_PRECISION_FP64 (default): every operation in fp64, within 1e-10
+ * relative of the reference.  RSOT_CUDA_PRECISION_FP32: truncated
+ * evaluations form the exponent in FP32 and exponentiate with the hardware
+ * ex2 (sums, J, D and the gradient accumulate in fp64; candidate sets stay
+ * exact); deviation from fp64 ~1e-6 relative, asserted <= 2e-5 in the tests.
+ * Dense evaluations (cutoff = +inf) always run in fp64.  BASELINE cfg5 asks
+ * for both precisions; the reference has fp64 only. */
+#define RSOT_CUDA_PRECISION_FP64 0
+#define RSOT_CUDA_PRECISION_FP32 1
+int rsot_cuda_ctx_set_precision(rsot_cuda_ctx* ctx, int precision);
+
 /* ---- measurement ----------------------------------------------------------
  * Enables CUDA-event timing of the hot kernels inside each evaluation
  * (events on the launching stream); rsot_cuda_last_kernel_ms returns the

@@ -110,6 +110,7 @@ struct rsot_cuda_ctx {
   RefineWorkspace refine;
   double* h_pinned = nullptr;  // small pinned staging for scalars
   bool timing = false;
+  int precision = RSOT_CUDA_PRECISION_FP64;
   cudaEvent_t ev[8] = {};
   double last_ms[3] = {0, 0, 0};
 };
@@ -197,7 +198,8 @@ int enqueue_eval(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
   launch_prologue(dt, b, eps, s);
   if (std::isfinite(cutoff)) {
     const int rc = run_truncated(c->trunc, da, a->cells, dt, t->cells, b, eps,
-                                 cutoff, c->num_sms, dbg, s, g_last_error);
+                                 cutoff, c->num_sms, dbg, s, g_last_error,
+                                 c->precision == RSOT_CUDA_PRECISION_FP32);
     if (rc != 0) return fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error);
   } else {
     const DenseLaunch plan = plan_dense(da.nq, dt.n, c->num_sms);
@@ -612,6 +614,14 @@ int rsot_cuda_softmax_refine(rsot_cuda_ctx* c, rsot_cuda_targets* coarse,
                           static_cast<int>(n_fine), eps, cutoff, c->num_sms, psi_out, c->stream,
                           g_last_error);
   return rc ? fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error) : RSOT_CUDA_OK;
+}
+
+int rsot_cuda_ctx_set_precision(rsot_cuda_ctx* c, int precision) {
+  if (!c) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null context");
+  if (precision != RSOT_CUDA_PRECISION_FP64 && precision != RSOT_CUDA_PRECISION_FP32)
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "unknown precision");
+  c->precision = precision;
+  return RSOT_CUDA_OK;
 }
 
 int rsot_cuda_ctx_set_timing(rsot_cuda_ctx* c, int enable) {

@@ -579,7 +579,8 @@ __device__ __forceinline__ void fused_stage(FusedSmem& sm, const FusedArgs& A, d
   }
 }
 
-__device__ __forceinline__ int fused_cull(const FusedSmem& sm, int cnt, const WarpBox& w,
+template <class SM>
+__device__ __forceinline__ int fused_cull(const SM& sm, int cnt, const WarpBox& w,
                                           float thr, unsigned char* __restrict__ list) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
@@ -604,7 +605,8 @@ __device__ __forceinline__ int fused_cull(const FusedSmem& sm, int cnt, const Wa
 }
 
 // Packed FP32x2 squared distances of item t to the thread's atoms (a, b).
-__device__ __forceinline__ float2 fused_d2(const FusedSmem& sm, const FusedAtoms& at, int t) {
+template <class SM, class AT>
+__device__ __forceinline__ float2 fused_d2(const SM& sm, const AT& at, int t) {
   const float4 n01 = sm.tN0[t];
   const float2 n2 = sm.tN1[t];
   const float2 dx = __fadd2_rn(at.F0, make_float2(n01.x, n01.y));
@@ -631,8 +633,9 @@ __device__ __forceinline__ void fused_masks(float2 d0, float2 d1, float2 nlo, fl
 }
 
 // Exact reference predicate for the pairs inside the FP32 error band (rare).
-__device__ __noinline__ void fused_exact(const FusedSmem& sm, const FusedArgs& A,
-                                         const FusedAtoms& at, int t0, int t1, unsigned border,
+template <class SM, class AT>
+__device__ __noinline__ void fused_exact(const SM& sm, const FusedArgs& A,
+                                         const AT& at, int t0, int t1, unsigned border,
                                          unsigned* in) {
   for (int bit = 0; bit < 4; ++bit) {
     if (!((border >> bit) & 1u)) continue;
@@ -806,13 +809,13 @@ template <bool DEBUG>
 __device__ __forceinline__ void fused_finalize(const FusedArgs& A, double B, bool wide, bool valid,
                                                bool nonempty, double cnt_contrib, uint32_t dbg_count,
                                                double S, double xsq, int q, uint64_t hash,
-                                               double& W) {
+                                               double& W, double smin = 0x1p-960) {
   const int lane = threadIdx.x & 31;
   const double4 p = valid ? A.xs[q] : make_double4(0, 0, 0, 0);
   const double shift = wide ? 0.0 : xsq;
   const double m = p.w;
   const bool empty = valid && !nonempty;
-  const bool flag = valid && nonempty && (!(S >= 0x1p-960) || !(S <= 0x1p960));
+  const bool flag = valid && nonempty && (!(S >= smin) || !(S <= 0x1p960));
   double L = (B - shift + log2(S)) * kLn2;
   double w = valid && nonempty ? m / S : 0.0;
   // Empty candidate sets: resolved after this kernel by trunc_nearest_empty
@@ -918,6 +921,274 @@ trunc_fused(FusedArgs A) {
     fused_scan<2, true, DEBUG>(sm, A, wb, cull_thr, B, at);
   else
     fused_scan<2, false, DEBUG>(sm, A, wb, cull_thr, B, at);
+}
+
+// ---------------------------------------------------------------------------
+// Mixed-precision (fp32) truncated evaluation (BASELINE cfg5 "fp32"): the
+// same scan, culling and exact candidate sets as trunc_fused; the exponent
+// s = (b2_j - B) - c2 d^2 is formed in FP32 from the FP32 pre-test distance
+// and 2^s runs on the MUFU (ex2.approx.ftz); tile sums in FP32 are added into
+// fp64 per-atom sums.  The shift B is per CTA: the running max of the staged
+// b2 (phase 1 rescales its sums when a tile raises it), so any psi range
+// keeps the sums in range.  Atoms whose sum falls below 2^-80 take the exact
+// fp64 path; empty sets use the same exact nearest kernel.  Expected
+// deviation from the fp64 result: ~1e-6 relative (FP32 distance and
+// exponent rounding); the tests assert 2e-5.
+
+struct Fused32Smem {
+  float tW[kT / 32][kTileT];           // per-warp (b2_j - B) of the staged tile
+  double tB2[kTileT];                  // b2_j of the staged tile
+  float4 tN0[kTileT];                  // {-y0', -y0', -y1', -y1'}
+  float2 tN1[kTileT];                  // {-y2', -y2'}
+  int tK[kTileT];                      // cell-order target position
+  int tJ[kTileT];                      // original target index
+  int rowStart[kT];
+  int rowPref[kT + 1];
+  unsigned char wlist[kT / 32][kTileT];
+  float colW[kT / 32][kTileT];
+  float wmax[kT / 32];
+  Region R;
+  double sh[200];
+  int shi[40];
+};
+
+struct Atoms32 {
+  float2 F0, F1, F2;         // local FP32 coordinates of (a, b)
+  float lo_thr, hi_thr;
+  int qa, qb;
+  double Sa, Sb;             // phase 1 sums relative to the CTA shift
+  uint32_t tot;
+  unsigned anyf;
+  uint32_t ca, cb;
+  uint64_t ha, hb;
+  float wa, wb;              // phase 2 weights m_q / S_q
+};
+
+__device__ __forceinline__ float fast_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float butterfly16f(float (&v)[16]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int h = 8, o = 16; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const float send = up ? v[i] : v[i + h];
+      const float keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+__device__ __forceinline__ void fused_stage32(Fused32Smem& sm, const FusedArgs& A, int base,
+                                              int cnt) {
+  const double o0 = sm.R.o[0], o1 = sm.R.o[1], o2 = sm.R.o[2];
+  float mx = -INFINITY;
+  for (int t = threadIdx.x; t < cnt; t += kT) {
+    const int s = base + t;
+    const int r = find_row(sm.rowPref, s);
+    const int k = sm.rowStart[r] + (s - sm.rowPref[r]);
+    const double4 y = A.ys[k];
+    const double b2 = A.b2s[k];
+    const float f0 = -static_cast<float>(y.x - o0), f1 = -static_cast<float>(y.y - o1),
+                f2 = -static_cast<float>(y.z - o2);
+    sm.tN0[t] = make_float4(f0, f0, f1, f1);
+    sm.tN1[t] = make_float2(f2, f2);
+    sm.tB2[t] = b2;
+    sm.tK[t] = k;
+    sm.tJ[t] = A.tperm[k];
+    mx = fmaxf(mx, __double2float_ru(b2));
+  }
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) sm.wmax[threadIdx.x >> 5] = mx;
+}
+
+template <int PHASE, bool DEBUG>
+__device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox& wb,
+                             float cull_thr, double& Bc, Atoms32& at) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* const list = sm.wlist[warp];
+  float* const tw = sm.tW[warp];
+  const float2 nlo = make_float2(-at.lo_thr, -at.lo_thr);
+  const float2 nhi = make_float2(-at.hi_thr, -at.hi_thr);
+  const float nc2f = static_cast<float>(-A.c2);
+  const float2 nc2 = make_float2(nc2f, nc2f);
+  const int ny = sm.R.c_hi[1] - sm.R.c_lo[1] + 1;
+  const int nrows = ny * (sm.R.c_hi[2] - sm.R.c_lo[2] + 1);
+  for (int rb = 0; rb < nrows; rb += kT) {
+    int st = 0, ln = 0;
+    if (rb + threadIdx.x < nrows)
+      row_range(A.g, sm.R, A.r_scan, A.cell_start, rb + threadIdx.x, st, ln);
+    int total = 0;
+    const int pre = block_exclusive_scan<kT>(ln, sm.shi, &total);
+    sm.rowStart[threadIdx.x] = st;
+    sm.rowPref[threadIdx.x] = pre;
+    if (threadIdx.x == 0) sm.rowPref[kT] = total;
+    for (int base = 0; base < total; base += kTileT) {
+      const int cnt = min(kTileT, total - base);
+      __syncthreads();
+      fused_stage32(sm, A, base, cnt);
+      __syncthreads();
+      if (PHASE == 1) {
+        // CTA-uniform running shift (same value in every thread)
+        const float tm = fmaxf(fmaxf(sm.wmax[0], sm.wmax[1]), fmaxf(sm.wmax[2], sm.wmax[3]));
+        const double Bn = fmax(Bc, static_cast<double>(tm));
+        if (Bn > Bc) {
+          const double f = exp2(Bc - Bn);
+          at.Sa *= f;
+          at.Sb *= f;
+          Bc = Bn;
+        }
+      }
+      for (int t = lane; t < cnt; t += 32) tw[t] = static_cast<float>(sm.tB2[t] - Bc);
+      const int nsel = fused_cull(sm, cnt, wb, cull_thr, list);
+      if (PHASE == 1) {
+        float2 acc = make_float2(0.f, 0.f);
+        for (int i = 0; i < nsel; i += 2) {
+          const bool v1 = i + 1 < nsel;
+          const int t0 = list[i];
+          const int t1 = v1 ? list[i + 1] : t0;
+          const float2 d0 = fused_d2(sm, at, t0), d1 = fused_d2(sm, at, t1);
+          unsigned in, bd;
+          fused_masks(d0, d1, nlo, nhi, v1, in, bd);
+          if (__any_sync(0xffffffffu, bd != 0u)) {
+            if (bd) fused_exact(sm, A, at, t0, t1, bd, &in);
+          }
+          if (__any_sync(0xffffffffu, in != 0u)) {
+            const float w0 = tw[t0], w1 = tw[t1];
+            const float2 s0 = __ffma2_rn(nc2, d0, make_float2(w0, w0));
+            const float2 s1 = __ffma2_rn(nc2, d1, make_float2(w1, w1));
+            const float e0a = fast_ex2((in & 1u) ? s0.x : -INFINITY);
+            const float e0b = fast_ex2((in & 2u) ? s0.y : -INFINITY);
+            const float e1a = fast_ex2((in & 4u) ? s1.x : -INFINITY);
+            const float e1b = fast_ex2((in & 8u) ? s1.y : -INFINITY);
+            acc = __fadd2_rn(acc, make_float2(e0a, e0b));
+            acc = __fadd2_rn(acc, make_float2(e1a, e1b));
+            at.tot += __popc(in);
+            at.anyf |= in;
+            if (DEBUG) {
+              at.ca += __popc(in & 5u);
+              at.cb += __popc(in & 10u);
+              if (in & 1u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
+              if (in & 4u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
+              if (in & 2u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
+              if (in & 8u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
+            }
+          }
+        }
+        at.Sa += static_cast<double>(acc.x);
+        at.Sb += static_cast<double>(acc.y);
+      } else {
+        float* const col = sm.colW[warp];
+        for (int s = lane; s < cnt; s += 32) col[s] = 0.f;
+        __syncwarp();
+        for (int b0 = 0; b0 < nsel; b0 += 16) {
+          float v[16];
+#pragma unroll
+          for (int p = 0; p < 8; ++p) {
+            const int i = b0 + 2 * p;
+            const bool v0 = i < nsel, v1 = i + 1 < nsel;
+            const int t0 = v0 ? list[i] : list[0];
+            const int t1 = v1 ? list[i + 1] : t0;
+            const float2 d0 = fused_d2(sm, at, t0), d1 = fused_d2(sm, at, t1);
+            unsigned in, bd;
+            fused_masks(d0, d1, nlo, nhi, v1, in, bd);
+            if (!v0) in = bd = 0u;
+            if (__any_sync(0xffffffffu, bd != 0u)) {
+              if (bd) fused_exact(sm, A, at, t0, t1, bd, &in);
+            }
+            v[2 * p] = 0.f;
+            v[2 * p + 1] = 0.f;
+            if (__any_sync(0xffffffffu, in != 0u)) {
+              const float w0 = tw[t0], w1 = tw[t1];
+              const float2 s0 = __ffma2_rn(nc2, d0, make_float2(w0, w0));
+              const float2 s1 = __ffma2_rn(nc2, d1, make_float2(w1, w1));
+              const float e0a = fast_ex2((in & 1u) ? s0.x : -INFINITY);
+              const float e0b = fast_ex2((in & 2u) ? s0.y : -INFINITY);
+              const float e1a = fast_ex2((in & 4u) ? s1.x : -INFINITY);
+              const float e1b = fast_ex2((in & 8u) ? s1.y : -INFINITY);
+              v[2 * p] = fmaf(at.wb, e0b, at.wa * e0a);
+              v[2 * p + 1] = fmaf(at.wb, e1b, at.wa * e1a);
+            }
+          }
+          const float tot = butterfly16f(v);
+          const int item = b0 + (lane >> 1);
+          if (!(lane & 1) && item < nsel) col[list[item]] = tot;
+        }
+        __syncthreads();
+        for (int s = threadIdx.x; s < cnt; s += kT) {
+          const double c = ((static_cast<double>(sm.colW[0][s]) + sm.colW[1][s]) + sm.colW[2][s]) +
+                           sm.colW[3][s];
+          if (c > 0.0) fp_add(A.gacc + 3 * static_cast<size_t>(sm.tJ[s]), c);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <bool DEBUG>
+__global__ void __launch_bounds__(kT, 4)
+trunc_fused32(FusedArgs A) {
+  __shared__ Fused32Smem sm;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Atoms32 at;
+  at.qa = blockIdx.x * kFA + warp * 64 + lane;
+  at.qb = at.qa + 32;
+  const bool va = at.qa < A.nq, vb = at.qb < A.nq;
+  const double4 pa = va ? A.xs[at.qa] : make_double4(0, 0, 0, 0);
+  const double4 pb = vb ? A.xs[at.qb] : make_double4(0, 0, 0, 0);
+  {
+    double lo[3], hi[3];
+    lo[0] = fmin(va ? pa.x : INFINITY, vb ? pb.x : INFINITY);
+    lo[1] = fmin(va ? pa.y : INFINITY, vb ? pb.y : INFINITY);
+    lo[2] = fmin(va ? pa.z : INFINITY, vb ? pb.z : INFINITY);
+    hi[0] = fmax(va ? pa.x : -INFINITY, vb ? pb.x : -INFINITY);
+    hi[1] = fmax(va ? pa.y : -INFINITY, vb ? pb.y : -INFINITY);
+    hi[2] = fmax(va ? pa.z : -INFINITY, vb ? pb.z : -INFINITY);
+    Region R;
+    setup_region(A.g, lo, hi, A.r2, A.r_scan, A.c2, sm.sh, R);
+    if (threadIdx.x == 0) sm.R = R;
+    __syncthreads();
+  }
+  const double o0 = sm.R.o[0], o1 = sm.R.o[1], o2 = sm.R.o[2];
+  const float big = 1e30f;
+  at.F0 = make_float2(va ? static_cast<float>(pa.x - o0) : big, vb ? static_cast<float>(pb.x - o0) : big);
+  at.F1 = make_float2(va ? static_cast<float>(pa.y - o1) : big, vb ? static_cast<float>(pb.y - o1) : big);
+  at.F2 = make_float2(va ? static_cast<float>(pa.z - o2) : big, vb ? static_cast<float>(pb.z - o2) : big);
+  at.lo_thr = sm.R.lo_thr;
+  at.hi_thr = sm.R.hi_thr;
+  at.Sa = at.Sb = 0.0;
+  at.tot = 0;
+  at.anyf = 0;
+  at.ca = at.cb = 0;
+  at.ha = at.hb = 0;
+  WarpBox wb;
+  {
+    const WarpBox w1 = warp_box(va, at.F0.x, at.F1.x, at.F2.x);
+    const WarpBox w2 = warp_box(vb, at.F0.y, at.F1.y, at.F2.y);
+    wb.lo0 = fminf(w1.lo0, w2.lo0); wb.lo1 = fminf(w1.lo1, w2.lo1); wb.lo2 = fminf(w1.lo2, w2.lo2);
+    wb.hi0 = fmaxf(w1.hi0, w2.hi0); wb.hi1 = fmaxf(w1.hi1, w2.hi1); wb.hi2 = fmaxf(w1.hi2, w2.hi2);
+  }
+  const float cull_thr = sm.R.hi_thr * 1.0001f;
+  double Bc = -0x1p1000;  // running CTA shift (log2 units)
+
+  fused_scan32<1, DEBUG>(sm, A, wb, cull_thr, Bc, at);
+
+  double wa, wb2;
+  fused_finalize<DEBUG>(A, Bc, true, va, (at.anyf & 5u) != 0u, static_cast<double>(at.tot), at.ca,
+                        at.Sa, 0.0, at.qa, at.ha, wa, 0x1p-80);
+  fused_finalize<DEBUG>(A, Bc, true, vb, (at.anyf & 10u) != 0u, 0.0, at.cb, at.Sb, 0.0, at.qb,
+                        at.hb, wb2, 0x1p-80);
+  at.wa = static_cast<float>(wa);
+  at.wb = static_cast<float>(wb2);
+
+  fused_scan32<2, DEBUG>(sm, A, wb, cull_thr, Bc, at);
 }
 
 __global__ void trunc_assemble_fp(const unsigned long long* __restrict__ gacc, int n,
@@ -1214,7 +1485,7 @@ static int ensure_trunc_ws(TruncWorkspace& ws, int nq, int n, std::string& err) 
 int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
                   const DeviceTargets& t, TargetCells& tc, EvalBuffers& b,
                   double eps, double cutoff, int num_sms, DebugOut* dbg,
-                  cudaStream_t s, std::string& err) {
+                  cudaStream_t s, std::string& err, bool fp32) {
   // cost.hpp:38-42 and spatial_index.cpp:50,54, evaluated on the host exactly
   // as the reference does.
   const double radius = cutoff < 0.0 ? 0.0 : std::sqrt(2.0 * cutoff);
@@ -1243,10 +1514,17 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
     A.cnt_out = ws.cnt;
     const int nblk = (nq + kFA - 1) / kFA;
     if (b.timing) cudaEventRecord(b.timing[1], s);
-    if (dbg)
-      (note_launch(), trunc_fused<true><<<nblk, kT, 0, s>>>(A));
-    else
-      (note_launch(), trunc_fused<false><<<nblk, kT, 0, s>>>(A));
+    if (fp32) {
+      if (dbg)
+        (note_launch(), trunc_fused32<true><<<nblk, kT, 0, s>>>(A));
+      else
+        (note_launch(), trunc_fused32<false><<<nblk, kT, 0, s>>>(A));
+    } else {
+      if (dbg)
+        (note_launch(), trunc_fused<true><<<nblk, kT, 0, s>>>(A));
+      else
+        (note_launch(), trunc_fused<false><<<nblk, kT, 0, s>>>(A));
+    }
     if (b.timing) cudaEventRecord(b.timing[2], s);
     const int nb_near = std::min(4 * num_sms, (nq + 255) / 256 * 8 + 1);
     if (dbg)

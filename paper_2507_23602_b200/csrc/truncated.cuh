@@ -85,7 +85,7 @@ struct TruncWorkspace {
 int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
                   const DeviceTargets& t, TargetCells& tc, EvalBuffers& b,
                   double eps, double cutoff, int num_sms, DebugOut* dbg,
-                  cudaStream_t s, std::string& err);
+                  cudaStream_t s, std::string& err, bool fp32 = false);
 
 // Dense-path debug outputs (count = N, hash over all targets, ln S_q).
 void launch_dense_debug(const DeviceAtoms& a, const DeviceTargets& t,

@@ -286,6 +286,15 @@ class Context:
     def synchronize(self) -> None:
         _lib.check(self.lib.rsot_cuda_ctx_synchronize(self.handle))
 
+    def set_precision(self, precision: str) -> None:
+        """"fp64" (default, reference-exact) or "fp32" (mixed: FP32 exponent
+        + hardware ex2 for truncated evaluations; ~1e-6 relative)."""
+        code = {"fp64": 0, "fp32": 1}.get(precision)
+        if code is None:
+            raise ValueError(f"unknown precision {precision!r}")
+        _lib.check(self.lib.rsot_cuda_ctx_set_precision(self.handle, code))
+        self.precision = precision
+
     def set_timing(self, on: bool) -> None:
         _lib.check(self.lib.rsot_cuda_ctx_set_timing(self.handle, 1 if on else 0))
 

@@ -7,6 +7,8 @@ import paper_2507_23602_b200 as rs
 from paper_2507_23602_b200 import synth
 
 ctx = rs.Context.default(0)
+prec = os.environ.get("RSOT_PRECISION", "fp64")
+ctx.set_precision(prec)
 for name in sys.argv[1:] or ["cfg3", "cfg5"]:
     p = synth.make(name)
     atoms = rs.SourceAtoms(dim=p.dim, points=p.atoms, masses=p.masses)
@@ -19,5 +21,5 @@ for name in sys.argv[1:] or ["cfg3", "cfg5"]:
                              rs.TruncationState(cutoff=p.cutoff(psi)), ctx=ctx)
         res.append(ctx.last_kernel_ms())
     a, b, t = np.median(np.array(res[1:]), axis=0)
-    print(f"cpr={os.environ.get('RSOT_CELLS_PER_RADIUS','default')} {name}: passA {a:.2f} ms passB {b:.2f} ms "
-          f"total {t:.2f} ms pairs {r.candidate_pairs} -> {r.candidate_pairs/t/1e6:.3e} pairs/s", flush=True)
+    print(f"{prec} cpr={os.environ.get('RSOT_CELLS_PER_RADIUS','default')} {name}: passA {a:.2f} ms passB {b:.2f} ms "
+          f"total {t:.2f} ms pairs {r.candidate_pairs} -> {r.candidate_pairs/t/1e-3:.3e} pairs/s", flush=True)

@@ -265,21 +265,36 @@ __device__ void fp_add(unsigned long long* acc, double m) {
   const double fr = frexp(m, &e);                   // m = fr * 2^e, fr in [0.5,1)
   const unsigned long long mant = static_cast<unsigned long long>(ldexp(fr, 53));
   const int sh = e - 53 + 150;                       // value = mant * 2^sh
-  unsigned long long limb[3] = {0, 0, 0};
+  unsigned long long l0 = 0, l1 = 0, l2 = 0;
   if (sh < 0) {
-    if (sh > -64) limb[0] = mant >> (-sh);
+    if (sh > -64) l0 = mant >> (-sh);
   } else {
     const int w = sh >> 6, b = sh & 63;
-    if (w < 3) limb[w] = mant << b;
-    if (b && w + 1 < 3) limb[w + 1] = mant >> (64 - b);
+    const unsigned long long lo = mant << b;
+    const unsigned long long hi = b ? (mant >> (64 - b)) : 0ull;
+    if (w == 0) { l0 = lo; l1 = hi; }
+    else if (w == 1) { l1 = lo; l2 = hi; }
+    else if (w == 2) { l2 = lo; }
   }
   unsigned long long carry = 0;
-  for (int i = 0; i < 3; ++i) {
-    const unsigned long long add = limb[i] + carry;
-    const unsigned long long c1 = (add < limb[i]) ? 1ull : 0ull;
-    if (add == 0 && c1 == 0) { carry = 0; continue; }
-    const unsigned long long old = atomicAdd(&acc[i], add);
-    carry = c1 + ((old + add < old) ? 1ull : 0ull);
+  {
+    if (l0) {
+      const unsigned long long old = atomicAdd(&acc[0], l0);
+      carry = (old + l0 < old) ? 1ull : 0ull;
+    }
+  }
+  {
+    const unsigned long long add = l1 + carry;
+    const unsigned long long c1 = (add < l1) ? 1ull : 0ull;
+    carry = c1;
+    if (add) {
+      const unsigned long long old = atomicAdd(&acc[1], add);
+      carry += (old + add < old) ? 1ull : 0ull;
+    }
+  }
+  {
+    const unsigned long long add = l2 + carry;
+    if (add) atomicAdd(&acc[2], add);
   }
 }
 
@@ -590,10 +605,10 @@ __device__ __forceinline__ int fused_cull(const SM& sm, int cnt, const WarpBox& 
     bool keep = false;
     if (t < cnt) {
       const float4 a = sm.tN0[t];
-      const float2 b = sm.tN1[t];
+      const float bz = sm.tN1[t].x;
       const float dx = fmaxf(fmaxf(w.lo0 + a.x, -a.x - w.hi0), 0.f);
       const float dy = fmaxf(fmaxf(w.lo1 + a.z, -a.z - w.hi1), 0.f);
-      const float dz = fmaxf(fmaxf(w.lo2 + b.x, -b.x - w.hi2), 0.f);
+      const float dz = fmaxf(fmaxf(w.lo2 + bz, -bz - w.hi2), 0.f);
       keep = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= thr;
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);
@@ -627,22 +642,28 @@ __device__ __forceinline__ unsigned sign4(float2 u0, float2 u1) {
 // lo <= d2 < hi (decided by the exact fp64 predicate).
 __device__ __forceinline__ void fused_masks(float2 d0, float2 d1, float2 nlo, float2 nhi, bool v1,
                                             unsigned& in, unsigned& border) {
-  const unsigned keep = v1 ? 0xFu : 0x3u;
-  in = sign4(__fadd2_rn(d0, nlo), __fadd2_rn(d1, nlo)) & keep;
-  border = sign4(__fadd2_rn(d0, nhi), __fadd2_rn(d1, nhi)) & keep & ~in;
+  const float lo = -nlo.x, hi = -nhi.x;
+  const bool i0 = d0.x < lo, i1 = d0.y < lo;
+  const bool i2 = v1 && d1.x < lo, i3 = v1 && d1.y < lo;
+  const bool b0 = !i0 && d0.x < hi, b1 = !i1 && d0.y < hi;
+  const bool b2 = v1 && !i2 && d1.x < hi, b3 = v1 && !i3 && d1.y < hi;
+  in = static_cast<unsigned>(i0) | (static_cast<unsigned>(i1) << 1) |
+       (static_cast<unsigned>(i2) << 2) | (static_cast<unsigned>(i3) << 3);
+  border = static_cast<unsigned>(b0) | (static_cast<unsigned>(b1) << 1) |
+           (static_cast<unsigned>(b2) << 2) | (static_cast<unsigned>(b3) << 3);
 }
 
 // Exact reference predicate for the pairs inside the FP32 error band (rare).
 template <class SM, class AT>
-__device__ __noinline__ void fused_exact(const SM& sm, const FusedArgs& A,
-                                         const AT& at, int t0, int t1, unsigned border,
-                                         unsigned* in) {
+__device__ __noinline__ unsigned fused_exact(const SM& sm, const FusedArgs& A, const AT& at, int t0,
+                                             int t1, unsigned border, unsigned in) {
   for (int bit = 0; bit < 4; ++bit) {
     if (!((border >> bit) & 1u)) continue;
     const double4 yg = A.ys[sm.tK[bit < 2 ? t0 : t1]];
     const double4 x = A.xs[(bit & 1) ? at.qb : at.qa];
-    if (exact_inside(x.x, x.y, x.z, yg.x, yg.y, yg.z, A.r2)) *in |= 1u << bit;
+    if (exact_inside(x.x, x.y, x.z, yg.x, yg.y, yg.z, A.r2)) in |= 1u << bit;
   }
+  return in;
 }
 
 // SAFE: CTA whose exponents may leave [-1020, 1000] (spread chunk or huge
@@ -691,7 +712,7 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
             d1 = fused_d2(sm, at, t1);
           }
           if (__any_sync(0xffffffffu, bd != 0u)) {
-            if (bd) fused_exact(sm, A, at, c0, c1, bd, &in);
+            if (bd) in = fused_exact(sm, A, at, c0, c1, bd, in);
           }
           if (__any_sync(0xffffffffu, in != 0u)) {
             const double4 y0 = sm.tD[c0];
@@ -734,7 +755,7 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
             fused_masks(fused_d2(sm, at, t0), fused_d2(sm, at, t1), nlo, nhi, v1, in, bd);
             if (!v0) in = bd = 0u;
             if (__any_sync(0xffffffffu, bd != 0u)) {
-              if (bd) fused_exact(sm, A, at, t0, t1, bd, &in);
+              if (bd) in = fused_exact(sm, A, at, t0, t1, bd, in);
             }
             v[2 * p] = 0.0;
             v[2 * p + 1] = 0.0;
@@ -936,10 +957,8 @@ trunc_fused(FusedArgs A) {
 // exponent rounding); the tests assert 2e-5.
 
 struct Fused32Smem {
-  float tW[kT / 32][kTileT];           // per-warp (b2_j - B) of the staged tile
-  double tB2[kTileT];                  // b2_j of the staged tile
   float4 tN0[kTileT];                  // {-y0', -y0', -y1', -y1'}
-  float2 tN1[kTileT];                  // {-y2', -y2'}
+  float4 tN1[kTileT];                  // {-y2', -y2', b2_j - B, b2_j - B}
   int tK[kTileT];                      // cell-order target position
   int tJ[kTileT];                      // original target index
   int rowStart[kT];
@@ -957,10 +976,8 @@ struct Atoms32 {
   float lo_thr, hi_thr;
   int qa, qb;
   double Sa, Sb;             // phase 1 sums relative to the CTA shift
-  uint32_t tot;
-  unsigned anyf;
-  uint32_t ca, cb;
-  uint64_t ha, hb;
+  uint32_t ca, cb;           // accepted pairs per atom
+  uint64_t ha, hb;           // candidate hashes (debug)
   float wa, wb;              // phase 2 weights m_q / S_q
 };
 
@@ -985,27 +1002,179 @@ __device__ __forceinline__ float butterfly16f(float (&v)[16]) {
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
+// Stages tile [base, base + cnt) (kTileT = 2 kT: entries tid and tid + kT).
+// The tile's b2 maximum is reduced before the tile is written, so the staged
+// exponent offsets are relative to the updated CTA shift.  Two barriers per
+// tile; the global loads are issued before the first one.
+template <int PHASE>
 __device__ __forceinline__ void fused_stage32(Fused32Smem& sm, const FusedArgs& A, int base,
-                                              int cnt) {
-  const double o0 = sm.R.o[0], o1 = sm.R.o[1], o2 = sm.R.o[2];
+                                              int cnt, double& Bc, Atoms32& at) {
+  static_assert(kTileT == 2 * kT, "two staged entries per thread");
+  double4 y[2];
+  double b2[2];
+  int k[2];
   float mx = -INFINITY;
-  for (int t = threadIdx.x; t < cnt; t += kT) {
-    const int s = base + t;
-    const int r = find_row(sm.rowPref, s);
-    const int k = sm.rowStart[r] + (s - sm.rowPref[r]);
-    const double4 y = A.ys[k];
-    const double b2 = A.b2s[k];
-    const float f0 = -static_cast<float>(y.x - o0), f1 = -static_cast<float>(y.y - o1),
-                f2 = -static_cast<float>(y.z - o2);
-    sm.tN0[t] = make_float4(f0, f0, f1, f1);
-    sm.tN1[t] = make_float2(f2, f2);
-    sm.tB2[t] = b2;
-    sm.tK[t] = k;
-    sm.tJ[t] = A.tperm[k];
-    mx = fmaxf(mx, __double2float_ru(b2));
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int t = threadIdx.x + u * kT;
+    k[u] = 0;
+    b2[u] = -INFINITY;
+    y[u] = make_double4(0, 0, 0, 0);
+    if (t < cnt) {
+      const int s = base + t;
+      const int r = find_row(sm.rowPref, s);
+      k[u] = sm.rowStart[r] + (s - sm.rowPref[r]);
+      y[u] = A.ys[k[u]];
+      b2[u] = A.b2s[k[u]];
+      mx = fmaxf(mx, __double2float_ru(b2[u]));
+    }
   }
-  mx = warp_max(mx);
-  if ((threadIdx.x & 31) == 0) sm.wmax[threadIdx.x >> 5] = mx;
+  if (PHASE == 1) {
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) sm.wmax[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();  // previous tile fully consumed; wmax visible
+  if (PHASE == 1) {
+    // CTA-uniform running shift (same value in every thread)
+    const float tm = fmaxf(fmaxf(sm.wmax[0], sm.wmax[1]), fmaxf(sm.wmax[2], sm.wmax[3]));
+    const double Bn = fmax(Bc, static_cast<double>(tm));
+    if (Bn > Bc) {
+      const double f = exp2(Bc - Bn);
+      at.Sa *= f;
+      at.Sb *= f;
+      Bc = Bn;
+    }
+  }
+  const double o0 = sm.R.o[0], o1 = sm.R.o[1], o2 = sm.R.o[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int t = threadIdx.x + u * kT;
+    if (t < cnt) {
+      const float f0 = -static_cast<float>(y[u].x - o0), f1 = -static_cast<float>(y[u].y - o1),
+                  f2 = -static_cast<float>(y[u].z - o2);
+      const float w = static_cast<float>(b2[u] - Bc);
+      sm.tN0[t] = make_float4(f0, f0, f1, f1);
+      sm.tN1[t] = make_float4(f2, f2, w, w);
+      sm.tK[t] = k[u];
+      sm.tJ[t] = A.tperm[k[u]];
+    }
+  }
+  __syncthreads();
+}
+
+// FP32x2 squared distances of item t to atoms (a, b) and the item's offset.
+__device__ __forceinline__ float2 fused_d2w(const Fused32Smem& sm, const Atoms32& at, int t,
+                                           float& w) {
+  const float4 n01 = sm.tN0[t];
+  const float4 n2 = sm.tN1[t];
+  const float2 dx = __fadd2_rn(at.F0, make_float2(n01.x, n01.y));
+  const float2 dy = __fadd2_rn(at.F1, make_float2(n01.z, n01.w));
+  const float2 dz = __fadd2_rn(at.F2, make_float2(n2.x, n2.y));
+  w = n2.z;
+  float2 d2 = __fmul2_rn(dx, dx);
+  d2 = __ffma2_rn(dy, dy, d2);
+  return __ffma2_rn(dz, dz, d2);
+}
+
+// Per-scan constants of the FP32 step.
+struct Step32 {
+  float lo;        // pairs with d2 < lo are in (FP32 decision)
+  float nmid, hw;  // band [lo, hi] <=> |d2 - mid| <= hw (inflated: no misses)
+  float nbig, lobig;  // indicator sat(lo*BIG - d2*BIG) = [d2 < lo] exactly
+  float2 nlo, nhi;
+  float2 nc2;
+};
+
+__device__ __forceinline__ float sat_fma(float a, float b, float c) {
+  float r;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// Step of 2 targets (t0, t1; PAIR = false: t0 only) x atoms (a, b).
+// PHASE 1 accumulates the masked exponentials into acc and the accepted
+// pair counts into cnt (floats, exact per tile); PHASE 2 returns the
+// weighted column values of t0 and t1.  Pairs in the FP32 error band take
+// the exact fp64 predicate (warp-uniform slow path, also used in DEBUG
+// builds for the candidate hashes).
+template <int PHASE, bool PAIR, bool DEBUG>
+__device__ __forceinline__ float2 step32(const Fused32Smem& sm, const FusedArgs& A, Atoms32& at,
+                                         const Step32& K, int t0, int t1, float2& acc,
+                                         float2& cnt) {
+  float w0, w1 = 0.f;
+  const float2 d0 = fused_d2w(sm, at, t0, w0);
+  const float2 d1 = PAIR ? fused_d2w(sm, at, t1, w1) : d0;
+  float bm = fminf(fabsf(d0.x + K.nmid), fabsf(d0.y + K.nmid));
+  if (PAIR) bm = fminf(bm, fminf(fabsf(d1.x + K.nmid), fabsf(d1.y + K.nmid)));
+  float2 i0, i1 = make_float2(0.f, 0.f);
+  bool work;
+  if (DEBUG || __any_sync(0xffffffffu, bm <= K.hw)) {
+    unsigned in, bd;
+    fused_masks(d0, d1, K.nlo, K.nhi, PAIR, in, bd);
+    if (bd) in = fused_exact(sm, A, at, t0, t1, bd, in);
+    i0 = make_float2((in & 1u) ? 1.f : 0.f, (in & 2u) ? 1.f : 0.f);
+    if (PAIR) i1 = make_float2((in & 4u) ? 1.f : 0.f, (in & 8u) ? 1.f : 0.f);
+    if (DEBUG && PHASE == 1) {
+      if (in & 1u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
+      if (in & 4u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
+      if (in & 2u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
+      if (in & 8u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
+    }
+    work = __any_sync(0xffffffffu, in != 0u);
+  } else {
+    float m = fminf(d0.x, d0.y);
+    if (PAIR) m = fminf(m, fminf(d1.x, d1.y));
+    work = __any_sync(0xffffffffu, m < K.lo);
+    if (work) {
+      i0 = make_float2(sat_fma(d0.x, K.nbig, K.lobig), sat_fma(d0.y, K.nbig, K.lobig));
+      if (PAIR) i1 = make_float2(sat_fma(d1.x, K.nbig, K.lobig), sat_fma(d1.y, K.nbig, K.lobig));
+    }
+  }
+  float2 out = make_float2(0.f, 0.f);
+  if (work) {
+    const float2 s0 = __ffma2_rn(K.nc2, d0, make_float2(w0, w0));
+    const float2 e0 = __fmul2_rn(make_float2(fast_ex2(s0.x), fast_ex2(s0.y)), i0);
+    float2 e1 = make_float2(0.f, 0.f);
+    if (PAIR) {
+      const float2 s1 = __ffma2_rn(K.nc2, d1, make_float2(w1, w1));
+      e1 = __fmul2_rn(make_float2(fast_ex2(s1.x), fast_ex2(s1.y)), i1);
+    }
+    if (PHASE == 1) {
+      acc = __fadd2_rn(acc, e0);
+      cnt = __fadd2_rn(cnt, i0);
+      if (PAIR) {
+        acc = __fadd2_rn(acc, e1);
+        cnt = __fadd2_rn(cnt, i1);
+      }
+    } else {
+      out.x = fmaf(at.wb, e0.y, at.wa * e0.x);
+      if (PAIR) out.y = fmaf(at.wb, e1.y, at.wa * e1.x);
+    }
+  }
+  return out;
+}
+
+template <bool FULL, bool DEBUG>
+__device__ __forceinline__ void batch32(const Fused32Smem& sm, const FusedArgs& A, Atoms32& at,
+                                        const Step32& K, const unsigned char* list, int b0, int nsel,
+                                        float* col) {
+  const int lane = threadIdx.x & 31;
+  float v[16];
+  float2 dummy = make_float2(0.f, 0.f), dummy2 = dummy;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int i = b0 + 2 * p;
+    float2 val = make_float2(0.f, 0.f);
+    if (FULL || i + 1 < nsel)
+      val = step32<2, true, DEBUG>(sm, A, at, K, list[i], list[i + 1], dummy, dummy2);
+    else if (i < nsel)
+      val = step32<2, false, DEBUG>(sm, A, at, K, list[i], list[i], dummy, dummy2);
+    v[2 * p] = val.x;
+    v[2 * p + 1] = val.y;
+  }
+  const float tot = butterfly16f(v);
+  const int item = b0 + (lane >> 1);
+  if (!(lane & 1) && item < nsel) col[list[item]] = tot;
 }
 
 template <int PHASE, bool DEBUG>
@@ -1013,11 +1182,26 @@ __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox&
                              float cull_thr, double& Bc, Atoms32& at) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* const list = sm.wlist[warp];
-  float* const tw = sm.tW[warp];
-  const float2 nlo = make_float2(-at.lo_thr, -at.lo_thr);
-  const float2 nhi = make_float2(-at.hi_thr, -at.hi_thr);
+  Step32 K;
+  K.lo = at.lo_thr;
+  K.nlo = make_float2(-at.lo_thr, -at.lo_thr);
+  K.nhi = make_float2(-at.hi_thr, -at.hi_thr);
+  {
+    // [lo, hi] inside [mid - hw, mid + hw] after every FP32 rounding: the
+    // rounding of mid and of d2 - mid is covered by 4 ulp(hi) of slack
+    const double lo = at.lo_thr, hi = at.hi_thr;
+    const float mid = static_cast<float>(0.5 * (lo + hi));
+    K.nmid = -mid;
+    K.hw = static_cast<float>(fmax(hi - mid, mid - lo) * (1.0 + 0x1p-20) +
+                              4.0 * fabs(hi) * 0x1p-23) + 1e-30f;
+  }
+  // power of two: lo * BIG and d2 * BIG are exact, so the FMA rounds
+  // BIG (lo - d2) once: >= 2^77 when d2 < lo, <= 0 otherwise
+  const float big = at.lo_thr > 0.f ? ldexpf(1.f, 100 - ilogbf(at.lo_thr)) : 0.f;
+  K.nbig = -big;
+  K.lobig = at.lo_thr * big;
   const float nc2f = static_cast<float>(-A.c2);
-  const float2 nc2 = make_float2(nc2f, nc2f);
+  K.nc2 = make_float2(nc2f, nc2f);
   const int ny = sm.R.c_hi[1] - sm.R.c_lo[1] + 1;
   const int nrows = ny * (sm.R.c_hi[2] - sm.R.c_lo[2] + 1);
   for (int rb = 0; rb < nrows; rb += kT) {
@@ -1031,95 +1215,24 @@ __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox&
     if (threadIdx.x == 0) sm.rowPref[kT] = total;
     for (int base = 0; base < total; base += kTileT) {
       const int cnt = min(kTileT, total - base);
-      __syncthreads();
-      fused_stage32(sm, A, base, cnt);
-      __syncthreads();
-      if (PHASE == 1) {
-        // CTA-uniform running shift (same value in every thread)
-        const float tm = fmaxf(fmaxf(sm.wmax[0], sm.wmax[1]), fmaxf(sm.wmax[2], sm.wmax[3]));
-        const double Bn = fmax(Bc, static_cast<double>(tm));
-        if (Bn > Bc) {
-          const double f = exp2(Bc - Bn);
-          at.Sa *= f;
-          at.Sb *= f;
-          Bc = Bn;
-        }
-      }
-      for (int t = lane; t < cnt; t += 32) tw[t] = static_cast<float>(sm.tB2[t] - Bc);
+      fused_stage32<PHASE>(sm, A, base, cnt, Bc, at);
       const int nsel = fused_cull(sm, cnt, wb, cull_thr, list);
       if (PHASE == 1) {
-        float2 acc = make_float2(0.f, 0.f);
-        for (int i = 0; i < nsel; i += 2) {
-          const bool v1 = i + 1 < nsel;
-          const int t0 = list[i];
-          const int t1 = v1 ? list[i + 1] : t0;
-          const float2 d0 = fused_d2(sm, at, t0), d1 = fused_d2(sm, at, t1);
-          unsigned in, bd;
-          fused_masks(d0, d1, nlo, nhi, v1, in, bd);
-          if (__any_sync(0xffffffffu, bd != 0u)) {
-            if (bd) fused_exact(sm, A, at, t0, t1, bd, &in);
-          }
-          if (__any_sync(0xffffffffu, in != 0u)) {
-            const float w0 = tw[t0], w1 = tw[t1];
-            const float2 s0 = __ffma2_rn(nc2, d0, make_float2(w0, w0));
-            const float2 s1 = __ffma2_rn(nc2, d1, make_float2(w1, w1));
-            const float e0a = fast_ex2((in & 1u) ? s0.x : -INFINITY);
-            const float e0b = fast_ex2((in & 2u) ? s0.y : -INFINITY);
-            const float e1a = fast_ex2((in & 4u) ? s1.x : -INFINITY);
-            const float e1b = fast_ex2((in & 8u) ? s1.y : -INFINITY);
-            acc = __fadd2_rn(acc, make_float2(e0a, e0b));
-            acc = __fadd2_rn(acc, make_float2(e1a, e1b));
-            at.tot += __popc(in);
-            at.anyf |= in;
-            if (DEBUG) {
-              at.ca += __popc(in & 5u);
-              at.cb += __popc(in & 10u);
-              if (in & 1u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
-              if (in & 4u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
-              if (in & 2u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
-              if (in & 8u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
-            }
-          }
-        }
+        float2 acc = make_float2(0.f, 0.f), cn = make_float2(0.f, 0.f);
+        int i = 0;
+        for (; i + 1 < nsel; i += 2) step32<1, true, DEBUG>(sm, A, at, K, list[i], list[i + 1], acc, cn);
+        if (i < nsel) step32<1, false, DEBUG>(sm, A, at, K, list[i], list[i], acc, cn);
         at.Sa += static_cast<double>(acc.x);
         at.Sb += static_cast<double>(acc.y);
+        at.ca += static_cast<uint32_t>(cn.x);
+        at.cb += static_cast<uint32_t>(cn.y);
       } else {
         float* const col = sm.colW[warp];
         for (int s = lane; s < cnt; s += 32) col[s] = 0.f;
         __syncwarp();
-        for (int b0 = 0; b0 < nsel; b0 += 16) {
-          float v[16];
-#pragma unroll
-          for (int p = 0; p < 8; ++p) {
-            const int i = b0 + 2 * p;
-            const bool v0 = i < nsel, v1 = i + 1 < nsel;
-            const int t0 = v0 ? list[i] : list[0];
-            const int t1 = v1 ? list[i + 1] : t0;
-            const float2 d0 = fused_d2(sm, at, t0), d1 = fused_d2(sm, at, t1);
-            unsigned in, bd;
-            fused_masks(d0, d1, nlo, nhi, v1, in, bd);
-            if (!v0) in = bd = 0u;
-            if (__any_sync(0xffffffffu, bd != 0u)) {
-              if (bd) fused_exact(sm, A, at, t0, t1, bd, &in);
-            }
-            v[2 * p] = 0.f;
-            v[2 * p + 1] = 0.f;
-            if (__any_sync(0xffffffffu, in != 0u)) {
-              const float w0 = tw[t0], w1 = tw[t1];
-              const float2 s0 = __ffma2_rn(nc2, d0, make_float2(w0, w0));
-              const float2 s1 = __ffma2_rn(nc2, d1, make_float2(w1, w1));
-              const float e0a = fast_ex2((in & 1u) ? s0.x : -INFINITY);
-              const float e0b = fast_ex2((in & 2u) ? s0.y : -INFINITY);
-              const float e1a = fast_ex2((in & 4u) ? s1.x : -INFINITY);
-              const float e1b = fast_ex2((in & 8u) ? s1.y : -INFINITY);
-              v[2 * p] = fmaf(at.wb, e0b, at.wa * e0a);
-              v[2 * p + 1] = fmaf(at.wb, e1b, at.wa * e1a);
-            }
-          }
-          const float tot = butterfly16f(v);
-          const int item = b0 + (lane >> 1);
-          if (!(lane & 1) && item < nsel) col[list[item]] = tot;
-        }
+        int b0 = 0;
+        for (; b0 + 16 <= nsel; b0 += 16) batch32<true, DEBUG>(sm, A, at, K, list, b0, nsel, col);
+        if (b0 < nsel) batch32<false, DEBUG>(sm, A, at, K, list, b0, nsel, col);
         __syncthreads();
         for (int s = threadIdx.x; s < cnt; s += kT) {
           const double c = ((static_cast<double>(sm.colW[0][s]) + sm.colW[1][s]) + sm.colW[2][s]) +
@@ -1164,8 +1277,6 @@ trunc_fused32(FusedArgs A) {
   at.lo_thr = sm.R.lo_thr;
   at.hi_thr = sm.R.hi_thr;
   at.Sa = at.Sb = 0.0;
-  at.tot = 0;
-  at.anyf = 0;
   at.ca = at.cb = 0;
   at.ha = at.hb = 0;
   WarpBox wb;
@@ -1181,10 +1292,10 @@ trunc_fused32(FusedArgs A) {
   fused_scan32<1, DEBUG>(sm, A, wb, cull_thr, Bc, at);
 
   double wa, wb2;
-  fused_finalize<DEBUG>(A, Bc, true, va, (at.anyf & 5u) != 0u, static_cast<double>(at.tot), at.ca,
+  fused_finalize<DEBUG>(A, Bc, true, va, at.ca != 0u, static_cast<double>(at.ca + at.cb), at.ca,
                         at.Sa, 0.0, at.qa, at.ha, wa, 0x1p-80);
-  fused_finalize<DEBUG>(A, Bc, true, vb, (at.anyf & 10u) != 0u, 0.0, at.cb, at.Sb, 0.0, at.qb,
-                        at.hb, wb2, 0x1p-80);
+  fused_finalize<DEBUG>(A, Bc, true, vb, at.cb != 0u, 0.0, at.cb, at.Sb, 0.0, at.qb, at.hb, wb2,
+                        0x1p-80);
   at.wa = static_cast<float>(wa);
   at.wb = static_cast<float>(wb2);
 

@@ -109,3 +109,11 @@ def test_fp32_vs_fp64_full_cfg5(ctx32):
     scale = float(np.max(r64.gradient + 2 * p.nu))
     assert np.max(np.abs(r32.gradient - r64.gradient)) <= TOL32 * scale
     assert abs(r32.D - r64.D) <= TOL32 * r64.D
+    ctx64 = rs.Context.default(0)
+    for k in (1, 2, 3):
+        psi = p.psi(k)
+        tr = rs.TruncationState(cutoff=p.cutoff(psi))
+        a = rs.evaluate_dual(atoms, tgt, rs.DualPotential(psi), cfg, tr, ctx=ctx32)
+        b = rs.evaluate_dual(atoms, tgt, rs.DualPotential(psi), cfg, tr, ctx=ctx64)
+        assert a.candidate_pairs == b.candidate_pairs and a.empty_candidate_atoms == b.empty_candidate_atoms
+        assert abs(a.J - b.J) <= TOL32 * abs(b.J)

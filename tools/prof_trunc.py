@@ -6,6 +6,7 @@ from paper_2507_23602_b200 import synth
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
 nev = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 ctx = rs.Context.default(0)
+ctx.set_precision(os.environ.get("RSOT_PRECISION", "fp64"))
 p = synth.make(name)
 atoms = rs.SourceAtoms(dim=p.dim, points=p.atoms, masses=p.masses)
 tgt = rs.TargetMeasure(dim=p.dim, points=p.targets, weights=p.nu)

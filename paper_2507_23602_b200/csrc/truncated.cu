@@ -496,9 +496,7 @@ struct FusedAtoms {
   float lo_thr, hi_thr;      // FP32 decision thresholds
   int qa, qb;                // Hilbert positions of the two atoms
   double Sa, Sb;             // phase 1 sums
-  uint32_t tot;              // accepted pairs of both atoms
-  unsigned anyf;             // OR of the pair masks (bits 0/2: atom a, 1/3: atom b)
-  uint32_t ca, cb;           // per-atom candidate counts (debug builds)
+  uint32_t ca, cb;           // accepted pairs per atom
   uint64_t ha, hb;           // candidate hashes (debug)
   double wa, wb;             // phase 2: m_q / S~_q (0 for empty / exact-path atoms)
 };
@@ -653,30 +651,193 @@ __device__ __forceinline__ void fused_masks(float2 d0, float2 d1, float2 nlo, fl
            (static_cast<unsigned>(b2) << 2) | (static_cast<unsigned>(b3) << 3);
 }
 
+// Per-scan constants of the FP32 step.
+struct Step32 {
+  float lo;        // pairs with d2 < lo are in (FP32 decision)
+  float nmid, hw;  // band [lo, hi] <=> |d2 - mid| <= hw (inflated: no misses)
+  float nbig, lobig;  // indicator sat(lo*BIG - d2*BIG) = [d2 < lo] exactly
+  float2 nlo, nhi;
+  float2 nc2;
+};
+
+__device__ __forceinline__ float sat_fma(float a, float b, float c) {
+  float r;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+__device__ __forceinline__ Step32 make_step(float lo_thr, float hi_thr) {
+  Step32 K;
+  K.lo = lo_thr;
+  K.nlo = make_float2(-lo_thr, -lo_thr);
+  K.nhi = make_float2(-hi_thr, -hi_thr);
+  {
+    // [lo, hi] inside [mid - hw, mid + hw] after every FP32 rounding: the
+    // rounding of mid and of d2 - mid is covered by 4 ulp(hi) of slack
+    const double lo = lo_thr, hi = hi_thr;
+    const float mid = static_cast<float>(0.5 * (lo + hi));
+    K.nmid = -mid;
+    K.hw = static_cast<float>(fmax(hi - mid, mid - lo) * (1.0 + 0x1p-20) +
+                              4.0 * fabs(hi) * 0x1p-23) + 1e-30f;
+  }
+  // power of two: lo * BIG and d2 * BIG are exact, so the FMA rounds
+  // BIG (lo - d2) once: >= 2^77 when d2 < lo, <= 0 otherwise
+  const float big = lo_thr > 0.f ? ldexpf(1.f, 100 - ilogbf(lo_thr)) : 0.f;
+  K.nbig = -big;
+  K.lobig = lo_thr * big;
+  K.nc2 = make_float2(0.f, 0.f);
+  return K;
+}
+
+// Band test of a step: some pair with |d2 - mid| <= hw, i.e. possibly in
+// [lo, hi] where the exact fp64 predicate decides (false positives harmless).
+template <bool PAIR>
+__device__ __forceinline__ bool step_in_band(const Step32& K, float2 d0, float2 d1) {
+  float bm = fminf(fabsf(d0.x + K.nmid), fabsf(d0.y + K.nmid));
+  if (PAIR) bm = fminf(bm, fminf(fabsf(d1.x + K.nmid), fabsf(d1.y + K.nmid)));
+  return bm <= K.hw;
+}
+
 // Exact reference predicate for the pairs inside the FP32 error band (rare).
-template <class SM, class AT>
-__device__ __noinline__ unsigned fused_exact(const SM& sm, const FusedArgs& A, const AT& at, int t0,
-                                             int t1, unsigned border, unsigned in) {
+template <class SM>
+__device__ __forceinline__ unsigned fused_exact(const SM& sm, const FusedArgs& A, int qa, int qb,
+                                                int t0, int t1, unsigned border, unsigned in) {
   for (int bit = 0; bit < 4; ++bit) {
     if (!((border >> bit) & 1u)) continue;
     const double4 yg = A.ys[sm.tK[bit < 2 ? t0 : t1]];
-    const double4 x = A.xs[(bit & 1) ? at.qb : at.qa];
+    const double4 x = A.xs[(bit & 1) ? qb : qa];
     if (exact_inside(x.x, x.y, x.z, yg.x, yg.y, yg.z, A.r2)) in |= 1u << bit;
   }
   return in;
 }
 
+// Pair bitmask of a step that has a pair in the FP32 error band (bit 2i:
+// atom a, 2i+1: atom b of item i): FP32 decision outside the band, exact fp64
+// predicate inside.  Out of line to keep the unrolled fast paths compact.
+template <class SM>
+__device__ __noinline__ unsigned slow_mask(const SM& sm, const FusedArgs& A, int qa, int qb,
+                                           const Step32& K, int t0, int t1, float2 d0, float2 d1,
+                                           bool pair) {
+  unsigned in, bd;
+  fused_masks(d0, d1, K.nlo, K.nhi, pair, in, bd);
+  if (bd) in = fused_exact(sm, A, qa, qb, t0, t1, bd, in);
+  return in;
+}
+
+// Step of 2 targets (t0, t1; PAIR = false: t0 only) x atoms (a, b) of the
+// fp64 kernel.  The FP32 pre-test decides clear pairs with 4 FSETP; a step
+// with a pair in the error band (warp-uniform, rare) takes the bitmask path
+// with the exact fp64 predicate (also used in DEBUG builds for the hashes).
+// PHASE 1 accumulates S~ of both atoms and the accepted pair counts (floats,
+// exact per tile); PHASE 2 returns the weighted column values of t0, t1.
 // SAFE: CTA whose exponents may leave [-1020, 1000] (spread chunk or huge
-// psi range): per-atom shift carried in every exponent when R.wide, and the
+// psi range): per-atom shift carried in every exponent when wide, and the
 // exponent split clamped.
+template <int PHASE, bool PAIR, bool SAFE, bool DEBUG>
+__device__ __forceinline__ double2 step64d(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at,
+                                           const Step32& K, bool wide, int t0, int t1, float2 d0,
+                                           float2 d1, float2& cnt) {
+  bool k0a, k0b, k1a = false, k1b = false;
+  bool work;
+  if (DEBUG || __any_sync(0xffffffffu, step_in_band<PAIR>(K, d0, d1))) {
+    const unsigned in = slow_mask(sm, A, at.qa, at.qb, K, t0, t1, d0, d1, PAIR);
+    k0a = in & 1u;
+    k0b = in & 2u;
+    k1a = in & 4u;
+    k1b = in & 8u;
+    if (DEBUG && PHASE == 1) {
+      if (k0a) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
+      if (k1a) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
+      if (k0b) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
+      if (k1b) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
+    }
+    work = __any_sync(0xffffffffu, in != 0u);
+  } else {
+    float m = fminf(d0.x, d0.y);
+    if (PAIR) m = fminf(m, fminf(d1.x, d1.y));
+    work = __any_sync(0xffffffffu, m < K.lo);
+    k0a = d0.x < K.lo;
+    k0b = d0.y < K.lo;
+    if (PAIR) {
+      k1a = d1.x < K.lo;
+      k1b = d1.y < K.lo;
+    }
+  }
+  double2 out = make_double2(0.0, 0.0);
+  if (work) {
+    const double4 y0 = sm.tD[t0];
+    double sa0 = chain3(at.Xa, y0), sb0 = chain3(at.Xb, y0);
+    if (wide) {
+      sa0 -= at.xsqa;
+      sb0 -= at.xsqb;
+    }
+    if (PHASE == 1) {
+      cnt = __fadd2_rn(cnt, make_float2(k0a ? 1.f : 0.f, k0b ? 1.f : 0.f));
+      at.Sa = exp2_acc_masked<SAFE>(sa0, at.Sa, sm.tbl, k0a);
+      at.Sb = exp2_acc_masked<SAFE>(sb0, at.Sb, sm.tbl, k0b);
+    } else {
+      out.x = exp2_pair_weighted<SAFE>(sa0, sb0, at.wa, at.wb, sm.tbl, k0a, k0b);
+    }
+    if (PAIR) {
+      const double4 y1 = sm.tD[t1];
+      double sa1 = chain3(at.Xa, y1), sb1 = chain3(at.Xb, y1);
+      if (wide) {
+        sa1 -= at.xsqa;
+        sb1 -= at.xsqb;
+      }
+      if (PHASE == 1) {
+        cnt = __fadd2_rn(cnt, make_float2(k1a ? 1.f : 0.f, k1b ? 1.f : 0.f));
+        at.Sa = exp2_acc_masked<SAFE>(sa1, at.Sa, sm.tbl, k1a);
+        at.Sb = exp2_acc_masked<SAFE>(sb1, at.Sb, sm.tbl, k1b);
+      } else {
+        out.y = exp2_pair_weighted<SAFE>(sa1, sb1, at.wa, at.wb, sm.tbl, k1a, k1b);
+      }
+    }
+  }
+  return out;
+}
+
+template <int PHASE, bool PAIR, bool SAFE, bool DEBUG>
+__device__ __forceinline__ double2 step64(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at,
+                                          const Step32& K, bool wide, int t0, int t1,
+                                          float2& cnt) {
+  const float2 d0 = fused_d2(sm, at, t0);
+  const float2 d1 = PAIR ? fused_d2(sm, at, t1) : d0;
+  return step64d<PHASE, PAIR, SAFE, DEBUG>(sm, A, at, K, wide, t0, t1, d0, d1, cnt);
+}
+
+template <bool SAFE, bool DEBUG>
+__device__ __forceinline__ void batch64(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at,
+                                        const Step32& K, bool wide, const unsigned char* list,
+                                        int b0, int nsel, double* col) {
+  const int lane = threadIdx.x & 31;
+  double v[16];
+  float2 dummy = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int i = b0 + 2 * p;
+    double2 val = make_double2(0.0, 0.0);
+    if (i < nsel) {
+      // a lone last item pairs with itself; its second column is dropped
+      const int t0 = list[i];
+      const int t1 = i + 1 < nsel ? list[i + 1] : t0;
+      val = step64<2, true, SAFE, DEBUG>(sm, A, at, K, wide, t0, t1, dummy);
+    }
+    v[2 * p] = val.x;
+    v[2 * p + 1] = i + 1 < nsel ? val.y : 0.0;
+  }
+  const double tot = butterfly16(v);
+  const int item = b0 + (lane >> 1);
+  if (!(lane & 1) && item < nsel) col[list[item]] = tot;
+}
+
 template <int PHASE, bool SAFE, bool DEBUG>
 __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb, float cull_thr,
                            double B, FusedAtoms& at) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* const list = sm.wlist[warp];
   const bool wide = SAFE && sm.R.wide;
-  const float2 nlo = make_float2(-at.lo_thr, -at.lo_thr);
-  const float2 nhi = make_float2(-at.hi_thr, -at.hi_thr);
+  const Step32 K = make_step(at.lo_thr, at.hi_thr);
   const int ny = sm.R.c_hi[1] - sm.R.c_lo[1] + 1;
   const int nrows = ny * (sm.R.c_hi[2] - sm.R.c_lo[2] + 1);
   for (int rb = 0; rb < nrows; rb += kT) {
@@ -696,88 +857,32 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
       const int nsel = fused_cull(sm, cnt, wb, cull_thr, list);
       if (PHASE == 1) {
         // software-pipelined: the next step's list entries and distances are
-        // loaded before this step's exponentials (hides LDS latency).
-        int t0 = nsel > 0 ? list[0] : 0;
-        int t1 = nsel > 1 ? list[1] : t0;
-        float2 d0 = fused_d2(sm, at, t0), d1 = fused_d2(sm, at, t1);
-        for (int i = 0; i < nsel; i += 2) {
-          const bool v1 = i + 1 < nsel;
-          unsigned in, bd;
-          fused_masks(d0, d1, nlo, nhi, v1, in, bd);
-          const int c0 = t0, c1 = t1;
-          if (i + 2 < nsel) {
-            t0 = list[i + 2];
-            t1 = (i + 3 < nsel) ? list[i + 3] : t0;
-            d0 = fused_d2(sm, at, t0);
-            d1 = fused_d2(sm, at, t1);
-          }
-          if (__any_sync(0xffffffffu, bd != 0u)) {
-            if (bd) in = fused_exact(sm, A, at, c0, c1, bd, in);
-          }
-          if (__any_sync(0xffffffffu, in != 0u)) {
-            const double4 y0 = sm.tD[c0];
-            const double4 y1 = sm.tD[c1];
-            double sa0 = chain3(at.Xa, y0), sb0 = chain3(at.Xb, y0);
-            double sa1 = chain3(at.Xa, y1), sb1 = chain3(at.Xb, y1);
-            if (wide) {
-              sa0 -= at.xsqa; sa1 -= at.xsqa;
-              sb0 -= at.xsqb; sb1 -= at.xsqb;
+        // loaded before this step's exponentials (hides LDS latency)
+        float2 cn = make_float2(0.f, 0.f);
+        int i = 0;
+        if (nsel >= 2) {
+          int t0 = list[0], t1 = list[1];
+          float2 d0 = fused_d2(sm, at, t0), d1 = fused_d2(sm, at, t1);
+          for (; i + 1 < nsel; i += 2) {
+            const int c0 = t0, c1 = t1;
+            const float2 e0 = d0, e1 = d1;
+            if (i + 3 < nsel) {
+              t0 = list[i + 2];
+              t1 = list[i + 3];
+              d0 = fused_d2(sm, at, t0);
+              d1 = fused_d2(sm, at, t1);
             }
-            at.Sa = exp2_acc_masked<SAFE>(sa0, at.Sa, sm.tbl, in & 1u);
-            at.Sb = exp2_acc_masked<SAFE>(sb0, at.Sb, sm.tbl, in & 2u);
-            at.Sa = exp2_acc_masked<SAFE>(sa1, at.Sa, sm.tbl, in & 4u);
-            at.Sb = exp2_acc_masked<SAFE>(sb1, at.Sb, sm.tbl, in & 8u);
-            at.tot += __popc(in);
-            at.anyf |= in;
-            if (DEBUG) {
-              at.ca += __popc(in & 5u);
-              at.cb += __popc(in & 10u);
-              if (in & 1u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[c0]));
-              if (in & 4u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[c1]));
-              if (in & 2u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[c0]));
-              if (in & 8u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[c1]));
-            }
+            step64d<1, true, SAFE, DEBUG>(sm, A, at, K, wide, c0, c1, e0, e1, cn);
           }
         }
+        if (i < nsel) step64<1, false, SAFE, DEBUG>(sm, A, at, K, wide, list[i], list[i], cn);
+        at.ca += static_cast<uint32_t>(cn.x);
+        at.cb += static_cast<uint32_t>(cn.y);
       } else {
         double* const col = sm.colW[warp];
         for (int s = lane; s < cnt; s += 32) col[s] = 0.0;
         __syncwarp();
-        for (int b0 = 0; b0 < nsel; b0 += 16) {
-          double v[16];
-#pragma unroll
-          for (int p = 0; p < 8; ++p) {
-            const int i = b0 + 2 * p;
-            const bool v0 = i < nsel, v1 = i + 1 < nsel;
-            const int t0 = v0 ? list[i] : list[0];
-            const int t1 = v1 ? list[i + 1] : t0;
-            unsigned in, bd;
-            fused_masks(fused_d2(sm, at, t0), fused_d2(sm, at, t1), nlo, nhi, v1, in, bd);
-            if (!v0) in = bd = 0u;
-            if (__any_sync(0xffffffffu, bd != 0u)) {
-              if (bd) in = fused_exact(sm, A, at, t0, t1, bd, in);
-            }
-            v[2 * p] = 0.0;
-            v[2 * p + 1] = 0.0;
-            if (__any_sync(0xffffffffu, in != 0u)) {
-              const double4 y0 = sm.tD[t0];
-              const double4 y1 = sm.tD[t1];
-              double sa0 = chain3(at.Xa, y0), sb0 = chain3(at.Xb, y0);
-              double sa1 = chain3(at.Xa, y1), sb1 = chain3(at.Xb, y1);
-              if (wide) {
-                sa0 -= at.xsqa; sa1 -= at.xsqa;
-                sb0 -= at.xsqb; sb1 -= at.xsqb;
-              }
-              v[2 * p] = exp2_pair_weighted<SAFE>(sa0, sb0, at.wa, at.wb, sm.tbl, in & 1u, in & 2u);
-              v[2 * p + 1] = exp2_pair_weighted<SAFE>(sa1, sb1, at.wa, at.wb, sm.tbl, in & 4u, in & 8u);
-            }
-          }
-          const double tot = butterfly16(v);
-          const int item = b0 + (lane >> 1);
-          if (!(lane & 1) && item < nsel) col[list[item]] = tot;
-        }
-      }
-      if (PHASE == 2) {
+        for (int b0 = 0; b0 < nsel; b0 += 16) batch64<SAFE, DEBUG>(sm, A, at, K, wide, list, b0, nsel, col);
         __syncthreads();
         for (int s = threadIdx.x; s < cnt; s += kT) {
           const double c = ((sm.colW[0][s] + sm.colW[1][s]) + sm.colW[2][s]) + sm.colW[3][s];
@@ -909,8 +1014,6 @@ trunc_fused(FusedArgs A) {
   at.lo_thr = sm.R.lo_thr;
   at.hi_thr = sm.R.hi_thr;
   at.Sa = at.Sb = 0.0;
-  at.tot = 0;
-  at.anyf = 0;
   at.ca = at.cb = 0;
   at.ha = at.hb = 0;
   WarpBox wb;
@@ -933,10 +1036,10 @@ trunc_fused(FusedArgs A) {
     fused_scan<1, false, DEBUG>(sm, A, wb, cull_thr, B, at);
 
   // pair counter: the lane's accepted pairs are booked on atom a
-  fused_finalize<DEBUG>(A, B, wide, va, (at.anyf & 5u) != 0u, static_cast<double>(at.tot), at.ca,
+  fused_finalize<DEBUG>(A, B, wide, va, at.ca != 0u, static_cast<double>(at.ca + at.cb), at.ca,
                         at.Sa, at.xsqa, at.qa, at.ha, at.wa);
-  fused_finalize<DEBUG>(A, B, wide, vb, (at.anyf & 10u) != 0u, 0.0, at.cb, at.Sb, at.xsqb, at.qb,
-                        at.hb, at.wb);
+  fused_finalize<DEBUG>(A, B, wide, vb, at.cb != 0u, 0.0, at.cb, at.Sb, at.xsqb, at.qb, at.hb,
+                        at.wb);
 
   if (safe)
     fused_scan<2, true, DEBUG>(sm, A, wb, cull_thr, B, at);
@@ -1076,21 +1179,6 @@ __device__ __forceinline__ float2 fused_d2w(const Fused32Smem& sm, const Atoms32
   return __ffma2_rn(dz, dz, d2);
 }
 
-// Per-scan constants of the FP32 step.
-struct Step32 {
-  float lo;        // pairs with d2 < lo are in (FP32 decision)
-  float nmid, hw;  // band [lo, hi] <=> |d2 - mid| <= hw (inflated: no misses)
-  float nbig, lobig;  // indicator sat(lo*BIG - d2*BIG) = [d2 < lo] exactly
-  float2 nlo, nhi;
-  float2 nc2;
-};
-
-__device__ __forceinline__ float sat_fma(float a, float b, float c) {
-  float r;
-  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
-
 // Step of 2 targets (t0, t1; PAIR = false: t0 only) x atoms (a, b).
 // PHASE 1 accumulates the masked exponentials into acc and the accepted
 // pair counts into cnt (floats, exact per tile); PHASE 2 returns the
@@ -1104,14 +1192,10 @@ __device__ __forceinline__ float2 step32(const Fused32Smem& sm, const FusedArgs&
   float w0, w1 = 0.f;
   const float2 d0 = fused_d2w(sm, at, t0, w0);
   const float2 d1 = PAIR ? fused_d2w(sm, at, t1, w1) : d0;
-  float bm = fminf(fabsf(d0.x + K.nmid), fabsf(d0.y + K.nmid));
-  if (PAIR) bm = fminf(bm, fminf(fabsf(d1.x + K.nmid), fabsf(d1.y + K.nmid)));
   float2 i0, i1 = make_float2(0.f, 0.f);
   bool work;
-  if (DEBUG || __any_sync(0xffffffffu, bm <= K.hw)) {
-    unsigned in, bd;
-    fused_masks(d0, d1, K.nlo, K.nhi, PAIR, in, bd);
-    if (bd) in = fused_exact(sm, A, at, t0, t1, bd, in);
+  if (DEBUG || __any_sync(0xffffffffu, step_in_band<PAIR>(K, d0, d1))) {
+    const unsigned in = slow_mask(sm, A, at.qa, at.qb, K, t0, t1, d0, d1, PAIR);
     i0 = make_float2((in & 1u) ? 1.f : 0.f, (in & 2u) ? 1.f : 0.f);
     if (PAIR) i1 = make_float2((in & 4u) ? 1.f : 0.f, (in & 8u) ? 1.f : 0.f);
     if (DEBUG && PHASE == 1) {
@@ -1182,24 +1266,7 @@ __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox&
                              float cull_thr, double& Bc, Atoms32& at) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* const list = sm.wlist[warp];
-  Step32 K;
-  K.lo = at.lo_thr;
-  K.nlo = make_float2(-at.lo_thr, -at.lo_thr);
-  K.nhi = make_float2(-at.hi_thr, -at.hi_thr);
-  {
-    // [lo, hi] inside [mid - hw, mid + hw] after every FP32 rounding: the
-    // rounding of mid and of d2 - mid is covered by 4 ulp(hi) of slack
-    const double lo = at.lo_thr, hi = at.hi_thr;
-    const float mid = static_cast<float>(0.5 * (lo + hi));
-    K.nmid = -mid;
-    K.hw = static_cast<float>(fmax(hi - mid, mid - lo) * (1.0 + 0x1p-20) +
-                              4.0 * fabs(hi) * 0x1p-23) + 1e-30f;
-  }
-  // power of two: lo * BIG and d2 * BIG are exact, so the FMA rounds
-  // BIG (lo - d2) once: >= 2^77 when d2 < lo, <= 0 otherwise
-  const float big = at.lo_thr > 0.f ? ldexpf(1.f, 100 - ilogbf(at.lo_thr)) : 0.f;
-  K.nbig = -big;
-  K.lobig = at.lo_thr * big;
+  Step32 K = make_step(at.lo_thr, at.hi_thr);
   const float nc2f = static_cast<float>(-A.c2);
   K.nc2 = make_float2(nc2f, nc2f);
   const int ny = sm.R.c_hi[1] - sm.R.c_lo[1] + 1;

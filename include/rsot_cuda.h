@@ -158,6 +158,31 @@ int rsot_cuda_softmax_refine(rsot_cuda_ctx* ctx, rsot_cuda_targets* coarse,
                              size_t n_fine, rsot_cuda_atoms* atoms, double eps,
                              double cutoff, double* psi_out);
 
+/* ---- PlanView (proj/src/plan.cpp) ----------------------------------------
+ * The plan induced by a potential, over this handle's atoms.
+ * rsot_cuda_plan_candidates: the PlanView ctor's candidate sets (plan.cpp:
+ *   37-46): idx_out[offsets[q] .. offsets[q+1]) receives atom q's ascending
+ *   candidate list (all targets for cutoff = +inf; the ball query of radius
+ *   sqrt(2 cutoff), or the nearest target when it is empty).  offsets[nq+1]
+ *   is the prefix sum of the per-atom counts (rsot_cuda_eval_debug's
+ *   cand_count for the same cutoff).
+ * rsot_cuda_plan_moments: with log_s = the ctor's log_S_q (rsot_cuda_eval_debug
+ *   log_s) and the candidate lists (offsets == NULL: every target), the
+ *   plan-density reductions of plan.cpp: target_marginals (:85-91,
+ *   marginal_out[n]), the unnormalised first moments sum_q p m_q x_q of
+ *   all_conditional_barycenters (:123-140, moment_out[3n]), barycentric_map
+ *   (:142-156, map_out[3nq]) and modal_map's target index (:158-182,
+ *   modal_out[nq], lowest index on ties).  Outputs may be NULL.  Sums are
+ *   order independent (fixed point), so results are bitwise reproducible. */
+int rsot_cuda_plan_candidates(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
+                              rsot_cuda_targets* targets, double cutoff,
+                              const uint64_t* offsets, uint64_t* idx_out);
+int rsot_cuda_plan_moments(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
+                           rsot_cuda_targets* targets, const double* psi, double eps,
+                           const double* log_s, const uint64_t* offsets,
+                           const uint64_t* idx, double* marginal_out, double* moment_out,
+                           double* map_out, uint64_t* modal_out);
+
 /* ---- precision ------------------------------------------------------------
  * RSOT_CUDA_PRECISION_FP64 (default): every operation in fp64, within 1e-10
  * relative of the reference.  RSOT_CUDA_PRECISION_FP32: truncated

@@ -65,6 +65,9 @@ class COracle:
         L.oracle_softmax_refine.restype = c_int
         L.oracle_softmax_refine.argtypes = [c_size_t, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p,
                                             c_size_t, c_void_p, c_void_p, c_double, c_double, c_void_p]
+        L.oracle_plan_view.restype = c_int
+        L.oracle_plan_view.argtypes = [c_size_t, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p, c_void_p,
+                                       c_double, c_double] + [c_void_p] * 8
         L.oracle_ball_radius.restype = c_double
         L.oracle_ball_radius.argtypes = [c_double]
         L.oracle_cutoff_pointwise.restype = c_double
@@ -112,6 +115,27 @@ class COracle:
                                           _p(am), float(eps), float(cutoff), _p(out))
         if rc != 0:
             raise ValueError(self.L.oracle_last_error().decode())
+        return out
+
+    def plan_view(self, atoms, masses, targets, nu, psi, eps, cutoff=math.inf):
+        """PlanView (plan.cpp): dict of log_s, count, marginal, moment (n,3),
+        bary (n,3), starved (first starved index or -1), map (nq,3), modal."""
+        a, t = _pts(atoms), _pts(targets)
+        m = np.ascontiguousarray(masses, dtype=np.float64)
+        nu = np.ascontiguousarray(nu, dtype=np.float64)
+        psi = np.ascontiguousarray(psi, dtype=np.float64)
+        nq, n = len(a), len(t)
+        out = dict(log_s=np.zeros(nq), count=np.zeros(nq, dtype=np.uint64), marginal=np.zeros(n),
+                   moment=np.zeros((n, 3)), bary=np.zeros((n, 3)), map=np.zeros((nq, 3)),
+                   modal=np.zeros(nq, dtype=np.uint64))
+        st = ctypes.c_int64(-1)
+        rc = self.L.oracle_plan_view(nq, _p(a), _p(m), n, _p(t), _p(nu), _p(psi), float(eps), float(cutoff),
+                                     _p(out["log_s"]), _p(out["count"]), _p(out["marginal"]),
+                                     _p(out["moment"]), _p(out["bary"]), _p(out["map"]), _p(out["modal"]),
+                                     ctypes.byref(st))
+        if rc != 0:
+            raise ValueError(self.L.oracle_last_error().decode())
+        out["starved"] = int(st.value)
         return out
 
     def hash_term(self, j: int) -> int:
@@ -168,6 +192,8 @@ class RefLib:
                                          c_void_p]
         L.ref_covering_cost.restype = c_int
         L.ref_covering_cost.argtypes = [c_void_p, POINTER(c_double)]
+        L.ref_plan_view.restype = c_int
+        L.ref_plan_view.argtypes = [c_void_p, c_void_p, c_double, c_double] + [c_void_p] * 6
         self.L = L
 
     def problem(self, dim, atoms, masses, targets, nu):
@@ -206,6 +232,20 @@ class RefProblem:
                                            int(workers), _p(out))
         if rc != 0:
             raise ValueError(self.lib.L.ref_last_error().decode())
+        return out
+
+    def plan_view(self, psi, eps, cutoff=math.inf):
+        psi = np.ascontiguousarray(psi, dtype=np.float64)
+        nq, n = len(self.atoms), len(self.targets)
+        out = dict(count=np.zeros(nq, dtype=np.uint64), marginal=np.zeros(n), bary=np.zeros((n, 3)),
+                   map=np.zeros((nq, 3)), modal=np.zeros(nq, dtype=np.uint64))
+        st = ctypes.c_int64(-1)
+        rc = self.lib.L.ref_plan_view(self.h, _p(psi), float(eps), float(cutoff), _p(out["count"]),
+                                      _p(out["marginal"]), _p(out["bary"]), ctypes.byref(st), _p(out["map"]),
+                                      _p(out["modal"]))
+        if rc != 0:
+            raise ValueError(self.lib.L.ref_last_error().decode())
+        out["starved"] = int(st.value)
         return out
 
     def covering_cost(self):

@@ -13,6 +13,7 @@
 
 #include "rsot/evaluate.hpp"
 #include "rsot/measures.hpp"
+#include "rsot/plan.hpp"
 #include "rsot/solve.hpp"
 #include "rsot/spatial_index.hpp"
 
@@ -129,6 +130,51 @@ int ref_softmax_refine(void* prob, const double* coarse_psi, const double* fine_
         rsot::softmax_refine(p->target, cpsi, fine, p->atoms, eps,
                              rsot::CostKind::SqEuclidean, cutoff, workers);
     std::memcpy(psi_out, out.data(), sizeof(double) * n_fine);
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return -1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -2;
+  }
+}
+
+// rsot::PlanView (plan.cpp) on this problem: candidate counts, target
+// marginals, conditional barycentres (starved index or -1), barycentric map
+// and modal target indices.  Outputs may be NULL.
+int ref_plan_view(void* prob, const double* psi, double eps, double cutoff, uint64_t* count_out,
+                  double* marginal_out, double* bary_out, int64_t* starved_out,
+                  double* map_out, uint64_t* modal_out) {
+  auto* p = static_cast<RefProblem*>(prob);
+  try {
+    rsot::DualPotential pot{std::vector<double>(psi, psi + p->target.size()), rsot::Gauge::Raw};
+    const rsot::PlanView plan(p->atoms, p->target, pot, eps, rsot::CostKind::SqEuclidean, cutoff, 1);
+    if (count_out)
+      for (size_t q = 0; q < p->atoms.size(); ++q) count_out[q] = plan.candidates(q).size();
+    if (marginal_out) {
+      const std::vector<double> m = plan.target_marginals();
+      std::memcpy(marginal_out, m.data(), sizeof(double) * m.size());
+    }
+    if (bary_out) {
+      *starved_out = -1;
+      try {
+        const rsot::PointList b = plan.all_conditional_barycenters();
+        std::memcpy(bary_out, b.data(), sizeof(double) * 3 * b.size());
+      } catch (const std::runtime_error& e) {
+        const std::string msg = e.what();
+        const auto k = msg.rfind(' ');
+        *starved_out = std::stoll(msg.substr(k + 1));
+      }
+    }
+    if (map_out) {
+      const rsot::MapSample m = rsot::barycentric_map(plan);
+      std::memcpy(map_out, m.mapped.data(), sizeof(double) * 3 * m.mapped.size());
+    }
+    if (modal_out) {
+      const rsot::MapSample m = rsot::modal_map(plan);
+      for (size_t q = 0; q < m.target_index.size(); ++q) modal_out[q] = m.target_index[q];
+    }
     return 0;
   } catch (const std::invalid_argument& e) {
     g_err = e.what();

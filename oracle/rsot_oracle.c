@@ -567,3 +567,107 @@ double oracle_cutoff_bootstrap(double covering, double psi_range,
   const double c = covering + psi_range + eps * log(eps / (nu_min * tau));
   return dmax(c, covering);
 }
+
+/* ---- PlanView (proj/src/plan.cpp) ---------------------------------------
+ * ctor (:12-59): candidate sets (all targets, or the ball query with the
+ * nearest-target fallback) and log_S_q; target_marginals (:85-91);
+ * all_conditional_barycenters (:123-140, unnormalised first moments and
+ * tilde returned, plus the normalised barycentres); barycentric_map
+ * (:142-156); modal_map (:158-182).  SqEuclidean, single worker. */
+int oracle_plan_view(size_t nq, const double* ax, const double* am, size_t n,
+                     const double* ty, const double* nu, const double* psi,
+                     double eps, double cutoff, double* log_s_out,
+                     uint64_t* count_out, double* marginal_out,
+                     double* moment_out, double* bary_out, double* map_out,
+                     uint64_t* modal_out, int64_t* starved_out) {
+  for (size_t j = 0; j < n; ++j)
+    if (!isfinite(psi[j])) {
+      g_last_error = "potential has non-finite entries";
+      return ORACLE_INVALID_ARGUMENT;
+    }
+  const int truncated = isfinite(cutoff);
+  const double radius = oracle_ball_radius(cutoff);
+  oracle_grid* grid = oracle_grid_create(ty, n); /* plan.cpp:31 */
+  if (!grid) return ORACLE_INVALID_ARGUMENT;
+  double* log_nu = (double*)malloc(sizeof(double) * (n ? n : 1));
+  for (size_t j = 0; j < n; ++j) log_nu[j] = log(nu[j]);
+  uint64_t* cand = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));
+  size_t ccap = n ? n : 1;
+  double* expo = (double*)malloc(sizeof(double) * (n ? n : 1));
+  if (marginal_out)
+    for (size_t j = 0; j < n; ++j) marginal_out[j] = 0.0;
+  if (moment_out)
+    for (size_t j = 0; j < 3 * n; ++j) moment_out[j] = 0.0;
+  for (size_t q = 0; q < nq; ++q) {
+    const double* x = ax + 3 * q;
+    size_t nc;
+    if (!truncated) {
+      nc = n;
+      for (size_t j = 0; j < n; ++j) cand[j] = j;
+    } else {
+      nc = ball_query_into(grid, x, radius, &cand, &ccap);
+    }
+    if (nc == 0) {
+      cand[0] = oracle_grid_nearest(grid, x);
+      nc = 1;
+    }
+    double emax = -INFINITY; /* :47-57 */
+    for (size_t i = 0; i < nc; ++i) {
+      const uint64_t j = cand[i];
+      expo[i] = (psi[j] - 0.5 * sqdist(x, ty + 3 * j)) / eps + log_nu[j];
+      emax = (emax < expo[i]) ? expo[i] : emax;
+    }
+    double sum = 0.0;
+    for (size_t i = 0; i < nc; ++i) sum += exp(expo[i] - emax);
+    const double lS = emax + log(sum);
+    if (log_s_out) log_s_out[q] = lS;
+    if (count_out) count_out[q] = nc;
+    /* plan_density (:70-83) recomputes e with std::log(weights[j]) */
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    uint64_t best = n;
+    double best_score = -INFINITY;
+    for (size_t i = 0; i < nc; ++i) {
+      const uint64_t j = cand[i];
+      const double c = 0.5 * sqdist(x, ty + 3 * j);
+      const double e = (psi[j] - c) / eps + log(nu[j]);
+      const double p = exp(e - lS);
+      const double w = p * am[q];
+      if (marginal_out) marginal_out[j] += w;
+      if (moment_out) {
+        moment_out[3 * j] += w * x[0];
+        moment_out[3 * j + 1] += w * x[1];
+        moment_out[3 * j + 2] += w * x[2];
+      }
+      t0 += p * ty[3 * j];
+      t1 += p * ty[3 * j + 1];
+      t2 += p * ty[3 * j + 2];
+      const double score = psi[j] - c + eps * log(nu[j]); /* :172-175 */
+      if (score > best_score) {
+        best_score = score;
+        best = j;
+      }
+    }
+    if (map_out) {
+      map_out[3 * q] = t0;
+      map_out[3 * q + 1] = t1;
+      map_out[3 * q + 2] = t2;
+    }
+    if (modal_out) modal_out[q] = best;
+  }
+  if (starved_out) *starved_out = -1;
+  if (bary_out && marginal_out && moment_out)
+    for (size_t j = 0; j < n; ++j) { /* :134-139 */
+      if (marginal_out[j] < 1e-30) {
+        if (starved_out && *starved_out < 0) *starved_out = (int64_t)j;
+        bary_out[3 * j] = bary_out[3 * j + 1] = bary_out[3 * j + 2] = 0.0;
+        continue;
+      }
+      const double inv = 1.0 / marginal_out[j];
+      for (int d = 0; d < 3; ++d) bary_out[3 * j + d] = inv * moment_out[3 * j + d];
+    }
+  free(log_nu);
+  free(cand);
+  free(expo);
+  oracle_grid_destroy(grid);
+  return ORACLE_OK;
+}

@@ -92,6 +92,19 @@ int oracle_evaluate_dual(size_t nq, const double* atom_xyz,
                          oracle_scalars* out, uint32_t* cand_count,
                          uint64_t* cand_hash, double* log_s);
 
+/* PlanView (proj/src/plan.cpp), SqEuclidean: per-atom log_S (ctor
+ * :47-57) and candidate count; target_marginals (:85-91); unnormalised first
+ * moments sum_q p m_q x_q and normalised conditional barycentres (:123-140;
+ * *starved_out = first index with marginal < 1e-30, else -1);
+ * barycentric_map (:142-156) and modal_map target indices (:158-182).
+ * Every output may be NULL (bary needs marginal and moment). */
+int oracle_plan_view(size_t nq, const double* atom_xyz, const double* atom_mass,
+                     size_t n, const double* target_xyz, const double* target_nu,
+                     const double* psi, double eps, double cutoff, double* log_s_out,
+                     uint64_t* count_out, double* marginal_out, double* moment_out,
+                     double* bary_out, double* map_out, uint64_t* modal_out,
+                     int64_t* starved_out);
+
 /* rsot::softmax_refine (proj/src/solve.cpp:62-142), SqEuclidean, single
  * worker: psi_out[n_fine] from the coarse potential.  Returns
  * ORACLE_INVALID_ARGUMENT on non-finite input or output (require_finite). */

@@ -12,6 +12,11 @@ from .rsot import (  # noqa: F401
     DualPotential,
     EvalResult,
     Gauge,
+    MapKind,
+    MapSample,
+    PlanView,
+    barycentric_map,
+    modal_map,
     SolverConfig,
     SourceAtoms,
     SpatialIndex,

@@ -616,6 +616,47 @@ int rsot_cuda_softmax_refine(rsot_cuda_ctx* c, rsot_cuda_targets* coarse,
   return rc ? fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error) : RSOT_CUDA_OK;
 }
 
+int rsot_cuda_plan_candidates(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
+                              double cutoff, const uint64_t* offsets, uint64_t* idx_out) {
+  int rc = check_ready(c, a, t);
+  if (rc) return rc;
+  if (!offsets || (a->nq && offsets[a->nq] && !idx_out))
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  if (std::isnan(cutoff)) return fail(RSOT_CUDA_INVALID_ARGUMENT, "cutoff is NaN");
+  if (!std::isfinite(cutoff)) {  // dense: every target, ascending (plan.cpp:40-42)
+    for (size_t q = 0; q < a->nq; ++q) {
+      if (offsets[q + 1] - offsets[q] != t->n)
+        return fail(RSOT_CUDA_INVALID_ARGUMENT, "offsets do not match the dense candidate count");
+      for (size_t j = 0; j < t->n; ++j) idx_out[offsets[q] + j] = j;
+    }
+    return RSOT_CUDA_OK;
+  }
+  rc = run_plan_candidates(c->trunc, DeviceAtoms{a->x, static_cast<int>(a->nq)}, make_dt(t),
+                           t->cells, cutoff, offsets, idx_out, c->stream, g_last_error);
+  return rc ? fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error) : RSOT_CUDA_OK;
+}
+
+int rsot_cuda_plan_moments(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
+                           const double* psi, double eps, const double* log_s,
+                           const uint64_t* offsets, const uint64_t* idx, double* marginal_out,
+                           double* moment_out, double* map_out, uint64_t* modal_out) {
+  int rc = check_ready(c, a, t);
+  if (rc) return rc;
+  if (!psi || (a->nq && !log_s) || (offsets && offsets[a->nq] && !idx))
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  if (!(eps > 0.0)) return fail(RSOT_CUDA_INVALID_ARGUMENT, "epsilon must be > 0");
+  for (size_t j = 0; j < t->n; ++j)
+    if (!std::isfinite(psi[j]))
+      return fail(RSOT_CUDA_INVALID_ARGUMENT, "potential has non-finite entries");
+  if (offsets && idx)
+    for (uint64_t k = 0; k < offsets[a->nq]; ++k)
+      if (idx[k] >= t->n) return fail(RSOT_CUDA_INVALID_ARGUMENT, "candidate index out of range");
+  rc = run_plan_moments(DeviceAtoms{a->x, static_cast<int>(a->nq)}, make_dt(t), psi, eps, log_s,
+                        offsets, idx, a->cells.bbox_lo, marginal_out, moment_out, map_out,
+                        modal_out, c->stream, g_last_error);
+  return rc ? fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error) : RSOT_CUDA_OK;
+}
+
 int rsot_cuda_ctx_set_precision(rsot_cuda_ctx* c, int precision) {
   if (!c) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null context");
   if (precision != RSOT_CUDA_PRECISION_FP64 && precision != RSOT_CUDA_PRECISION_FP32)

@@ -630,10 +630,6 @@ __device__ __forceinline__ float2 fused_d2(const SM& sm, const AT& at, int t) {
   return __ffma2_rn(dz, dz, d2);
 }
 
-__device__ __forceinline__ unsigned sign4(float2 u0, float2 u1) {
-  return (__float_as_uint(u0.x) >> 31) | ((__float_as_uint(u0.y) >> 31) << 1) |
-         ((__float_as_uint(u1.x) >> 31) << 2) | ((__float_as_uint(u1.y) >> 31) << 3);
-}
 
 // 4-bit pair masks for items (t0, t1) x atoms (a, b): bit 2i = atom a,
 // bit 2i+1 = atom b.  in: d2 < lo (sign of d2 - lo is exact); border:
@@ -1591,6 +1587,146 @@ GridDesc plan_grid(const double blo[3], const double bhi[3], int n, double r) {
   return g;
 }
 
+// ---------------------------------------------------------------------------
+// PlanView (proj/src/plan.cpp) on the GPU: explicit candidate lists (the
+// ctor's ball query + nearest fallback, ascending per atom) and the
+// plan-density reductions over them (target marginals, first moments,
+// barycentric and modal maps).
+
+// Warp per atom: candidate indices into idx[off[q], off[q+1]) (unordered;
+// sorted afterwards), the nearest target when the ball is empty.
+__global__ void plan_fill_kernel(const double4* __restrict__ xs, int nq,
+                                 const double4* __restrict__ ys, const int* __restrict__ tperm,
+                                 const int* __restrict__ cell_start, GridDev g, double r2,
+                                 double r_scan, int scan, const unsigned long long* __restrict__ off,
+                                 unsigned long long* __restrict__ idx, int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int q = warp; q < nq; q += nwarps) {
+    const double4 x = xs[q];
+    const unsigned long long base = off[q];
+    unsigned long long pos = 0;
+    if (scan) {
+      const double v[3] = {x.x, x.y, x.z};
+      int c_lo[3], c_hi[3];
+      for (int d = 0; d < 3; ++d) {
+        c_lo[d] = cell_of(g, d, v[d] - r_scan);
+        c_hi[d] = cell_of(g, d, v[d] + r_scan);
+      }
+      for (int cz = c_lo[2]; cz <= c_hi[2]; ++cz)
+        for (int cy = c_lo[1]; cy <= c_hi[1]; ++cy) {
+          const long long row = (static_cast<long long>(cz) * g.dims[1] + cy) * g.dims[0];
+          const int b = cell_start[row + c_lo[0]], e = cell_start[row + c_hi[0] + 1];
+          for (int k0 = b; k0 < e; k0 += 32) {
+            const int k = k0 + lane;
+            bool in = false;
+            if (k < e) {
+              const double4 y = ys[k];
+              in = exact_inside(x.x, x.y, x.z, y.x, y.y, y.z, r2);
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, in);
+            if (in) idx[base + pos + __popc(m & lt)] = static_cast<unsigned long long>(tperm[k]);
+            pos += __popc(m);
+          }
+        }
+    }
+    if (pos == 0) {
+      double bd;
+      int bj, bk;
+      warp_nearest(g, ys, tperm, cell_start, x.x, x.y, x.z, bd, bj, bk);
+      if (lane == 0) idx[base] = static_cast<unsigned long long>(bj);
+      pos = 1;
+    }
+    if (lane == 0 && pos != off[q + 1] - base) atomicExch(bad, 1);
+  }
+}
+
+// Warp per atom over its candidates (all targets when off == nullptr):
+// p = exp(e - log_S_q) exactly as plan_density (plan.cpp:70-83); target
+// mass and first moments into 192-bit fixed point (moments of x - lo, so
+// every term is non-negative; order independent), barycentric image and
+// modal argmax (lowest index on ties) per atom.
+__global__ void plan_moments_kernel(const double4* __restrict__ xs, int nq,
+                                    const double4* __restrict__ ys, int n,
+                                    const double* __restrict__ psi, double eps,
+                                    const double* __restrict__ log_s,
+                                    const unsigned long long* __restrict__ off,
+                                    const unsigned long long* __restrict__ idx, double lo0,
+                                    double lo1, double lo2, unsigned long long* __restrict__ acc,
+                                    double* __restrict__ map, unsigned long long* __restrict__ modal) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int q = warp; q < nq; q += nwarps) {
+    const double4 x = xs[q];
+    const double L = log_s[q];
+    const unsigned long long b = off ? off[q] : 0ull;
+    const unsigned long long e = off ? off[q + 1] : static_cast<unsigned long long>(n);
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    double best = -INFINITY;
+    unsigned long long bj = ~0ull;
+    for (unsigned long long k = b + lane; k < e; k += 32) {
+      const unsigned long long j = off ? idx[k] : k;
+      const double4 y = ys[j];
+      const double c = __dmul_rn(0.5, exact_sqdist(x.x, x.y, x.z, y.x, y.y, y.z));
+      const double ex = __dadd_rn(__ddiv_rn(__dsub_rn(psi[j], c), eps), y.w);
+      const double p = exp(__dsub_rn(ex, L));
+      if (acc) {
+        const double w = __dmul_rn(p, x.w);
+        unsigned long long* a = acc + 12 * j;
+        fp_add(a, w);
+        fp_add(a + 3, __dmul_rn(w, x.x - lo0));
+        fp_add(a + 6, __dmul_rn(w, x.y - lo1));
+        fp_add(a + 9, __dmul_rn(w, x.z - lo2));
+      }
+      t0 = __dadd_rn(t0, __dmul_rn(p, y.x));
+      t1 = __dadd_rn(t1, __dmul_rn(p, y.y));
+      t2 = __dadd_rn(t2, __dmul_rn(p, y.z));
+      const double score = __dadd_rn(__dsub_rn(psi[j], c), __dmul_rn(eps, y.w));
+      if (score > best || (score == best && j < bj)) {
+        best = score;
+        bj = j;
+      }
+    }
+    t0 = warp_sum(t0);
+    t1 = warp_sum(t1);
+    t2 = warp_sum(t2);
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const unsigned long long oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (ob > best || (ob == best && oj < bj)) {
+        best = ob;
+        bj = oj;
+      }
+    }
+    if (lane == 0) {
+      if (map) {
+        map[3 * q] = t0;
+        map[3 * q + 1] = t1;
+        map[3 * q + 2] = t2;
+      }
+      if (modal) modal[q] = bj;
+    }
+  }
+}
+
+__global__ void plan_assemble_kernel(const unsigned long long* __restrict__ acc, int n, double lo0,
+                                     double lo1, double lo2, double* __restrict__ marginal,
+                                     double* __restrict__ moment) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const unsigned long long* a = acc + 12 * static_cast<size_t>(j);
+  const double t = fp_to_double(a);
+  if (marginal) marginal[j] = t;
+  if (moment) {
+    moment[3 * j] = fp_to_double(a + 3) + lo0 * t;
+    moment[3 * j + 1] = fp_to_double(a + 6) + lo1 * t;
+    moment[3 * j + 2] = fp_to_double(a + 9) + lo2 * t;
+  }
+}
+
 }  // namespace
 
 void PointOrders::release() {
@@ -1792,6 +1928,101 @@ int run_covering_cost(TruncWorkspace& ws, const DeviceAtoms& a, const DeviceTarg
   cudaFree(d2);
   cudaFree(idx);
   cudaFree(dres);
+  return 0;
+}
+
+int run_plan_candidates(TruncWorkspace& ws, const DeviceAtoms& a, const DeviceTargets& t,
+                        TargetCells& tc, double cutoff, const uint64_t* off_host,
+                        uint64_t* idx_host, cudaStream_t s, std::string& err) {
+  const int nq = a.nq;
+  if (nq == 0) return 0;
+  const double radius = cutoff < 0.0 ? 0.0 : std::sqrt(2.0 * cutoff);  // cost.hpp:38-42
+  const double r2 = radius * radius;
+  const bool scan = radius > 0.0;
+  const double r_use = scan ? radius : 0.0;
+  const double r_scan = r_use * (1.0 + 1e-9) + 1e-300;
+  if (ensure_target_cells(ws, t, tc, r_use, s, err)) return 1;
+  const size_t total = off_host[nq];
+  unsigned long long *off = nullptr, *idx = nullptr, *sorted = nullptr;
+  int* bad = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  TCK(cudaMalloc(&off, sizeof(unsigned long long) * (nq + 1)));
+  TCK(cudaMalloc(&idx, sizeof(unsigned long long) * std::max<size_t>(total, 1)));
+  TCK(cudaMalloc(&sorted, sizeof(unsigned long long) * std::max<size_t>(total, 1)));
+  TCK(cudaMalloc(&bad, sizeof(int)));
+  TCK(cudaMemcpyAsync(off, off_host, sizeof(unsigned long long) * (nq + 1), cudaMemcpyHostToDevice, s));
+  TCK(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  (note_launch(), plan_fill_kernel<<<std::min(8192, (nq + 7) / 8), 256, 0, s>>>(
+      a.x, nq, tc.pc, tc.perm_c, tc.cell_start, to_dev(tc.g), r2, r_scan, scan ? 1 : 0, off, idx,
+      bad));
+  TCK(cub::DeviceSegmentedSort::SortKeys(tmp, tmp_bytes, idx, sorted, static_cast<int64_t>(total), nq,
+                                         off, off + 1, s));
+  TCK(cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 1)));
+  TCK(cub::DeviceSegmentedSort::SortKeys(tmp, tmp_bytes, idx, sorted, static_cast<int64_t>(total), nq,
+                                         off, off + 1, s));
+  int hbad = 0;
+  TCK(cudaMemcpyAsync(idx_host, sorted, sizeof(unsigned long long) * total, cudaMemcpyDeviceToHost, s));
+  TCK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  TCK(cudaStreamSynchronize(s));
+  cudaFree(off);
+  cudaFree(idx);
+  cudaFree(sorted);
+  cudaFree(bad);
+  cudaFree(tmp);
+  if (hbad) {
+    err = "plan candidates: offsets do not match the candidate counts";
+    return 1;
+  }
+  return 0;
+}
+
+int run_plan_moments(const DeviceAtoms& a, const DeviceTargets& t, const double* psi_host,
+                     double eps, const double* log_s_host, const uint64_t* off_host,
+                     const uint64_t* idx_host, const double atom_lo[3], double* marginal,
+                     double* moment, double* map, uint64_t* modal, cudaStream_t s,
+                     std::string& err) {
+  const int nq = a.nq, n = t.n;
+  const size_t total = off_host ? off_host[nq] : 0;
+  double *psi = nullptr, *ls = nullptr, *dmarg = nullptr, *dmom = nullptr, *dmap = nullptr;
+  unsigned long long *off = nullptr, *idx = nullptr, *acc = nullptr, *dmodal = nullptr;
+  TCK(cudaMalloc(&psi, sizeof(double) * std::max(n, 1)));
+  TCK(cudaMalloc(&ls, sizeof(double) * std::max(nq, 1)));
+  TCK(cudaMemcpyAsync(psi, psi_host, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  TCK(cudaMemcpyAsync(ls, log_s_host, sizeof(double) * nq, cudaMemcpyHostToDevice, s));
+  if (off_host) {
+    TCK(cudaMalloc(&off, sizeof(unsigned long long) * (nq + 1)));
+    TCK(cudaMalloc(&idx, sizeof(unsigned long long) * std::max<size_t>(total, 1)));
+    TCK(cudaMemcpyAsync(off, off_host, sizeof(unsigned long long) * (nq + 1), cudaMemcpyHostToDevice, s));
+    TCK(cudaMemcpyAsync(idx, idx_host, sizeof(unsigned long long) * total, cudaMemcpyHostToDevice, s));
+  }
+  const bool want_acc = marginal || moment;
+  if (want_acc) {
+    TCK(cudaMalloc(&acc, sizeof(unsigned long long) * 12 * std::max(n, 1)));
+    TCK(cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * 12 * std::max(n, 1), s));
+    TCK(cudaMalloc(&dmarg, sizeof(double) * std::max(n, 1)));
+    TCK(cudaMalloc(&dmom, sizeof(double) * 3 * std::max(n, 1)));
+  }
+  if (map) TCK(cudaMalloc(&dmap, sizeof(double) * 3 * std::max(nq, 1)));
+  if (modal) TCK(cudaMalloc(&dmodal, sizeof(unsigned long long) * std::max(nq, 1)));
+  if (nq > 0)
+    (note_launch(), plan_moments_kernel<<<std::min(8192, (nq + 7) / 8), 256, 0, s>>>(
+        a.x, nq, t.y, n, psi, eps, ls, off, idx, atom_lo[0], atom_lo[1], atom_lo[2], acc, dmap,
+        dmodal));
+  if (want_acc && n > 0) {
+    (note_launch(), plan_assemble_kernel<<<(n + 255) / 256, 256, 0, s>>>(acc, n, atom_lo[0], atom_lo[1],
+                                                                      atom_lo[2], dmarg, dmom));
+    if (marginal) TCK(cudaMemcpyAsync(marginal, dmarg, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    if (moment) TCK(cudaMemcpyAsync(moment, dmom, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+  }
+  if (map && nq) TCK(cudaMemcpyAsync(map, dmap, sizeof(double) * 3 * nq, cudaMemcpyDeviceToHost, s));
+  if (modal && nq)
+    TCK(cudaMemcpyAsync(modal, dmodal, sizeof(unsigned long long) * nq, cudaMemcpyDeviceToHost, s));
+  TCK(cudaStreamSynchronize(s));
+  void* ptrs[] = {psi, ls, dmarg, dmom, dmap, off, idx, acc, dmodal};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  TCK(cudaGetLastError());
   return 0;
 }
 

@@ -310,8 +310,8 @@ class Context:
         return v.value
 
 
-def _ptr(a: np.ndarray) -> ctypes.c_void_p:
-    return ctypes.c_void_p(a.ctypes.data)
+def _ptr(a: Optional[np.ndarray]) -> ctypes.c_void_p:
+    return ctypes.c_void_p(a.ctypes.data if a is not None else None)
 
 
 class DeviceTargets:
@@ -498,3 +498,106 @@ def evaluate_dual_debug(atoms: SourceAtoms, target: TargetMeasure, psi, eps: flo
                      candidate_pairs=int(sc.candidate_pairs),
                      empty_candidate_atoms=int(sc.empty_candidate_atoms))
     return res, cnt, hsh, logs
+
+
+# ---- PlanView (proj/include/rsot/plan.hpp, proj/src/plan.cpp) --------------
+
+class MapKind(enum.Enum):
+    Barycentric = 0
+    Modal = 1
+
+
+@dataclass
+class MapSample:
+    kind: MapKind
+    mapped: np.ndarray                  # (nq, 3) T(x_q)
+    target_index: Optional[np.ndarray]  # modal only
+    displacement: np.ndarray            # ||T(x_q) - x_q||
+
+
+class PlanView:
+    """The plan induced by a potential (plan.hpp:17-73).  The constructor
+    computes log_S_q and the candidate sets on the GPU (plan.cpp:12-59); the
+    reductions over the plan density run on the GPU over those sets."""
+
+    def __init__(self, atoms: SourceAtoms, target: TargetMeasure, psi: DualPotential, eps: float,
+                 kind: CostKind = CostKind.SqEuclidean, cutoff: float = math.inf, workers: int = 1,
+                 ctx: Optional[Context] = None):
+        if kind != CostKind.SqEuclidean:
+            raise ValueError("plan view: only the squared Euclidean cost runs on the GPU")
+        values = np.ascontiguousarray(np.asarray(psi.values, dtype=np.float64))
+        if len(values) != target.size():
+            raise ValueError("plan view: psi length != target count")
+        require_finite(values)
+        self.ctx = ctx or Context.default()
+        self.atoms, self.target, self.psi, self.eps, self.kind = atoms, target, values, float(eps), kind
+        self._dt = DeviceTargets(self.ctx, target.points, target.weights)
+        self._da = DeviceAtoms(self.ctx, atoms.points, atoms.masses, shard=False)
+        _, cnt, _, logs = evaluate_dual_debug(atoms, target, values, eps, cutoff, ctx=self.ctx)
+        self.log_S = logs
+        self.offsets = np.zeros(len(cnt) + 1, dtype=np.uint64)
+        np.cumsum(cnt.astype(np.uint64), out=self.offsets[1:])
+        self.idx = np.zeros(max(int(self.offsets[-1]), 1), dtype=np.uint64)
+        _lib.check(self.ctx.lib.rsot_cuda_plan_candidates(self.ctx.handle, self._da.handle, self._dt.handle,
+                                                          float(cutoff), _ptr(self.offsets), _ptr(self.idx)))
+        self.converged_known = False
+        self.converged = False
+
+    def set_convergence(self, grad_l1: float, delta_tol: float) -> None:
+        self.converged_known = True
+        self.converged = grad_l1 <= delta_tol
+
+    def candidates(self, q: int) -> np.ndarray:
+        return self.idx[int(self.offsets[q]):int(self.offsets[q + 1])].astype(np.int64)
+
+    def psi_value(self, j: int) -> float:
+        return float(self.psi[j])
+
+    def _moments(self, marginal=False, moment=False, bary_map=False, modal=False):
+        n, nq = self.target.size(), self.atoms.size()
+        out = dict(marginal=np.zeros(n) if marginal else None, moment=np.zeros((n, 3)) if moment else None,
+                   map=np.zeros((nq, 3)) if bary_map else None,
+                   modal=np.zeros(nq, dtype=np.uint64) if modal else None)
+        _lib.check(self.ctx.lib.rsot_cuda_plan_moments(
+            self.ctx.handle, self._da.handle, self._dt.handle, _ptr(self.psi), self.eps, _ptr(self.log_S),
+            _ptr(self.offsets), _ptr(self.idx), _ptr(out["marginal"]), _ptr(out["moment"]), _ptr(out["map"]),
+            _ptr(out["modal"])))
+        return out
+
+    def plan_density(self, q: int):
+        """(target index, probability) pairs of atom q (plan.cpp:70-83)."""
+        x = _points3(self.atoms.points)[q]
+        cand = self.candidates(q)
+        y = _points3(self.target.points)[cand]
+        c = 0.5 * (((x[0] - y[:, 0]) ** 2 + (x[1] - y[:, 1]) ** 2) + (x[2] - y[:, 2]) ** 2)
+        e = (self.psi[cand] - c) / self.eps + np.log(np.asarray(self.target.weights)[cand])
+        return list(zip(cand.tolist(), np.exp(e - self.log_S[q]).tolist()))
+
+    def target_marginals(self) -> np.ndarray:
+        return self._moments(marginal=True)["marginal"]
+
+    def all_conditional_barycenters(self) -> np.ndarray:
+        r = self._moments(marginal=True, moment=True)
+        tilde = r["marginal"]
+        bad = np.nonzero(tilde < 1e-30)[0]
+        if len(bad):
+            raise RuntimeError(f"target starved: index {int(bad[0])}")
+        return (1.0 / tilde)[:, None] * r["moment"]
+
+    def conditional_barycenter(self, j: int) -> np.ndarray:
+        return self.all_conditional_barycenters()[j]
+
+
+def barycentric_map(plan: PlanView) -> MapSample:
+    """T(x_q) = sum_j p_j(x_q) y_j (plan.cpp:142-156)."""
+    m = plan._moments(bary_map=True)["map"]
+    x = _points3(plan.atoms.points)
+    return MapSample(MapKind.Barycentric, m, None, np.sqrt(((m - x) ** 2).sum(axis=1)))
+
+
+def modal_map(plan: PlanView) -> MapSample:
+    """argmax_j (psi_j - c + eps ln nu_j), lowest index on ties (plan.cpp:158-182)."""
+    idx = plan._moments(modal=True)["modal"].astype(np.int64)
+    y = _points3(plan.target.points)[idx]
+    x = _points3(plan.atoms.points)
+    return MapSample(MapKind.Modal, y, idx, np.sqrt(((y - x) ** 2).sum(axis=1)))

@@ -237,3 +237,40 @@ def test_softmax_refine_identity_cases():
         t = -0.5 * ((ax - fy[k]) ** 2).sum(axis=1) / 0.1 - logS + np.log(am)
         m = t.max()
         assert out[k] == pytest.approx(-0.1 * (m + np.log(np.exp(t - m).sum())), rel=1e-12, abs=1e-14)
+
+
+def _ref_or_skip():
+    if not have_ref:
+        pytest.skip("reference library not built here")
+    from oracle.oracle import RefLib
+    return RefLib()
+
+
+@pytest.mark.parametrize("dim,n,nq,eps,cutoff", [(3, 300, 2000, 0.02, math.inf), (3, 300, 2000, 0.02, 0.01),
+                                                 (2, 200, 1500, 0.01, 0.002), (3, 50, 800, 0.05, -1.0)])
+def test_plan_view_oracle_equals_reference(dim, n, nq, eps, cutoff):
+    """PlanView restatement (oracle_plan_view) vs the reference plan.cpp
+    compiled from its sources: candidate counts, marginals, conditional
+    barycentres, barycentric and modal maps bit for bit."""
+    ref = _ref_or_skip()
+    rng = np.random.default_rng(5)
+    A, M, T, W, psi = random_instance(rng, dim, n, nq, 0.05)
+    o = C.plan_view(A, M, T, W, psi, eps, cutoff)
+    r = ref.problem(dim, A, M, T, W).plan_view(psi, eps, cutoff)
+    for k in ("count", "marginal", "bary", "map", "modal"):
+        assert np.array_equal(o[k], r[k]), k
+    assert o["starved"] == r["starved"] == -1
+
+
+def test_plan_view_oracle_starved_equals_reference():
+    ref = _ref_or_skip()
+    rng = np.random.default_rng(5)
+    A, M, T, W, psi = random_instance(rng, 3, 300, 2000, 0.05)
+    T[17] = [5, 5, 5]
+    T[40] = [6, 6, 6]
+    psi[17] = -10
+    for cutoff in (math.inf, 0.01):
+        o = C.plan_view(A, M, T, W, psi, 0.02, cutoff)
+        r = ref.problem(3, A, M, T, W).plan_view(psi, 0.02, cutoff)
+        assert o["starved"] == r["starved"] == 17
+        assert np.array_equal(o["marginal"], r["marginal"]) and np.array_equal(o["map"], r["map"])

@@ -323,5 +323,61 @@ double covering_cost_device(const SourceAtoms& atoms, const TargetMeasure& targe
   return c0;
 }
 
+// ---- PlanView building blocks (plan_cuda.cpp) -------------------------------
+
+void plan_build_device(const SourceAtoms& atoms, const TargetMeasure& target,
+                       const std::vector<double>& psi, double eps, double cutoff,
+                       std::vector<double>& log_S,
+                       std::vector<std::vector<std::size_t>>& candidates) {
+  auto& st = cuda_detail::state();
+  std::lock_guard<std::mutex> lock(st.mu);
+  rsot_cuda_targets* dt = st.get_targets(target);
+  rsot_cuda_atoms* da = st.get_atoms(atoms, /*full=*/true);
+  const std::size_t nq = atoms.size(), n = target.size();
+  log_S.assign(nq, 0.0);
+  std::vector<uint32_t> count(nq);
+  std::vector<double> g(n);
+  rsot_cuda_scalars sc{};
+  int rc = rsot_cuda_eval_debug(st.context(), da, dt, psi.data(), eps, cutoff, g.data(), &sc,
+                                count.data(), nullptr, log_S.data());
+  if (rc) cuda_detail::raise(rc, "PlanView (B200 drop-in)");
+  std::vector<uint64_t> off(nq + 1, 0);
+  for (std::size_t q = 0; q < nq; ++q) off[q + 1] = off[q] + count[q];
+  std::vector<uint64_t> idx(std::max<uint64_t>(off[nq], 1));
+  rc = rsot_cuda_plan_candidates(st.context(), da, dt, cutoff, off.data(), idx.data());
+  if (rc) cuda_detail::raise(rc, "PlanView (B200 drop-in)");
+  candidates.assign(nq, {});
+  for (std::size_t q = 0; q < nq; ++q)
+    candidates[q].assign(idx.begin() + static_cast<std::ptrdiff_t>(off[q]),
+                         idx.begin() + static_cast<std::ptrdiff_t>(off[q + 1]));
+}
+
+void plan_moments_device(const SourceAtoms& atoms, const TargetMeasure& target,
+                         const std::vector<double>& psi, double eps,
+                         const std::vector<double>& log_S,
+                         const std::vector<std::vector<std::size_t>>& candidates,
+                         double* marginal, double* moment, double* map, std::uint64_t* modal) {
+  auto& st = cuda_detail::state();
+  std::lock_guard<std::mutex> lock(st.mu);
+  rsot_cuda_targets* dt = st.get_targets(target);
+  rsot_cuda_atoms* da = st.get_atoms(atoms, /*full=*/true);
+  const std::size_t nq = atoms.size(), n = target.size();
+  // dense plans (every set = all targets, ascending) need no index upload
+  bool dense = true;
+  for (std::size_t q = 0; q < nq && dense; ++q) dense = candidates[q].size() == n;
+  std::vector<uint64_t> off, idx;
+  if (!dense) {
+    off.assign(nq + 1, 0);
+    for (std::size_t q = 0; q < nq; ++q) off[q + 1] = off[q] + candidates[q].size();
+    idx.reserve(std::max<uint64_t>(off[nq], 1));
+    for (const auto& c : candidates) idx.insert(idx.end(), c.begin(), c.end());
+    if (idx.empty()) idx.push_back(0);
+  }
+  const int rc = rsot_cuda_plan_moments(st.context(), da, dt, psi.data(), eps, log_S.data(),
+                                        dense ? nullptr : off.data(), dense ? nullptr : idx.data(),
+                                        marginal, moment, map, modal);
+  if (rc) cuda_detail::raise(rc, "PlanView (B200 drop-in)");
+}
+
 }  // namespace cuda
 }  // namespace rsot

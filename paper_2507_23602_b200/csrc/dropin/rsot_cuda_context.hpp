@@ -7,7 +7,11 @@
 // single GPU.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
+#include <vector>
+
+#include "rsot/measures.hpp"
 
 namespace rsot::cuda {
 
@@ -29,5 +33,22 @@ void clear_cache();
 
 // Kernel-launch counter of the underlying library (for tests/benchmarks).
 std::uint64_t kernel_launches();
+
+// GPU building blocks of the drop-in PlanView (plan_cuda.cpp), single GPU
+// (all atoms on this process's device):
+//   plan_build_device: log_S_q and the ascending candidate sets of the
+//     PlanView ctor (plan.cpp:12-59);
+//   plan_moments_device: over those sets, target marginals (n), first
+//     moments (3n), barycentric images (3 nq) and modal targets (nq); any
+//     output may be null.
+void plan_build_device(const SourceAtoms& atoms, const TargetMeasure& target,
+                       const std::vector<double>& psi, double eps, double cutoff,
+                       std::vector<double>& log_S,
+                       std::vector<std::vector<std::size_t>>& candidates);
+void plan_moments_device(const SourceAtoms& atoms, const TargetMeasure& target,
+                         const std::vector<double>& psi, double eps,
+                         const std::vector<double>& log_S,
+                         const std::vector<std::vector<std::size_t>>& candidates,
+                         double* marginal, double* moment, double* map, std::uint64_t* modal);
 
 }  // namespace rsot::cuda

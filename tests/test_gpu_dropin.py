@@ -4,6 +4,7 @@ measures}.cpp), compiled unmodified against the B200 drop-in library
 sources, GPU evaluate_dual / covering_cost).  The reference L-BFGS,
 epsilon-scaling, softmax_refine and multilevel drivers run on the host and
 call the GPU evaluator through the reference's Objective closure."""
+import math
 import os
 import subprocess
 
@@ -61,3 +62,33 @@ def test_cfg4_small_multilevel_solve_matches_reference():
     pr = np.fromfile(os.path.join(golden, "cfg4_small_ref_psi.f64"))
     pg = np.fromfile(dump)
     assert np.max(np.abs(pr - pg)) <= 1e-10 * np.max(np.abs(pr))
+
+
+@pytest.mark.parametrize("cutoff", [math.inf, 0.01, -1.0])
+def test_dropin_plan_view(tmp_path, cutoff):
+    """The drop-in PlanView (csrc/dropin/plan_cuda.cpp, unchanged plan.hpp)
+    through the reference's C++ interface vs the PlanView oracle (pinned to
+    the reference plan.cpp in tests/test_oracle.py)."""
+    import numpy as np
+    from conftest import random_instance
+    from oracle.oracle import COracle
+    rng = np.random.default_rng(44)
+    A, M, T, W, psi = random_instance(rng, 3, 400, 3000, 0.05)
+    for name, arr in (("atoms", A), ("masses", M), ("targets", T), ("nu", W), ("psi", psi)):
+        np.ascontiguousarray(arr, dtype=np.float64).tofile(tmp_path / f"{name}.f64")
+    exe = os.path.join(BIN, "plan_check")
+    assert os.path.exists(exe), "drop-in not built (build() in the build container)"
+    p = subprocess.run([exe, str(tmp_path), "0.02", repr(cutoff)], capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr
+    want = COracle().plan_view(A, M, T, W, psi, 0.02, cutoff)
+    assert np.array_equal(np.fromfile(tmp_path / "count.u64", dtype=np.uint64), want["count"])
+    marg = np.fromfile(tmp_path / "marginal.f64")
+    assert np.max(np.abs(marg - want["marginal"])) <= 1e-12 * np.max(want["marginal"])
+    starved = int(open(tmp_path / "starved.txt").read())
+    assert starved == want["starved"]
+    if starved < 0:
+        bary = np.fromfile(tmp_path / "bary.f64").reshape(-1, 3)
+        assert np.max(np.abs(bary - want["bary"])) <= 1e-12 * np.max(np.abs(want["bary"]))
+    mp = np.fromfile(tmp_path / "map.f64").reshape(-1, 3)
+    assert np.max(np.abs(mp - want["map"])) <= 1e-12
+    assert np.array_equal(np.fromfile(tmp_path / "modal.u64", dtype=np.uint64), want["modal"])

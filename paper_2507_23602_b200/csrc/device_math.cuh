@@ -8,11 +8,11 @@
 // origin o (x' = x - o, y' = y - o):
 //   e2_qj = (b2_j - c2|y'|^2) - c2|x'|^2 + (2 c2 x') . y'
 // so a pair costs three DFMA once the per-target and per-atom constants are
-// staged.  The sum of exponentials uses a table-driven exp2 with a degree-5
-// near-minimax polynomial (relative error 4.6e-15, vs the reference's libm
+// staged.  The sum of exponentials uses a table-driven exp2 (64 entries) with
+// a degree-4 near-minimax polynomial (relative error 2.4e-15, vs the reference's libm
 // exp at ~1e-16; the parity bar is 1e-10).  The final multiply by 2^k*T[i]
-// is fused into the accumulation FMA, so exp2 + accumulate is 9 FP64-pipe
-// instructions (3 DADD + 6 DFMA); the integer split runs on the INT pipe.
+// is fused into the accumulation FMA, so exp2 + accumulate is 8 FP64-pipe
+// instructions (3 DADD + 5 DFMA); the integer split runs on the INT pipe.
 #pragma once
 
 #include <cstdint>
@@ -23,67 +23,86 @@ namespace rsot_cuda {
 constexpr double kLog2e = 1.4426950408889634074;   // 0x1.71547652b82fep+0
 constexpr double kLn2 = 0.69314718055994530942;    // 0x1.62e42fefa39efp-1
 
-// 1.5 * 2^48: adding it rounds to the 1/16 grid and leaves round(16 s) in
-// the low mantissa bits.
-constexpr double kExpMagic = 0x1.8p48;
+// exp2 split s = n/64 + r: 1.5 * 2^46 added to s rounds it to the 1/64 grid
+// and leaves n = round(64 s) in the low mantissa word.
+constexpr double kExpMagic = 0x1.8p46;
+constexpr int kExpTab = 64;          // table entries 2^(i/64)
+constexpr int kExpUnit = 1 << 14;    // n * kExpUnit = (n >> 6) << 20 + (n & 63) << 14
+constexpr int kExpNMin = -65280;     // clamp of n: s >= -1020
+constexpr int kExpNMax = 64000;      //             s <=  1000
+constexpr int kExpZeroN = -65472;    // 64 * (-1023): scale word pattern +0.0
 
-// 2^(i/16) correctly rounded (mpmath, 200 bits), stored as {lo, hi - (i<<16)}
-// so that the scale 2^k * 2^(i/16) for n = 16k + i is the double with words
-// {lo, hi' + (n << 16)}: one IMAD instead of split/shift/add.
-__device__ __constant__ int2 kExp2Table[16] = {
-    {0x00000000, 0x3ff00000}, {0x6cf9890f, 0x3fefb558}, {0x3c7d517b, 0x3fef72b8},
-    {0x6e756238, 0x3fef387a}, {0x0a31b715, 0x3fef06fe}, {0x4c123422, 0x3feedea6},
-    {(int)0xd5362a27, 0x3feebfda}, {(int)0xdd485429, 0x3feeab07}, {0x667f3bcd, 0x3feea09e},
-    {0x73eb0187, 0x3feea114}, {0x422aa0db, 0x3feeace5}, {(int)0x82a3f090, 0x3feec491},
-    {(int)0x995ad3ad, 0x3feee89f}, {(int)0xdd85529c, 0x3fef199b}, {(int)0xdcfba487, 0x3fef5818},
-    {(int)0xa2a490da, 0x3fefa4af}};
+// 2^(i/64) correctly rounded (mpmath, 200 bits; tools/gen_exp2_table.py),
+// stored as {lo, hi - (i << 14)} so that the scale 2^k * 2^(i/64) for
+// n = 64k + i is the double with words {lo, hi' + n * 2^14}: one IMAD
+// instead of split/shift/add.
+__device__ __constant__ int2 kExp2Table[kExpTab] = {
+    {0x00000000, 0x3ff00000}, {0x3e778061, 0x3fefec9a}, {(int)0xd3158574, 0x3fefd9b0},
+    {0x18759bc8, 0x3fefc745}, {0x6cf9890f, 0x3fefb558}, {0x32d3d1a2, 0x3fefa3ec},
+    {(int)0xd0125b51, 0x3fef9301}, {(int)0xaea92de0, 0x3fef829a}, {0x3c7d517b, 0x3fef72b8},
+    {(int)0xeb6fcb75, 0x3fef635b}, {0x3168b9aa, 0x3fef5487}, {(int)0x88628cd6, 0x3fef463b},
+    {0x6e756238, 0x3fef387a}, {0x65e27cdd, 0x3fef2b45}, {(int)0xf51fdee1, 0x3fef1e9d},
+    {(int)0xa6e4030b, 0x3fef1285}, {0x0a31b715, 0x3fef06fe}, {(int)0xb26416ff, 0x3feefc08},
+    {0x373aa9cb, 0x3feef1a7}, {0x34e59ff7, 0x3feee7db}, {0x4c123422, 0x3feedea6},
+    {0x21f72e2a, 0x3feed60a}, {0x6061892d, 0x3feece08}, {(int)0xb5c13cd0, 0x3feec6a2},
+    {(int)0xd5362a27, 0x3feebfda}, {0x769d2ca7, 0x3feeb9b2}, {0x569d4f82, 0x3feeb42b},
+    {0x36b527da, 0x3feeaf47}, {(int)0xdd485429, 0x3feeab07}, {0x15ad2148, 0x3feea76f},
+    {(int)0xb03a5585, 0x3feea47e}, {(int)0x82552225, 0x3feea238}, {0x667f3bcd, 0x3feea09e},
+    {0x3c651a2f, 0x3fee9fb2}, {(int)0xe8ec5f74, 0x3fee9f75}, {0x564267c9, 0x3fee9feb},
+    {0x73eb0187, 0x3feea114}, {0x36cf4e62, 0x3feea2f3}, {(int)0x994cce13, 0x3feea589},
+    {(int)0x9b4492ed, 0x3feea8d9}, {0x422aa0db, 0x3feeace5}, {(int)0x99157736, 0x3feeb1ae},
+    {(int)0xb0cdc5e5, 0x3feeb737}, {(int)0x9fde4e50, 0x3feebd82}, {(int)0x82a3f090, 0x3feec491},
+    {0x7b5de565, 0x3feecc66}, {(int)0xb23e255d, 0x3feed503}, {0x5579fdbf, 0x3feede6b},
+    {(int)0x995ad3ad, 0x3feee89f}, {(int)0xb84f15fb, 0x3feef3a2}, {(int)0xf2fb5e47, 0x3feeff76},
+    {(int)0x904bc1d2, 0x3fef0c1e}, {(int)0xdd85529c, 0x3fef199b}, {0x2e57d14b, 0x3fef27f1},
+    {(int)0xdcef9069, 0x3fef3720}, {0x4a07897c, 0x3fef472d}, {(int)0xdcfba487, 0x3fef5818},
+    {0x03db3285, 0x3fef69e6}, {0x337b9b5f, 0x3fef7c97}, {(int)0xe78b3ff6, 0x3fef902e},
+    {(int)0xa2a490da, 0x3fefa4af}, {(int)0xee615a27, 0x3fefba1b}, {0x5b6e4540, 0x3fefd076},
+    {(int)0x819e90d8, 0x3fefe7c1}};
 
-// Near-minimax degree-5 fit of 2^r on [-1/32, 1/32] (mpmath chebyfit),
-// coefficients rounded to double; worst relative error 4.61e-15.  Kept in
-// constant memory so the DFMAs take them as c[][] operands (no per-loop
-// uniform-register materialisation).
-__device__ __constant__ double kPoly[6] = {0x1.0000000000014p+0, 0x1.62e42fefa39f3p-1,
-                                           0x1.ebfbdff555824p-3, 0x1.c6b08d6f2a289p-5,
-                                           0x1.3b2c9b8a6caeap-7, 0x1.5d897e525c216p-10};
+// Near-minimax degree-4 fit of 2^r on [-1/128, 1/128] (mpmath chebyfit,
+// tools/gen_exp2_table.py), coefficients rounded to double; worst relative
+// error 2.44e-15.  In constant memory so the DFMAs take them as c[][]
+// operands (no per-loop uniform-register materialisation).
+__device__ __constant__ double kPoly[5] = {0x1.0000000000000p+0, 0x1.62e42fefa0352p-1,
+                                           0x1.ebfbdff82ac52p-3, 0x1.c6b0c40d8c4e9p-5,
+                                           0x1.3b2ad0385b409p-7};
 #define kP0 (kPoly[0])
 #define kP1 (kPoly[1])
 #define kP2 (kPoly[2])
 #define kP3 (kPoly[3])
 #define kP4 (kPoly[4])
-#define kP5 (kPoly[5])
 
-// Copies the exp2 table into shared memory (16 x 8 B = 128 B: a half-warp
-// LDS.64 with any index pattern is one conflict-free wavefront).
+// Copies the exp2 table into shared memory (64 x 8 B = 512 B).
 __device__ __forceinline__ void load_exp2_table(int2* smem_tbl) {
-  if (threadIdx.x < 16) smem_tbl[threadIdx.x] = kExp2Table[threadIdx.x];
+  for (int i = threadIdx.x; i < kExpTab; i += blockDim.x) smem_tbl[i] = kExp2Table[i];
 }
 
-// acc + 2^s.  Exact split s = n/16 + r (|r| <= 1/32) by the magic-constant
-// addition, 2^r by the polynomial, 2^(n/16) by table + exponent add.  n is
-// clamped to [-16320, 16000]: s below -1020 contributes at most 2^-1019
+// acc + 2^s.  Exact split s = n/64 + r (|r| <= 1/128) by the magic-constant
+// addition, 2^r by the polynomial, 2^(n/64) by table + exponent add.  n is
+// clamped to [64 (-1020), 64 * 1000]: s below -1020 contributes at most 2^-1019
 // (the reference would add a subnormal or zero); s above 1000 yields at least
 // 2^999, which the callers detect (sum > 2^960) and route to the exact
-// per-atom path.  FP64 pipe: 3 DADD + 6 DFMA; INT: 2 IMNMX, LOP3, LEA, IMAD.
+// per-atom path.  FP64 pipe: 3 DADD + 5 DFMA; INT: 2 IMNMX, LOP3, LEA, IMAD.
 template <bool CLAMP = true>
 __device__ __forceinline__ double exp2_acc(double s, double acc,
                                            const int2* __restrict__ tbl) {
   const double kk = __dadd_rn(s, kExpMagic);
-  int n = __double2loint(kk);  // round(16 s)
-  if (CLAMP) n = min(max(n, -16320), 16000);
+  int n = __double2loint(kk);  // round(64 s)
+  if (CLAMP) n = min(max(n, kExpNMin), kExpNMax);
   const double kd = __dadd_rn(kk, -kExpMagic);
-  const double r = __dadd_rn(s, -kd);        // |r| <= 1/32
-  double p = fma(kP5, r, kP4);
-  p = fma(p, r, kP3);
+  const double r = __dadd_rn(s, -kd);        // |r| <= 1/128
+  double p = fma(kP4, r, kP3);
   p = fma(p, r, kP2);
   p = fma(p, r, kP1);
   p = fma(p, r, kP0);
-  const int2 t = tbl[n & 15];
-  const double scale = __hiloint2double(t.y + n * 65536, t.x);
+  const int2 t = tbl[n & (kExpTab - 1)];
+  const double scale = __hiloint2double(t.y + n * kExpUnit, t.x);
   return fma(p, scale, acc);
 }
 
 // acc + (take ? 2^s : 0) without a branch.  Lanes that do not take the
-// pair get n = -16368 = 16 * (-1023), whose scale word pattern is exactly
+// pair get n = kExpZeroN = 64 * (-1023), whose scale word pattern is exactly
 // +0.0 (one SEL on the INT pipe).  CLAMP = false is used when the caller has
 // proven every taken s lies in [-1020, 1000].
 template <bool CLAMP = true>
@@ -91,17 +110,16 @@ __device__ __forceinline__ double exp2_acc_masked(double s, double acc,
                                                   const int2* __restrict__ tbl, bool take) {
   const double kk = __dadd_rn(s, kExpMagic);
   int n = __double2loint(kk);
-  if (CLAMP) n = min(max(n, -16320), 16000);
+  if (CLAMP) n = min(max(n, kExpNMin), kExpNMax);
   const double kd = __dadd_rn(kk, -kExpMagic);
   const double r = __dadd_rn(s, -kd);
-  double p = fma(kP5, r, kP4);
-  p = fma(p, r, kP3);
+  double p = fma(kP4, r, kP3);
   p = fma(p, r, kP2);
   p = fma(p, r, kP1);
   p = fma(p, r, kP0);
-  n = take ? n : -16368;
-  const int2 t = tbl[n & 15];
-  return fma(p, __hiloint2double(t.y + n * 65536, t.x), acc);
+  n = take ? n : kExpZeroN;
+  const int2 t = tbl[n & (kExpTab - 1)];
+  return fma(p, __hiloint2double(t.y + n * kExpUnit, t.x), acc);
 }
 
 // Exact reference predicate (point.hpp:35-40, spatial_index.cpp:54):

@@ -484,7 +484,7 @@ struct FusedSmem {
   unsigned char wlist[kT / 32][kTileT];
   double colW[kT / 32][kTileT];
   Region R;                            // CTA-uniform scan region (kept out of registers)
-  int2 tbl[16];
+  int2 tbl[kExpTab];
   double sh[200];
   int shi[40];
 };
@@ -529,27 +529,25 @@ __device__ __forceinline__ double exp2_pair_weighted(double sa, double sb, doubl
   int na = __double2loint(kka);
   int nb = __double2loint(kkb);
   if (CLAMP) {
-    na = min(max(na, -16320), 16000);
-    nb = min(max(nb, -16320), 16000);
+    na = min(max(na, kExpNMin), kExpNMax);
+    nb = min(max(nb, kExpNMin), kExpNMax);
   }
   const double ra = __dadd_rn(sa, -__dadd_rn(kka, -kExpMagic));
   const double rb = __dadd_rn(sb, -__dadd_rn(kkb, -kExpMagic));
-  double qa = fma(kP5, ra, kP4);
-  double qb = fma(kP5, rb, kP4);
-  qa = fma(qa, ra, kP3);
-  qb = fma(qb, rb, kP3);
+  double qa = fma(kP4, ra, kP3);
+  double qb = fma(kP4, rb, kP3);
   qa = fma(qa, ra, kP2);
   qb = fma(qb, rb, kP2);
   qa = fma(qa, ra, kP1);
   qb = fma(qb, rb, kP1);
   qa = fma(qa, ra, kP0);
   qb = fma(qb, rb, kP0);
-  na = ta ? na : -16368;  // scale word pattern 0 -> +0.0
-  nb = tb ? nb : -16368;
-  const int2 Ta = tbl[na & 15];
-  const int2 Tb = tbl[nb & 15];
-  const double sca = __hiloint2double(Ta.y + na * 65536, Ta.x) * wa;
-  const double scb = __hiloint2double(Tb.y + nb * 65536, Tb.x) * wb;
+  na = ta ? na : kExpZeroN;  // scale word pattern 0 -> +0.0
+  nb = tb ? nb : kExpZeroN;
+  const int2 Ta = tbl[na & (kExpTab - 1)];
+  const int2 Tb = tbl[nb & (kExpTab - 1)];
+  const double sca = __hiloint2double(Ta.y + na * kExpUnit, Ta.x) * wa;
+  const double scb = __hiloint2double(Tb.y + nb * kExpUnit, Tb.x) * wb;
   return fma(qa, sca, qb * scb);
 }
 

@@ -73,8 +73,10 @@ int rsot_cuda_ctx_synchronize(rsot_cuda_ctx* ctx);
 int rsot_cuda_ctx_num_sms(rsot_cuda_ctx* ctx);
 
 /* ---- multi-GPU (atoms sharded, targets replicated) ------------------------
- * The gradient and scalars are combined with one ncclAllReduce(sum) per
- * evaluation.  Rank 0 creates the id and ships its 128 bytes
+ * The gradient and scalars are combined with one collective per evaluation
+ * (SURVEY.md §8e): ncclAllGather of the ranks' packed partial buffers and a
+ * rank-ordered sum on every rank, so results are bitwise identical across
+ * ranks and runs whatever algorithm NCCL picks.  Rank 0 creates the id and ships its 128 bytes
  * to the other ranks out of band (e.g. torch.distributed broadcast). */
 int rsot_cuda_comm_unique_id(unsigned char id_out[128]);
 int rsot_cuda_ctx_set_comm(rsot_cuda_ctx* ctx, int rank, int world,

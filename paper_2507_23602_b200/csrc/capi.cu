@@ -49,6 +49,8 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t,
                             ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool ok = false;
@@ -67,9 +69,10 @@ NcclApi& nccl() {
     api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(api.handle, "ncclGetUniqueId"));
     api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(api.handle, "ncclCommInitRank"));
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(api.handle, "ncclAllReduce"));
+    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(api.handle, "ncclAllGather"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.handle, "ncclCommDestroy"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.handle, "ncclGetErrorString"));
-    api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy;
+    api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.AllGather && api.CommDestroy;
   });
   return api;
 }
@@ -104,7 +107,7 @@ struct rsot_cuda_ctx {
   int rank = 0, world = 1;
   // workspace
   DevBuf<double> psi, b2, scal, part, partS, shiftA, atomL, atomLam, atomJ,
-      atomD, partG, res, g_out, scalars_out;
+      atomD, partG, res, g_out, scalars_out, gathered;
   DevBuf<int> flagged;
   TruncWorkspace trunc;
   RefineWorkspace refine;
@@ -163,6 +166,7 @@ int ensure_workspace(rsot_cuda_ctx* c, size_t nq, size_t n, const DenseLaunch& p
   RSOT_CK(c->res.ensure(n + kResTail));
   RSOT_CK(c->g_out.ensure(n));
   RSOT_CK(c->scalars_out.ensure(kResTail));
+  if (c->comm) RSOT_CK(c->gathered.ensure(static_cast<size_t>(c->world) * (n + kResTail)));
   return RSOT_CUDA_OK;
 }
 
@@ -207,12 +211,16 @@ int enqueue_eval(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
     if (dbg) launch_dense_debug(da, dt, b, *dbg, s);
   }
   if (c->comm) {
+    // one collective per evaluation: every rank gathers all packed partial
+    // buffers and sums them in rank order, so the result is bitwise the same
+    // on every rank and run to run (independent of NCCL's ring / tree / NVLS
+    // choice)
     NcclApi& api = nccl();
-    const ncclResult_t r = api.AllReduce(b.res, b.res, t->n + kResTail,
-                                         ncclDouble, ncclSum, c->comm, s);
+    const size_t len = t->n + kResTail;
+    const ncclResult_t r = api.AllGather(b.res, c->gathered.p, len, ncclDouble, c->comm, s);
     if (r != ncclSuccess)
-      return fail(RSOT_CUDA_RUNTIME_ERROR,
-                  std::string("ncclAllReduce: ") + api.GetErrorString(r));
+      return fail(RSOT_CUDA_RUNTIME_ERROR, std::string("ncclAllGather: ") + api.GetErrorString(r));
+    launch_rank_sum(c->gathered.p, c->world, len, b.res, s);
   }
   launch_finalize(dt, b, s);
   if (b.timing) cudaEventRecord(b.timing[5], s);
@@ -306,7 +314,7 @@ int rsot_cuda_ctx_destroy(rsot_cuda_ctx* c) {
   c->partS.release(); c->shiftA.release(); c->atomL.release();
   c->atomLam.release(); c->atomJ.release(); c->atomD.release();
   c->partG.release(); c->res.release(); c->g_out.release();
-  c->scalars_out.release(); c->flagged.release();
+  c->scalars_out.release(); c->flagged.release(); c->gathered.release();
   c->trunc.release();
   c->refine.release();
   if (c->h_pinned) cudaFreeHost(c->h_pinned);

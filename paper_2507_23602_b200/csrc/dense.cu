@@ -13,6 +13,7 @@
 //     the scatter of evaluate.cpp:151-153 becomes a register gather with a
 //     fixed summation order (no atomics), split over atom ranges and reduced
 //     in fixed order.  Bitwise reproducible for a fixed launch plan.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 
@@ -595,6 +596,25 @@ void launch_dense_gather(const double4* atoms, const double* lam, int nq, const 
   else
     (note_launch(), dense_passB<1><<<gB, kThreads, 0, s>>>(atoms, lam, nq, per_splitB, ty, b2, n, c2, partG));
   (note_launch(), reduce_partG<<<(n + 255) / 256, 256, 0, s>>>(partG, splitsB, n, G));
+}
+
+namespace {
+// Sum of the ranks' packed partial buffers in rank order (deterministic for a
+// given GPU count, independent of the collective's algorithm).
+__global__ void rank_sum_kernel(const double* __restrict__ gathered, int world, size_t len,
+                                double* __restrict__ out) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < len;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    double acc = gathered[i];
+    for (int r = 1; r < world; ++r) acc += gathered[r * len + i];
+    out[i] = acc;
+  }
+}
+}  // namespace
+
+void launch_rank_sum(const double* gathered, int world, size_t len, double* out, cudaStream_t s) {
+  const int blocks = static_cast<int>(std::min<size_t>(4096, (len + 255) / 256));
+  (note_launch(), rank_sum_kernel<<<blocks, 256, 0, s>>>(gathered, world, len, out));
 }
 
 void launch_finalize(const DeviceTargets& t, EvalBuffers& b, cudaStream_t s) {

@@ -20,7 +20,7 @@ void set_device(int device);
 
 // Attach an NCCL communicator: this process evaluates the atom shard
 // [rank's contiguous range) and evaluate_dual returns the global result on
-// every rank (one ncclAllReduce per evaluation).  `id` is 128 bytes from
+// every rank (one ncclAllGather + rank-ordered sum per evaluation).  `id` is 128 bytes from
 // unique_id() on rank 0, shipped to the other ranks out of band.
 void unique_id(unsigned char id[128]);
 void set_comm(int rank, int world, const unsigned char id[128]);

@@ -92,7 +92,10 @@ void launch_prologue(const DeviceTargets& t, EvalBuffers& b, double eps,
 void launch_dense(const DeviceAtoms& a, const DeviceTargets& t, EvalBuffers& b,
                   const DenseLaunch& plan, double eps, cudaStream_t s);
 
-// After the (optional) allreduce of b.res: g = res - nu, J -= sum psi nu.
+// out[i] = sum over r = 0..world-1 (in rank order) of gathered[r * len + i].
+void launch_rank_sum(const double* gathered, int world, size_t len, double* out, cudaStream_t s);
+
+// After the (optional) cross-rank sum of b.res: g = res - nu, J -= sum psi nu.
 void launch_finalize(const DeviceTargets& t, EvalBuffers& b, cudaStream_t s);
 
 // Deterministic fixed-order sum of x[0..n) into out[0] (two launches).

@@ -1,8 +1,9 @@
 """world_size-2 gloo test of the multi-GPU host logic on CPU.
 
 The B200 path shards atoms contiguously (rsot_cuda_shard_range), evaluates
-each shard, allreduces the packed partial buffer [g + nu | J + sum psi nu |
-D | pairs | empty | visited] and finalises once.  Here the
+each shard, all-gathers the packed partial buffers [g + nu | J + sum psi nu |
+D | pairs | empty | visited], sums them in rank order on every rank and
+finalises once.  Here the
 shard evaluation is the CPU oracle, the collective is gloo, and the
 result must equal the single-process evaluation."""
 import math
@@ -47,8 +48,11 @@ def _worker(rank, world, port, cutoff, q):
     buf = np.concatenate([part["gradient"] + W, [part["J"] + psinu, part["D"], part["candidate_pairs"],
                                                   part["empty_candidate_atoms"], part["atoms_visited"]]])
     t = torch.from_numpy(buf)
-    dist.all_reduce(t)
-    red = t.numpy()
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    red = parts[0].numpy().copy()
+    for r in range(1, world):  # rank order, as rank_sum_kernel
+        red += parts[r].numpy()
     n = len(W)
     g = red[:n] - W
     J = red[n] - psinu
@@ -56,12 +60,12 @@ def _worker(rank, world, port, cutoff, q):
     ok = (abs(J - full["J"]) <= 1e-12 * abs(full["J"]) and np.max(np.abs(g - full["gradient"])) <= 1e-14
           and abs(red[n + 1] - full["D"]) <= 1e-12 * full["D"] and int(red[n + 2]) == full["candidate_pairs"]
           and int(red[n + 3]) == full["empty_candidate_atoms"] and int(red[n + 4]) == len(A))
-    q.put((rank, bool(ok)))
+    q.put((rank, bool(ok), red.tobytes()))
     dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("cutoff", [math.inf, 0.01])
-def test_two_rank_shard_allreduce_matches_single(cutoff):
+def test_two_rank_shard_gather_sum_matches_single(cutoff):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -71,4 +75,5 @@ def test_two_rank_shard_allreduce_matches_single(cutoff):
     res = [q.get(timeout=300) for _ in procs]
     for p in procs:
         p.join(timeout=60)
-    assert sorted(res) == [(0, True), (1, True)]
+    assert sorted((r, ok) for r, ok, _ in res) == [(0, True), (1, True)]
+    assert res[0][2] == res[1][2]  # bitwise identical on every rank

@@ -286,3 +286,19 @@ def test_softmax_refine_cfg4_subsample(ctx):
     got = rs.softmax_refine(rs.TargetMeasure(dim=3, points=co.targets, weights=co.nu), cpsi, fine_pts,
                             rs.SourceAtoms(dim=3, points=sub.atoms, masses=sub.masses), 1e-3, cutoff=cut, ctx=ctx)
     assert np.max(np.abs(got - want)) <= 1e-10 * np.max(np.abs(want))
+
+
+def test_nccl_collective_path_single_rank():
+    """The multi-GPU reduction (ncclAllGather + rank-ordered sum, NCCL bound
+    with dlopen) on a 1-rank communicator: must reproduce the no-comm result
+    bit for bit, dense and truncated.  (Only one GPU is available here; the
+    2-rank host logic is tests/test_distributed.py.)"""
+    ctx1 = rs.Context(0)
+    ctx1.set_comm(0, 1, rs.Context.unique_id())
+    rng = np.random.default_rng(91)
+    A, M, T, W, psi = random_instance(rng, 3, 3000, 20000, 0.05)
+    for cutoff in (math.inf, 0.005):
+        a = gpu_eval(ctx1, A, M, T, W, psi, 0.01, cutoff)
+        b = gpu_eval(rs.Context.default(0), A, M, T, W, psi, 0.01, cutoff)
+        assert a["J"] == b["J"] and a["D"] == b["D"] and a["candidate_pairs"] == b["candidate_pairs"]
+        assert np.array_equal(a["gradient"], b["gradient"])

@@ -128,6 +128,19 @@ int rsot_cuda_eval_device(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
                           double* d_scalars);
 int rsot_cuda_check_status(rsot_cuda_ctx* ctx);
 
+/* rsot_cuda_eval with the reference's CostKind (cost.hpp:17):
+ * RSOT_CUDA_COST_SQEUCLIDEAN (c = |x-y|^2/2, the evaluator above) or
+ * RSOT_CUDA_COST_SQGEODESIC (c = acos(clamp(x.y, -1, 1))^2 on the unit
+ * sphere; a finite cutoff selects {j : c < cutoff} by a full scan and an
+ * empty set falls back to the Euclidean nearest target, evaluate.cpp:
+ * 119-133; fp64 acos/exp per pair, for the blue-noise application). */
+#define RSOT_CUDA_COST_SQEUCLIDEAN 0
+#define RSOT_CUDA_COST_SQGEODESIC 1
+int rsot_cuda_eval_cost(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
+                        rsot_cuda_targets* targets, const double* psi, double eps,
+                        double cutoff, int cost_kind, double* g_out,
+                        rsot_cuda_scalars* out);
+
 /* Parity/debug variant of rsot_cuda_eval that also returns, for this rank's
  * atoms, the candidate-set size (1 for empty-fallback atoms), the wrapping
  * sum of splitmix64(j) over the candidate set, and ln S_q.  Any of the three
@@ -137,6 +150,12 @@ int rsot_cuda_eval_debug(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
                          double eps, double cutoff, double* g_out,
                          rsot_cuda_scalars* out, uint32_t* cand_count,
                          uint64_t* cand_hash, double* log_s);
+/* rsot_cuda_eval_debug with a cost kind (RSOT_CUDA_COST_*). */
+int rsot_cuda_eval_debug_cost(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
+                              rsot_cuda_targets* targets, const double* psi, double eps,
+                              double cutoff, int cost_kind, double* g_out,
+                              rsot_cuda_scalars* out, uint32_t* cand_count,
+                              uint64_t* cand_hash, double* log_s);
 
 /* ---- spatial queries (SpatialIndex / covering_cost) ----------------------
  * nearest target for m host points (lowest index on ties,
@@ -165,7 +184,9 @@ int rsot_cuda_softmax_refine(rsot_cuda_ctx* ctx, rsot_cuda_targets* coarse,
  * rsot_cuda_plan_candidates: the PlanView ctor's candidate sets (plan.cpp:
  *   37-46): idx_out[offsets[q] .. offsets[q+1]) receives atom q's ascending
  *   candidate list (all targets for cutoff = +inf; the ball query of radius
- *   sqrt(2 cutoff), or the nearest target when it is empty).  offsets[nq+1]
+ *   sqrt(2 cutoff) -- a full scan {j : c < cutoff} for the geodesic cost --
+ *   or the nearest target when it is empty).  cost_kind: RSOT_CUDA_COST_*.
+ *   offsets[nq+1]
  *   is the prefix sum of the per-atom counts (rsot_cuda_eval_debug's
  *   cand_count for the same cutoff).
  * rsot_cuda_plan_moments: with log_s = the ctor's log_S_q (rsot_cuda_eval_debug
@@ -177,11 +198,11 @@ int rsot_cuda_softmax_refine(rsot_cuda_ctx* ctx, rsot_cuda_targets* coarse,
  *   modal_out[nq], lowest index on ties).  Outputs may be NULL.  Sums are
  *   order independent (fixed point), so results are bitwise reproducible. */
 int rsot_cuda_plan_candidates(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
-                              rsot_cuda_targets* targets, double cutoff,
+                              rsot_cuda_targets* targets, double cutoff, int cost_kind,
                               const uint64_t* offsets, uint64_t* idx_out);
 int rsot_cuda_plan_moments(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
                            rsot_cuda_targets* targets, const double* psi, double eps,
-                           const double* log_s, const uint64_t* offsets,
+                           int cost_kind, const double* log_s, const uint64_t* offsets,
                            const uint64_t* idx, double* marginal_out, double* moment_out,
                            double* map_out, uint64_t* modal_out);
 

@@ -65,6 +65,10 @@ class COracle:
         L.oracle_softmax_refine.restype = c_int
         L.oracle_softmax_refine.argtypes = [c_size_t, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p,
                                             c_size_t, c_void_p, c_void_p, c_double, c_double, c_void_p]
+        L.oracle_evaluate_dual_geodesic.restype = c_int
+        L.oracle_evaluate_dual_geodesic.argtypes = [c_size_t, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p,
+                                                    c_void_p, c_double, c_double, c_void_p, POINTER(Scalars),
+                                                    c_void_p, c_void_p]
         L.oracle_plan_view.restype = c_int
         L.oracle_plan_view.argtypes = [c_size_t, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p, c_void_p,
                                        c_double, c_double] + [c_void_p] * 8
@@ -115,6 +119,27 @@ class COracle:
                                           _p(am), float(eps), float(cutoff), _p(out))
         if rc != 0:
             raise ValueError(self.L.oracle_last_error().decode())
+        return out
+
+    def evaluate_dual_geodesic(self, atoms, masses, targets, nu, psi, eps, cutoff=math.inf,
+                               per_atom=False):
+        atoms, targets = _pts(atoms), _pts(targets)
+        masses = np.ascontiguousarray(masses, dtype=np.float64)
+        nu = np.ascontiguousarray(nu, dtype=np.float64)
+        psi = np.ascontiguousarray(psi, dtype=np.float64)
+        g = np.empty(len(targets))
+        sc = Scalars()
+        cnt = np.zeros(len(atoms), dtype=np.uint32) if per_atom else None
+        logs = np.zeros(len(atoms)) if per_atom else None
+        rc = self.L.oracle_evaluate_dual_geodesic(len(atoms), _p(atoms), _p(masses), len(targets), _p(targets),
+                                                  _p(nu), _p(psi), float(eps), float(cutoff), _p(g),
+                                                  ctypes.byref(sc), _p(cnt), _p(logs))
+        if rc != 0:
+            raise ValueError(self.L.oracle_last_error().decode())
+        out = dict(J=sc.J, D=sc.D, gradient=g, atoms_visited=sc.atoms_visited,
+                   candidate_pairs=sc.candidate_pairs, empty_candidate_atoms=sc.empty_candidate_atoms)
+        if per_atom:
+            out.update(count=cnt, log_s=logs)
         return out
 
     def plan_view(self, atoms, masses, targets, nu, psi, eps, cutoff=math.inf):
@@ -192,6 +217,9 @@ class RefLib:
                                          c_void_p]
         L.ref_covering_cost.restype = c_int
         L.ref_covering_cost.argtypes = [c_void_p, POINTER(c_double)]
+        L.ref_evaluate_dual_kind.restype = c_int
+        L.ref_evaluate_dual_kind.argtypes = [c_void_p, c_void_p, c_size_t, c_double, c_double, c_int, c_void_p,
+                                             POINTER(Scalars)]
         L.ref_plan_view.restype = c_int
         L.ref_plan_view.argtypes = [c_void_p, c_void_p, c_double, c_double] + [c_void_p] * 6
         self.L = L
@@ -233,6 +261,17 @@ class RefProblem:
         if rc != 0:
             raise ValueError(self.lib.L.ref_last_error().decode())
         return out
+
+    def evaluate_dual_geodesic(self, psi, eps, cutoff=math.inf):
+        psi = np.ascontiguousarray(psi, dtype=np.float64)
+        g = np.empty(len(self.targets))
+        sc = Scalars()
+        rc = self.lib.L.ref_evaluate_dual_kind(self.h, _p(psi), len(psi), float(eps), float(cutoff), 1, _p(g),
+                                               ctypes.byref(sc))
+        if rc != 0:
+            raise ValueError(self.lib.L.ref_last_error().decode())
+        return dict(J=sc.J, D=sc.D, gradient=g, atoms_visited=sc.atoms_visited,
+                    candidate_pairs=sc.candidate_pairs, empty_candidate_atoms=sc.empty_candidate_atoms)
 
     def plan_view(self, psi, eps, cutoff=math.inf):
         psi = np.ascontiguousarray(psi, dtype=np.float64)

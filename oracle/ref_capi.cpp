@@ -105,6 +105,37 @@ int ref_evaluate_dual(void* prob, const double* psi, size_t n, double eps,
   }
 }
 
+// rsot::evaluate_dual with cfg.cost_kind = kind (0 SqEuclidean, 1
+// SqGeodesicSphere), single worker.
+int ref_evaluate_dual_kind(void* prob, const double* psi, size_t n, double eps, double cutoff,
+                           int kind, double* g_out, ref_scalars* out) {
+  auto* p = static_cast<RefProblem*>(prob);
+  try {
+    rsot::SolverConfig cfg;
+    cfg.epsilon = eps;
+    cfg.workers = 1;
+    cfg.cost_kind = kind ? rsot::CostKind::SqGeodesicSphere : rsot::CostKind::SqEuclidean;
+    rsot::TruncationState trunc;
+    trunc.set_weight_stats(p->target.weights);
+    trunc.cutoff = cutoff;
+    rsot::DualPotential pot{std::vector<double>(psi, psi + n), rsot::Gauge::Raw};
+    const rsot::EvalResult r = rsot::evaluate_dual(p->atoms, p->target, pot, cfg, trunc, *p->index);
+    std::memcpy(g_out, r.gradient.data(), sizeof(double) * r.gradient.size());
+    out->J = r.J;
+    out->D = r.D;
+    out->atoms_visited = r.atoms_visited;
+    out->candidate_pairs = r.candidate_pairs;
+    out->empty_candidate_atoms = r.empty_candidate_atoms;
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return -1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -2;
+  }
+}
+
 // rsot::covering_cost (spatial_index.cpp:101-121 semantics).
 int ref_covering_cost(void* prob, double* out) {
   auto* p = static_cast<RefProblem*>(prob);

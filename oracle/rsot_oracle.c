@@ -671,3 +671,79 @@ int oracle_plan_view(size_t nq, const double* ax, const double* am, size_t n,
   oracle_grid_destroy(grid);
   return ORACLE_OK;
 }
+
+/* ---- evaluate_dual for CostKind::SqGeodesicSphere ------------------------
+ * evaluate.cpp:86-174 with cost.hpp:19-33: c = acos(clamp(x.y, -1, 1))^2,
+ * a finite cutoff selects {j : c < cutoff} by a full scan (:124-128; no ball
+ * radius for this cost), an empty set takes index.nearest (Euclidean, lowest
+ * index on ties, :129-132).  Single worker (the reference's workers = 1). */
+static double geo_cost(const double* x, const double* y) {
+  const double d = (x[0] * y[0] + x[1] * y[1]) + x[2] * y[2];
+  const double t = d < -1.0 ? -1.0 : (1.0 < d ? 1.0 : d);
+  const double g = acos(t);
+  return g * g;
+}
+
+int oracle_evaluate_dual_geodesic(size_t nq, const double* ax, const double* am, size_t n,
+                                  const double* ty, const double* nu, const double* psi,
+                                  double eps, double cutoff, double* g_out,
+                                  oracle_scalars* out, uint32_t* cnt, double* log_s) {
+  for (size_t j = 0; j < n; ++j)
+    if (!isfinite(psi[j])) {
+      g_last_error = "potential has non-finite entries";
+      return ORACLE_INVALID_ARGUMENT;
+    }
+  oracle_grid* grid = oracle_grid_create(ty, n);
+  if (!grid) return ORACLE_INVALID_ARGUMENT;
+  const int truncated = isfinite(cutoff);
+  double* log_nu = (double*)malloc(sizeof(double) * (n ? n : 1));
+  for (size_t j = 0; j < n; ++j) log_nu[j] = log(nu[j]);
+  uint64_t* cand = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));
+  double* expo = (double*)malloc(sizeof(double) * (n ? n : 1));
+  double J = 0.0, D = 0.0;
+  uint64_t pairs = 0, empty = 0;
+  for (size_t j = 0; j < n; ++j) g_out[j] = 0.0;
+  for (size_t q = 0; q < nq; ++q) {
+    const double* x = ax + 3 * q;
+    size_t nc = 0;
+    for (size_t j = 0; j < n; ++j)
+      if (!truncated || geo_cost(x, ty + 3 * j) < cutoff) cand[nc++] = j;
+    if (nc == 0) {
+      ++empty;
+      cand[nc++] = oracle_grid_nearest(grid, x);
+    }
+    pairs += nc;
+    double emax = -INFINITY;
+    for (size_t i = 0; i < nc; ++i) {
+      const uint64_t j = cand[i];
+      expo[i] = (psi[j] - geo_cost(x, ty + 3 * j)) / eps + log_nu[j];
+      emax = (emax < expo[i]) ? expo[i] : emax;
+    }
+    double sum = 0.0;
+    for (size_t i = 0; i < nc; ++i) {
+      expo[i] = exp(expo[i] - emax);
+      sum += expo[i];
+    }
+    const double lS = emax + log(sum);
+    J += eps * lS * am[q];
+    D += am[q] * exp(-lS);
+    const double scale = am[q] / sum;
+    for (size_t i = 0; i < nc; ++i) g_out[cand[i]] += expo[i] * scale;
+    if (cnt) cnt[q] = (uint32_t)nc;
+    if (log_s) log_s[q] = lS;
+  }
+  for (size_t j = 0; j < n; ++j) {
+    J -= psi[j] * nu[j];
+    g_out[j] -= nu[j];
+  }
+  out->J = J;
+  out->D = D;
+  out->candidate_pairs = pairs;
+  out->empty_candidate_atoms = empty;
+  out->atoms_visited = nq;
+  free(log_nu);
+  free(cand);
+  free(expo);
+  oracle_grid_destroy(grid);
+  return ORACLE_OK;
+}

@@ -105,6 +105,15 @@ int oracle_plan_view(size_t nq, const double* atom_xyz, const double* atom_mass,
                      double* bary_out, double* map_out, uint64_t* modal_out,
                      int64_t* starved_out);
 
+/* rsot::evaluate_dual for CostKind::SqGeodesicSphere (points on the unit
+ * sphere), single worker: full-scan truncation c < cutoff, Euclidean nearest
+ * for empty sets (evaluate.cpp:119-133, cost.hpp:19-33).  cand_count and
+ * log_s may be NULL. */
+int oracle_evaluate_dual_geodesic(size_t nq, const double* atom_xyz, const double* atom_mass,
+                                  size_t n, const double* target_xyz, const double* target_nu,
+                                  const double* psi, double eps, double cutoff, double* g_out,
+                                  oracle_scalars* out, uint32_t* cand_count, double* log_s);
+
 /* rsot::softmax_refine (proj/src/solve.cpp:62-142), SqEuclidean, single
  * worker: psi_out[n_fine] from the coarse potential.  Returns
  * ORACLE_INVALID_ARGUMENT on non-finite input or output (require_finite). */

@@ -62,9 +62,13 @@ _SIGNATURES = [
      [c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p, c_double, c_double, c_void_p]),
     ("rsot_cuda_ctx_set_timing", c_int, [c_void_p, c_int]),
     ("rsot_cuda_ctx_set_precision", c_int, [c_void_p, c_int]),
-    ("rsot_cuda_plan_candidates", c_int, [c_void_p, c_void_p, c_void_p, c_double, c_void_p, c_void_p]),
-    ("rsot_cuda_plan_moments", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_void_p, c_void_p,
-                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("rsot_cuda_eval_cost", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_int, c_void_p,
+                                    POINTER(RsotCudaScalars)]),
+    ("rsot_cuda_plan_candidates", c_int, [c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p, c_void_p]),
+    ("rsot_cuda_plan_moments", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p,
+                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("rsot_cuda_eval_debug_cost", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_int,
+                                          c_void_p, POINTER(RsotCudaScalars), c_void_p, c_void_p, c_void_p]),
     ("rsot_cuda_last_kernel_ms", c_int, [c_void_p, POINTER(c_double), POINTER(c_double), POINTER(c_double)]),
     ("rsot_cuda_measure_fp64_peak", c_int, [c_void_p, POINTER(c_double)]),
     ("rsot_cuda_kernel_launches", c_uint64, []),

@@ -20,6 +20,7 @@
 
 #include "../../include/rsot_cuda.h"
 #include "kernels.cuh"
+#include "geodesic.cuh"
 #include "refine.cuh"
 #include "truncated.cuh"
 
@@ -111,6 +112,7 @@ struct rsot_cuda_ctx {
   DevBuf<int> flagged;
   TruncWorkspace trunc;
   RefineWorkspace refine;
+  GeoWorkspace geo;
   double* h_pinned = nullptr;  // small pinned staging for scalars
   bool timing = false;
   int precision = RSOT_CUDA_PRECISION_FP64;
@@ -194,13 +196,19 @@ EvalBuffers buffers(rsot_cuda_ctx* c, double* g_out, double* scalars_out) {
 // Enqueues one evaluation reading psi from b.psi (device) and leaving the
 // final gradient / scalars in b.g_out / b.scalars_out.
 int enqueue_eval(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
-                 EvalBuffers& b, double eps, double cutoff, DebugOut* dbg) {
+                 EvalBuffers& b, double eps, double cutoff, DebugOut* dbg,
+                 int cost = RSOT_CUDA_COST_SQEUCLIDEAN) {
   const cudaStream_t s = c->stream;
   const DeviceTargets dt = make_dt(t);
   DeviceAtoms da{a->x, static_cast<int>(a->nq)};
   if (b.timing) cudaEventRecord(b.timing[0], s);
   launch_prologue(dt, b, eps, s);
-  if (std::isfinite(cutoff)) {
+  if (cost == RSOT_CUDA_COST_SQGEODESIC) {
+    const int rc = run_geodesic(c->geo, da, dt, b, eps, cutoff, s, g_last_error,
+                                dbg ? dbg->count : nullptr, dbg ? dbg->hash : nullptr,
+                                dbg ? dbg->log_s : nullptr);
+    if (rc != 0) return fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error);
+  } else if (std::isfinite(cutoff)) {
     const int rc = run_truncated(c->trunc, da, a->cells, dt, t->cells, b, eps,
                                  cutoff, c->num_sms, dbg, s, g_last_error,
                                  c->precision == RSOT_CUDA_PRECISION_FP32);
@@ -317,6 +325,7 @@ int rsot_cuda_ctx_destroy(rsot_cuda_ctx* c) {
   c->scalars_out.release(); c->flagged.release(); c->gathered.release();
   c->trunc.release();
   c->refine.release();
+  c->geo.release();
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
@@ -481,7 +490,7 @@ size_t rsot_cuda_atoms_size(const rsot_cuda_atoms* a) { return a ? a->nq : 0; }
 static int eval_common(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
                        const double* psi_host, const double* psi_dev, double eps,
                        double cutoff, double* g_dev, double* scal_dev,
-                       DebugOut* dbg) {
+                       DebugOut* dbg, int cost = RSOT_CUDA_COST_SQEUCLIDEAN) {
   if (!(eps > 0.0)) return fail(RSOT_CUDA_INVALID_ARGUMENT, "epsilon must be > 0");
   if (std::isnan(cutoff)) cutoff = INFINITY;  // isfinite(NaN) is false: dense
   const DenseLaunch plan = plan_dense(static_cast<int>(a->nq), static_cast<int>(t->n), c->num_sms);
@@ -493,7 +502,7 @@ static int eval_common(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* 
                             cudaMemcpyHostToDevice, c->stream));
   else
     b.psi = const_cast<double*>(psi_dev);
-  return enqueue_eval(c, a, t, b, eps, cutoff, dbg);
+  return enqueue_eval(c, a, t, b, eps, cutoff, dbg, cost);
 }
 
 int rsot_cuda_eval(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
@@ -503,6 +512,19 @@ int rsot_cuda_eval(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
   if (rc) return rc;
   if (!psi || !g_out || !out) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
   rc = eval_common(c, a, t, psi, nullptr, eps, cutoff, nullptr, nullptr, nullptr);
+  if (rc) return rc;
+  return finish_host_eval(c, t, g_out, out);
+}
+
+int rsot_cuda_eval_cost(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
+                        const double* psi, double eps, double cutoff, int cost_kind,
+                        double* g_out, rsot_cuda_scalars* out) {
+  int rc = check_ready(c, a, t);
+  if (rc) return rc;
+  if (!psi || !g_out || !out) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  if (cost_kind != RSOT_CUDA_COST_SQEUCLIDEAN && cost_kind != RSOT_CUDA_COST_SQGEODESIC)
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "unknown cost kind");
+  rc = eval_common(c, a, t, psi, nullptr, eps, cutoff, nullptr, nullptr, nullptr, cost_kind);
   if (rc) return rc;
   return finish_host_eval(c, t, g_out, out);
 }
@@ -532,15 +554,25 @@ int rsot_cuda_eval_debug(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets
                          const double* psi, double eps, double cutoff, double* g_out,
                          rsot_cuda_scalars* out, uint32_t* cand_count,
                          uint64_t* cand_hash, double* log_s) {
+  return rsot_cuda_eval_debug_cost(c, a, t, psi, eps, cutoff, RSOT_CUDA_COST_SQEUCLIDEAN, g_out,
+                                   out, cand_count, cand_hash, log_s);
+}
+
+int rsot_cuda_eval_debug_cost(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
+                              const double* psi, double eps, double cutoff, int cost_kind,
+                              double* g_out, rsot_cuda_scalars* out, uint32_t* cand_count,
+                              uint64_t* cand_hash, double* log_s) {
   int rc = check_ready(c, a, t);
   if (rc) return rc;
   if (!psi || !g_out || !out) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  if (cost_kind != RSOT_CUDA_COST_SQEUCLIDEAN && cost_kind != RSOT_CUDA_COST_SQGEODESIC)
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "unknown cost kind");
   DebugOut dbg;
   const size_t nq = a->nq ? a->nq : 1;
   RSOT_CK(cudaMalloc(&dbg.count, sizeof(uint32_t) * nq));
   RSOT_CK(cudaMalloc(&dbg.hash, sizeof(uint64_t) * nq));
   RSOT_CK(cudaMalloc(&dbg.log_s, sizeof(double) * nq));
-  rc = eval_common(c, a, t, psi, nullptr, eps, cutoff, nullptr, nullptr, &dbg);
+  rc = eval_common(c, a, t, psi, nullptr, eps, cutoff, nullptr, nullptr, &dbg, cost_kind);
   if (rc == 0) rc = finish_host_eval(c, t, g_out, out);
   if (rc == 0 && a->nq) {
     if (cand_count)
@@ -625,9 +657,12 @@ int rsot_cuda_softmax_refine(rsot_cuda_ctx* c, rsot_cuda_targets* coarse,
 }
 
 int rsot_cuda_plan_candidates(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
-                              double cutoff, const uint64_t* offsets, uint64_t* idx_out) {
+                              double cutoff, int cost_kind, const uint64_t* offsets,
+                              uint64_t* idx_out) {
   int rc = check_ready(c, a, t);
   if (rc) return rc;
+  if (cost_kind != RSOT_CUDA_COST_SQEUCLIDEAN && cost_kind != RSOT_CUDA_COST_SQGEODESIC)
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "unknown cost kind");
   if (!offsets || (a->nq && offsets[a->nq] && !idx_out))
     return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
   if (std::isnan(cutoff)) return fail(RSOT_CUDA_INVALID_ARGUMENT, "cutoff is NaN");
@@ -640,12 +675,13 @@ int rsot_cuda_plan_candidates(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_ta
     return RSOT_CUDA_OK;
   }
   rc = run_plan_candidates(c->trunc, DeviceAtoms{a->x, static_cast<int>(a->nq)}, make_dt(t),
-                           t->cells, cutoff, offsets, idx_out, c->stream, g_last_error);
+                           t->cells, cutoff, cost_kind == RSOT_CUDA_COST_SQGEODESIC, offsets,
+                           idx_out, c->stream, g_last_error);
   return rc ? fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error) : RSOT_CUDA_OK;
 }
 
 int rsot_cuda_plan_moments(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
-                           const double* psi, double eps, const double* log_s,
+                           const double* psi, double eps, int cost_kind, const double* log_s,
                            const uint64_t* offsets, const uint64_t* idx, double* marginal_out,
                            double* moment_out, double* map_out, uint64_t* modal_out) {
   int rc = check_ready(c, a, t);
@@ -653,13 +689,16 @@ int rsot_cuda_plan_moments(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targe
   if (!psi || (a->nq && !log_s) || (offsets && offsets[a->nq] && !idx))
     return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
   if (!(eps > 0.0)) return fail(RSOT_CUDA_INVALID_ARGUMENT, "epsilon must be > 0");
+  if (cost_kind != RSOT_CUDA_COST_SQEUCLIDEAN && cost_kind != RSOT_CUDA_COST_SQGEODESIC)
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "unknown cost kind");
   for (size_t j = 0; j < t->n; ++j)
     if (!std::isfinite(psi[j]))
       return fail(RSOT_CUDA_INVALID_ARGUMENT, "potential has non-finite entries");
   if (offsets && idx)
     for (uint64_t k = 0; k < offsets[a->nq]; ++k)
       if (idx[k] >= t->n) return fail(RSOT_CUDA_INVALID_ARGUMENT, "candidate index out of range");
-  rc = run_plan_moments(DeviceAtoms{a->x, static_cast<int>(a->nq)}, make_dt(t), psi, eps, log_s,
+  rc = run_plan_moments(DeviceAtoms{a->x, static_cast<int>(a->nq)}, make_dt(t), psi, eps,
+                        cost_kind == RSOT_CUDA_COST_SQGEODESIC, log_s,
                         offsets, idx, a->cells.bbox_lo, marginal_out, moment_out, map_out,
                         modal_out, c->stream, g_last_error);
   return rc ? fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error) : RSOT_CUDA_OK;

@@ -160,4 +160,58 @@ __device__ __forceinline__ uint64_t candidate_hash_term(uint64_t j) {
   return z ^ (z >> 31);
 }
 
+// 192-bit fixed point (scale 2^150) accumulation of a non-negative double.
+__device__ inline void fp_add(unsigned long long* acc, double m) {
+  if (!(m > 0.0)) return;
+  int e;
+  const double fr = frexp(m, &e);                   // m = fr * 2^e, fr in [0.5,1)
+  const unsigned long long mant = static_cast<unsigned long long>(ldexp(fr, 53));
+  const int sh = e - 53 + 150;                       // value = mant * 2^sh
+  unsigned long long l0 = 0, l1 = 0, l2 = 0;
+  if (sh < 0) {
+    if (sh > -64) l0 = mant >> (-sh);
+  } else {
+    const int w = sh >> 6, b = sh & 63;
+    const unsigned long long lo = mant << b;
+    const unsigned long long hi = b ? (mant >> (64 - b)) : 0ull;
+    if (w == 0) { l0 = lo; l1 = hi; }
+    else if (w == 1) { l1 = lo; l2 = hi; }
+    else if (w == 2) { l2 = lo; }
+  }
+  unsigned long long carry = 0;
+  {
+    if (l0) {
+      const unsigned long long old = atomicAdd(&acc[0], l0);
+      carry = (old + l0 < old) ? 1ull : 0ull;
+    }
+  }
+  {
+    const unsigned long long add = l1 + carry;
+    const unsigned long long c1 = (add < l1) ? 1ull : 0ull;
+    carry = c1;
+    if (add) {
+      const unsigned long long old = atomicAdd(&acc[1], add);
+      carry += (old + add < old) ? 1ull : 0ull;
+    }
+  }
+  {
+    const unsigned long long add = l2 + carry;
+    if (add) atomicAdd(&acc[2], add);
+  }
+}
+
+__device__ inline double fp_to_double(const unsigned long long* acc) {
+  return (static_cast<double>(acc[2]) * 0x1p-22 + static_cast<double>(acc[1]) * 0x1p-86) +
+         static_cast<double>(acc[0]) * 0x1p-150;
+}
+
+// cost.hpp:19-33: dot(p, q) = (p0 q0 + p1 q1) + p2 q2, clamp, acos, square.
+__device__ __forceinline__ double geo_cost(double x0, double x1, double x2, double y0, double y1,
+                                           double y2) {
+  const double d = __dadd_rn(__dadd_rn(__dmul_rn(x0, y0), __dmul_rn(x1, y1)), __dmul_rn(x2, y2));
+  const double t = d < -1.0 ? -1.0 : (1.0 < d ? 1.0 : d);
+  const double g = acos(t);
+  return __dmul_rn(g, g);
+}
+
 }  // namespace rsot_cuda

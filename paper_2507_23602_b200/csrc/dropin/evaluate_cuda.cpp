@@ -227,9 +227,6 @@ EvalResult evaluate_dual(const SourceAtoms& atoms, const TargetMeasure& target,
   if (psi.size() != n_targets)
     throw std::invalid_argument("evaluate_dual: psi length != target count");
   require_finite(psi.values);
-  if (cfg.cost_kind != CostKind::SqEuclidean)
-    throw std::invalid_argument(
-        "evaluate_dual (B200): SqGeodesicSphere is out of scope for the GPU evaluator");
   if (atoms.masses.size() != atoms.points.size())
     throw std::invalid_argument("evaluate_dual: atom mass/point size mismatch");
 
@@ -240,8 +237,11 @@ EvalResult evaluate_dual(const SourceAtoms& atoms, const TargetMeasure& target,
   EvalResult result;
   result.gradient.assign(n_targets, 0.0);
   rsot_cuda_scalars sc{};
-  const int rc = rsot_cuda_eval(st.context(), da, dt, psi.values.data(), cfg.epsilon, trunc.cutoff,
-                                result.gradient.data(), &sc);
+  // cost.hpp:17: SqGeodesicSphere runs the full-scan geodesic kernels
+  const int kind = cfg.cost_kind == CostKind::SqGeodesicSphere ? RSOT_CUDA_COST_SQGEODESIC
+                                                               : RSOT_CUDA_COST_SQEUCLIDEAN;
+  const int rc = rsot_cuda_eval_cost(st.context(), da, dt, psi.values.data(), cfg.epsilon,
+                                     trunc.cutoff, kind, result.gradient.data(), &sc);
   if (rc) cuda_detail::raise(rc, "rsot_cuda_eval");
   result.J = sc.J;
   result.D = sc.D;
@@ -326,7 +326,7 @@ double covering_cost_device(const SourceAtoms& atoms, const TargetMeasure& targe
 // ---- PlanView building blocks (plan_cuda.cpp) -------------------------------
 
 void plan_build_device(const SourceAtoms& atoms, const TargetMeasure& target,
-                       const std::vector<double>& psi, double eps, double cutoff,
+                       const std::vector<double>& psi, double eps, double cutoff, bool geodesic,
                        std::vector<double>& log_S,
                        std::vector<std::vector<std::size_t>>& candidates) {
   auto& st = cuda_detail::state();
@@ -338,13 +338,14 @@ void plan_build_device(const SourceAtoms& atoms, const TargetMeasure& target,
   std::vector<uint32_t> count(nq);
   std::vector<double> g(n);
   rsot_cuda_scalars sc{};
-  int rc = rsot_cuda_eval_debug(st.context(), da, dt, psi.data(), eps, cutoff, g.data(), &sc,
-                                count.data(), nullptr, log_S.data());
+  const int kind = geodesic ? RSOT_CUDA_COST_SQGEODESIC : RSOT_CUDA_COST_SQEUCLIDEAN;
+  int rc = rsot_cuda_eval_debug_cost(st.context(), da, dt, psi.data(), eps, cutoff, kind, g.data(),
+                                     &sc, count.data(), nullptr, log_S.data());
   if (rc) cuda_detail::raise(rc, "PlanView (B200 drop-in)");
   std::vector<uint64_t> off(nq + 1, 0);
   for (std::size_t q = 0; q < nq; ++q) off[q + 1] = off[q] + count[q];
   std::vector<uint64_t> idx(std::max<uint64_t>(off[nq], 1));
-  rc = rsot_cuda_plan_candidates(st.context(), da, dt, cutoff, off.data(), idx.data());
+  rc = rsot_cuda_plan_candidates(st.context(), da, dt, cutoff, kind, off.data(), idx.data());
   if (rc) cuda_detail::raise(rc, "PlanView (B200 drop-in)");
   candidates.assign(nq, {});
   for (std::size_t q = 0; q < nq; ++q)
@@ -353,7 +354,7 @@ void plan_build_device(const SourceAtoms& atoms, const TargetMeasure& target,
 }
 
 void plan_moments_device(const SourceAtoms& atoms, const TargetMeasure& target,
-                         const std::vector<double>& psi, double eps,
+                         const std::vector<double>& psi, double eps, bool geodesic,
                          const std::vector<double>& log_S,
                          const std::vector<std::vector<std::size_t>>& candidates,
                          double* marginal, double* moment, double* map, std::uint64_t* modal) {
@@ -373,7 +374,9 @@ void plan_moments_device(const SourceAtoms& atoms, const TargetMeasure& target,
     for (const auto& c : candidates) idx.insert(idx.end(), c.begin(), c.end());
     if (idx.empty()) idx.push_back(0);
   }
-  const int rc = rsot_cuda_plan_moments(st.context(), da, dt, psi.data(), eps, log_S.data(),
+  const int rc = rsot_cuda_plan_moments(st.context(), da, dt, psi.data(), eps,
+                                        geodesic ? RSOT_CUDA_COST_SQGEODESIC : RSOT_CUDA_COST_SQEUCLIDEAN,
+                                        log_S.data(),
                                         dense ? nullptr : off.data(), dense ? nullptr : idx.data(),
                                         marginal, moment, map, modal);
   if (rc) cuda_detail::raise(rc, "PlanView (B200 drop-in)");

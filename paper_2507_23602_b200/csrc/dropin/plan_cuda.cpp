@@ -10,8 +10,8 @@
 // The per-atom / per-target accessors (plan_density, conditional_density,
 // conditional_barycenter) and the pointwise helpers (displacement_interpolate,
 // transfer_field) are cheap queries over the cached sets and stay host code
-// with the reference's semantics.  Only the squared Euclidean cost runs on
-// the GPU; the geodesic (blue-noise) cost is out of scope and rejected.
+// with the reference's semantics.  Both cost kinds run on the GPU (the
+// geodesic one by full scans, as the reference).
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -48,9 +48,8 @@ PlanView::PlanView(const SourceAtoms& atoms, const TargetMeasure& target,
     throw std::invalid_argument("plan view: psi length != target count");
   require_finite(psi_);
   if (target_.points.empty()) throw std::invalid_argument("spatial index: empty point set");
-  if (kind_ != CostKind::SqEuclidean)
-    throw std::invalid_argument("PlanView (B200): SqGeodesicSphere is out of scope for the GPU path");
-  cuda::plan_build_device(atoms_, target_, psi_, eps_, cutoff, log_S_, candidates_);
+  cuda::plan_build_device(atoms_, target_, psi_, eps_, cutoff, kind_ == CostKind::SqGeodesicSphere,
+                          log_S_, candidates_);
 }
 
 void PlanView::set_convergence(double grad_l1, double delta_tol) {
@@ -67,8 +66,8 @@ std::vector<std::pair<std::size_t, double>> PlanView::plan_density(std::size_t q
 
 std::vector<double> PlanView::target_marginals() const {
   std::vector<double> marg(target_.size(), 0.0);
-  cuda::plan_moments_device(atoms_, target_, psi_, eps_, log_S_, candidates_, marg.data(), nullptr,
-                            nullptr, nullptr);
+  cuda::plan_moments_device(atoms_, target_, psi_, eps_, kind_ == CostKind::SqGeodesicSphere, log_S_,
+                            candidates_, marg.data(), nullptr, nullptr, nullptr);
   return marg;
 }
 
@@ -102,8 +101,8 @@ Point PlanView::conditional_barycenter(std::size_t j) const {
 PointList PlanView::all_conditional_barycenters() const {
   const std::size_t n = target_.size();
   std::vector<double> tilde(n), moment(3 * n);
-  cuda::plan_moments_device(atoms_, target_, psi_, eps_, log_S_, candidates_, tilde.data(),
-                            moment.data(), nullptr, nullptr);
+  cuda::plan_moments_device(atoms_, target_, psi_, eps_, kind_ == CostKind::SqGeodesicSphere, log_S_,
+                            candidates_, tilde.data(), moment.data(), nullptr, nullptr);
   PointList out(n);
   for (std::size_t j = 0; j < n; ++j) {
     if (tilde[j] < 1e-30) starved(j);
@@ -118,7 +117,8 @@ PointList PlanView::all_conditional_barycenters() const {
 struct MapBuilder {
   static void moments(const PlanView& p, double* marginal, double* moment, double* map,
                       std::uint64_t* modal) {
-    cuda::plan_moments_device(p.atoms_, p.target_, p.psi_, p.eps_, p.log_S_, p.candidates_,
+    cuda::plan_moments_device(p.atoms_, p.target_, p.psi_, p.eps_,
+                              p.kind_ == CostKind::SqGeodesicSphere, p.log_S_, p.candidates_,
                               marginal, moment, map, modal);
   }
 };

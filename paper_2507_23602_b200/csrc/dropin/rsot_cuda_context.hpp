@@ -42,11 +42,11 @@ std::uint64_t kernel_launches();
 //     moments (3n), barycentric images (3 nq) and modal targets (nq); any
 //     output may be null.
 void plan_build_device(const SourceAtoms& atoms, const TargetMeasure& target,
-                       const std::vector<double>& psi, double eps, double cutoff,
+                       const std::vector<double>& psi, double eps, double cutoff, bool geodesic,
                        std::vector<double>& log_S,
                        std::vector<std::vector<std::size_t>>& candidates);
 void plan_moments_device(const SourceAtoms& atoms, const TargetMeasure& target,
-                         const std::vector<double>& psi, double eps,
+                         const std::vector<double>& psi, double eps, bool geodesic,
                          const std::vector<double>& log_S,
                          const std::vector<std::vector<std::size_t>>& candidates,
                          double* marginal, double* moment, double* map, std::uint64_t* modal);

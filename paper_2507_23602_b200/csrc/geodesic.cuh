@@ -1,0 +1,34 @@
+// geodesic.cuh -- evaluate_dual for CostKind::SqGeodesicSphere (internal).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace rsot_cuda {
+
+struct GeoWorkspace {
+  double* L = nullptr; size_t atom_cap_L = 0;
+  double* J = nullptr; size_t atom_cap_J = 0;
+  double* D = nullptr; size_t atom_cap_D = 0;
+  double* cnt = nullptr; size_t atom_cap_c = 0;
+  double* empty = nullptr; size_t atom_cap_e = 0;
+  int* nearest = nullptr; size_t atom_cap_n = 0;
+  double* G = nullptr; size_t tgt_cap_G = 0;
+  unsigned long long* gacc = nullptr; size_t tgt_cap_a = 0;
+  double* red = nullptr; size_t red_cap = 0;
+  void release();
+};
+
+// Leaves the packed partial result [g + nu | J + sum psi nu | D | pairs |
+// empty | visited] of this rank's atoms in b.res (like launch_dense /
+// run_truncated); b.psi must hold psi.  cutoff = +inf: dense.
+// Optional per-atom debug outputs (candidate count, hash, ln S_q).
+int run_geodesic(GeoWorkspace& w, const DeviceAtoms& a, const DeviceTargets& t, EvalBuffers& b,
+                 double eps, double cutoff, cudaStream_t s, std::string& err,
+                 uint32_t* dbg_count = nullptr, uint64_t* dbg_hash = nullptr,
+                 double* dbg_log_s = nullptr);
+
+}  // namespace rsot_cuda

@@ -258,50 +258,6 @@ __device__ __forceinline__ WarpBox warp_box(bool valid, float a, float b, float 
   return w;
 }
 
-// 192-bit fixed point (scale 2^150) accumulation of a non-negative double.
-__device__ void fp_add(unsigned long long* acc, double m) {
-  if (!(m > 0.0)) return;
-  int e;
-  const double fr = frexp(m, &e);                   // m = fr * 2^e, fr in [0.5,1)
-  const unsigned long long mant = static_cast<unsigned long long>(ldexp(fr, 53));
-  const int sh = e - 53 + 150;                       // value = mant * 2^sh
-  unsigned long long l0 = 0, l1 = 0, l2 = 0;
-  if (sh < 0) {
-    if (sh > -64) l0 = mant >> (-sh);
-  } else {
-    const int w = sh >> 6, b = sh & 63;
-    const unsigned long long lo = mant << b;
-    const unsigned long long hi = b ? (mant >> (64 - b)) : 0ull;
-    if (w == 0) { l0 = lo; l1 = hi; }
-    else if (w == 1) { l1 = lo; l2 = hi; }
-    else if (w == 2) { l2 = lo; }
-  }
-  unsigned long long carry = 0;
-  {
-    if (l0) {
-      const unsigned long long old = atomicAdd(&acc[0], l0);
-      carry = (old + l0 < old) ? 1ull : 0ull;
-    }
-  }
-  {
-    const unsigned long long add = l1 + carry;
-    const unsigned long long c1 = (add < l1) ? 1ull : 0ull;
-    carry = c1;
-    if (add) {
-      const unsigned long long old = atomicAdd(&acc[1], add);
-      carry += (old + add < old) ? 1ull : 0ull;
-    }
-  }
-  {
-    const unsigned long long add = l2 + carry;
-    if (add) atomicAdd(&acc[2], add);
-  }
-}
-
-__device__ double fp_to_double(const unsigned long long* acc) {
-  return (static_cast<double>(acc[2]) * 0x1p-22 + static_cast<double>(acc[1]) * 0x1p-86) +
-         static_cast<double>(acc[0]) * 0x1p-150;
-}
 
 // Warp-cooperative exact nearest target (lexicographic (d^2, j) argmin) by
 // expanding Chebyshev rings of cells.  A ring is a set of cell rows; the
@@ -1633,6 +1589,44 @@ __global__ void plan_fill_kernel(const double4* __restrict__ xs, int nq,
     if (pos == 0) {
       double bd;
       int bj, bk;
+      warp_nearest(g, ys, tperm, cell_start, x.x, x.y, x.z, bd, bj, bk);  // index.nearest
+      if (lane == 0) idx[base] = static_cast<unsigned long long>(bj);
+      pos = 1;
+    }
+    if (lane == 0 && pos != off[q + 1] - base) atomicExch(bad, 1);
+  }
+}
+
+// Geodesic cost: full scan {j : c < cutoff} in index order (evaluate.cpp /
+// plan.cpp full-scan branch), Euclidean nearest when empty.
+__global__ void plan_fill_geo_kernel(const double4* __restrict__ xs, int nq,
+                                     const double4* __restrict__ yo, int n, double cutoff,
+                                     const double4* __restrict__ ys, const int* __restrict__ tperm,
+                                     const int* __restrict__ cell_start, GridDev g,
+                                     const unsigned long long* __restrict__ off,
+                                     unsigned long long* __restrict__ idx, int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int q = warp; q < nq; q += nwarps) {
+    const double4 x = xs[q];
+    const unsigned long long base = off[q];
+    unsigned long long pos = 0;
+    for (int k0 = 0; k0 < n; k0 += 32) {
+      const int k = k0 + lane;
+      bool in = false;
+      if (k < n) {
+        const double4 y = yo[k];
+        in = geo_cost(x.x, x.y, x.z, y.x, y.y, y.z) < cutoff;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, in);
+      if (in) idx[base + pos + __popc(m & lt)] = static_cast<unsigned long long>(k);
+      pos += __popc(m);
+    }
+    if (pos == 0) {
+      double bd;
+      int bj, bk;
       warp_nearest(g, ys, tperm, cell_start, x.x, x.y, x.z, bd, bj, bk);
       if (lane == 0) idx[base] = static_cast<unsigned long long>(bj);
       pos = 1;
@@ -1646,6 +1640,7 @@ __global__ void plan_fill_kernel(const double4* __restrict__ xs, int nq,
 // mass and first moments into 192-bit fixed point (moments of x - lo, so
 // every term is non-negative; order independent), barycentric image and
 // modal argmax (lowest index on ties) per atom.
+template <bool GEO>
 __global__ void plan_moments_kernel(const double4* __restrict__ xs, int nq,
                                     const double4* __restrict__ ys, int n,
                                     const double* __restrict__ psi, double eps,
@@ -1668,7 +1663,8 @@ __global__ void plan_moments_kernel(const double4* __restrict__ xs, int nq,
     for (unsigned long long k = b + lane; k < e; k += 32) {
       const unsigned long long j = off ? idx[k] : k;
       const double4 y = ys[j];
-      const double c = __dmul_rn(0.5, exact_sqdist(x.x, x.y, x.z, y.x, y.y, y.z));
+      const double c = GEO ? geo_cost(x.x, x.y, x.z, y.x, y.y, y.z)
+                           : __dmul_rn(0.5, exact_sqdist(x.x, x.y, x.z, y.x, y.y, y.z));
       const double ex = __dadd_rn(__ddiv_rn(__dsub_rn(psi[j], c), eps), y.w);
       const double p = exp(__dsub_rn(ex, L));
       if (acc) {
@@ -1930,11 +1926,11 @@ int run_covering_cost(TruncWorkspace& ws, const DeviceAtoms& a, const DeviceTarg
 }
 
 int run_plan_candidates(TruncWorkspace& ws, const DeviceAtoms& a, const DeviceTargets& t,
-                        TargetCells& tc, double cutoff, const uint64_t* off_host,
+                        TargetCells& tc, double cutoff, bool geo, const uint64_t* off_host,
                         uint64_t* idx_host, cudaStream_t s, std::string& err) {
   const int nq = a.nq;
   if (nq == 0) return 0;
-  const double radius = cutoff < 0.0 ? 0.0 : std::sqrt(2.0 * cutoff);  // cost.hpp:38-42
+  const double radius = geo ? 0.0 : (cutoff < 0.0 ? 0.0 : std::sqrt(2.0 * cutoff));  // cost.hpp:38-42
   const double r2 = radius * radius;
   const bool scan = radius > 0.0;
   const double r_use = scan ? radius : 0.0;
@@ -1951,9 +1947,13 @@ int run_plan_candidates(TruncWorkspace& ws, const DeviceAtoms& a, const DeviceTa
   TCK(cudaMalloc(&bad, sizeof(int)));
   TCK(cudaMemcpyAsync(off, off_host, sizeof(unsigned long long) * (nq + 1), cudaMemcpyHostToDevice, s));
   TCK(cudaMemsetAsync(bad, 0, sizeof(int), s));
-  (note_launch(), plan_fill_kernel<<<std::min(8192, (nq + 7) / 8), 256, 0, s>>>(
-      a.x, nq, tc.pc, tc.perm_c, tc.cell_start, to_dev(tc.g), r2, r_scan, scan ? 1 : 0, off, idx,
-      bad));
+  if (geo)
+    (note_launch(), plan_fill_geo_kernel<<<std::min(8192, (nq + 7) / 8), 256, 0, s>>>(
+        a.x, nq, t.y, t.n, cutoff, tc.pc, tc.perm_c, tc.cell_start, to_dev(tc.g), off, idx, bad));
+  else
+    (note_launch(), plan_fill_kernel<<<std::min(8192, (nq + 7) / 8), 256, 0, s>>>(
+        a.x, nq, tc.pc, tc.perm_c, tc.cell_start, to_dev(tc.g), r2, r_scan, scan ? 1 : 0, off, idx,
+        bad));
   TCK(cub::DeviceSegmentedSort::SortKeys(tmp, tmp_bytes, idx, sorted, static_cast<int64_t>(total), nq,
                                          off, off + 1, s));
   TCK(cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 1)));
@@ -1976,7 +1976,7 @@ int run_plan_candidates(TruncWorkspace& ws, const DeviceAtoms& a, const DeviceTa
 }
 
 int run_plan_moments(const DeviceAtoms& a, const DeviceTargets& t, const double* psi_host,
-                     double eps, const double* log_s_host, const uint64_t* off_host,
+                     double eps, bool geo, const double* log_s_host, const uint64_t* off_host,
                      const uint64_t* idx_host, const double atom_lo[3], double* marginal,
                      double* moment, double* map, uint64_t* modal, cudaStream_t s,
                      std::string& err) {
@@ -2003,8 +2003,12 @@ int run_plan_moments(const DeviceAtoms& a, const DeviceTargets& t, const double*
   }
   if (map) TCK(cudaMalloc(&dmap, sizeof(double) * 3 * std::max(nq, 1)));
   if (modal) TCK(cudaMalloc(&dmodal, sizeof(unsigned long long) * std::max(nq, 1)));
-  if (nq > 0)
-    (note_launch(), plan_moments_kernel<<<std::min(8192, (nq + 7) / 8), 256, 0, s>>>(
+  if (nq > 0 && geo)
+    (note_launch(), plan_moments_kernel<true><<<std::min(8192, (nq + 7) / 8), 256, 0, s>>>(
+        a.x, nq, t.y, n, psi, eps, ls, off, idx, atom_lo[0], atom_lo[1], atom_lo[2], acc, dmap,
+        dmodal));
+  else if (nq > 0)
+    (note_launch(), plan_moments_kernel<false><<<std::min(8192, (nq + 7) / 8), 256, 0, s>>>(
         a.x, nq, t.y, n, psi, eps, ls, off, idx, atom_lo[0], atom_lo[1], atom_lo[2], acc, dmap,
         dmodal));
   if (want_acc && n > 0) {

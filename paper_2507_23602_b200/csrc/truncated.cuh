@@ -102,14 +102,14 @@ int run_nearest_points(TruncWorkspace& ws, const DeviceTargets& t,
 // atom q's ascending candidate set (ball query, nearest when empty); the
 // offsets must come from the candidate counts of the same cutoff.
 int run_plan_candidates(TruncWorkspace& ws, const DeviceAtoms& a, const DeviceTargets& t,
-                        TargetCells& tc, double cutoff, const uint64_t* off_host,
+                        TargetCells& tc, double cutoff, bool geo, const uint64_t* off_host,
                         uint64_t* idx_host, cudaStream_t s, std::string& err);
 
 // PlanView reductions over candidate lists (off_host == nullptr: all
 // targets): target marginals, first moments (n x 3), barycentric map
 // (nq x 3), modal target per atom.  Outputs may be null.
 int run_plan_moments(const DeviceAtoms& a, const DeviceTargets& t, const double* psi_host,
-                     double eps, const double* log_s_host, const uint64_t* off_host,
+                     double eps, bool geo, const double* log_s_host, const uint64_t* off_host,
                      const uint64_t* idx_host, const double atom_lo[3], double* marginal,
                      double* moment, double* map, uint64_t* modal, cudaStream_t s,
                      std::string& err);

@@ -440,16 +440,19 @@ def evaluate_dual(atoms: SourceAtoms, target: TargetMeasure, psi: DualPotential,
     if len(values) != target.size():
         raise ValueError("evaluate_dual: psi length != target count")
     require_finite(values)
-    if cfg.cost_kind != CostKind.SqEuclidean:
-        raise NotImplementedError("SqGeodesicSphere is out of scope for the B200 evaluator")
     ctx = ctx or (index.ctx if index is not None else Context.default())
     dev_t = _device_targets(target, ctx)
     dev_a = _device_atoms(atoms, ctx)
     g = np.empty(target.size(), dtype=np.float64)
     sc = _lib.RsotCudaScalars()
-    _lib.check(ctx.lib.rsot_cuda_eval(ctx.handle, dev_a.handle, dev_t.handle, _ptr(values),
-                                      float(cfg.epsilon), float(trunc.cutoff), _ptr(g),
-                                      ctypes.byref(sc)))
+    if cfg.cost_kind == CostKind.SqEuclidean:
+        _lib.check(ctx.lib.rsot_cuda_eval(ctx.handle, dev_a.handle, dev_t.handle, _ptr(values),
+                                          float(cfg.epsilon), float(trunc.cutoff), _ptr(g),
+                                          ctypes.byref(sc)))
+    else:  # cost.hpp:27-30, full-scan truncation (evaluate.cpp:124-128)
+        _lib.check(ctx.lib.rsot_cuda_eval_cost(ctx.handle, dev_a.handle, dev_t.handle, _ptr(values),
+                                               float(cfg.epsilon), float(trunc.cutoff), 1, _ptr(g),
+                                               ctypes.byref(sc)))
     return EvalResult(J=sc.J, gradient=g, D=sc.D, atoms_visited=int(sc.atoms_visited),
                       candidate_pairs=int(sc.candidate_pairs),
                       empty_candidate_atoms=int(sc.empty_candidate_atoms))
@@ -478,8 +481,12 @@ def softmax_refine(coarse: TargetMeasure, coarse_psi, fine_points, atoms: Source
     return out
 
 
+def _cost_code(kind: CostKind) -> int:
+    return 1 if kind == CostKind.SqGeodesicSphere else 0
+
+
 def evaluate_dual_debug(atoms: SourceAtoms, target: TargetMeasure, psi, eps: float, cutoff: float,
-                        ctx: Optional[Context] = None):
+                        ctx: Optional[Context] = None, kind: CostKind = CostKind.SqEuclidean):
     """evaluate_dual plus per-atom candidate counts, candidate hashes and ln S_q
     (for selection parity against the oracle)."""
     ctx = ctx or Context.default()
@@ -491,9 +498,9 @@ def evaluate_dual_debug(atoms: SourceAtoms, target: TargetMeasure, psi, eps: flo
     hsh = np.zeros(dev_a.nq, dtype=np.uint64)
     logs = np.zeros(dev_a.nq, dtype=np.float64)
     sc = _lib.RsotCudaScalars()
-    _lib.check(ctx.lib.rsot_cuda_eval_debug(ctx.handle, dev_a.handle, dev_t.handle, _ptr(values),
-                                            float(eps), float(cutoff), _ptr(g), ctypes.byref(sc),
-                                            _ptr(cnt), _ptr(hsh), _ptr(logs)))
+    _lib.check(ctx.lib.rsot_cuda_eval_debug_cost(ctx.handle, dev_a.handle, dev_t.handle, _ptr(values),
+                                                 float(eps), float(cutoff), _cost_code(kind), _ptr(g),
+                                                 ctypes.byref(sc), _ptr(cnt), _ptr(hsh), _ptr(logs)))
     res = EvalResult(J=sc.J, gradient=g, D=sc.D, atoms_visited=int(sc.atoms_visited),
                      candidate_pairs=int(sc.candidate_pairs),
                      empty_candidate_atoms=int(sc.empty_candidate_atoms))
@@ -523,8 +530,6 @@ class PlanView:
     def __init__(self, atoms: SourceAtoms, target: TargetMeasure, psi: DualPotential, eps: float,
                  kind: CostKind = CostKind.SqEuclidean, cutoff: float = math.inf, workers: int = 1,
                  ctx: Optional[Context] = None):
-        if kind != CostKind.SqEuclidean:
-            raise ValueError("plan view: only the squared Euclidean cost runs on the GPU")
         values = np.ascontiguousarray(np.asarray(psi.values, dtype=np.float64))
         if len(values) != target.size():
             raise ValueError("plan view: psi length != target count")
@@ -533,13 +538,14 @@ class PlanView:
         self.atoms, self.target, self.psi, self.eps, self.kind = atoms, target, values, float(eps), kind
         self._dt = DeviceTargets(self.ctx, target.points, target.weights)
         self._da = DeviceAtoms(self.ctx, atoms.points, atoms.masses, shard=False)
-        _, cnt, _, logs = evaluate_dual_debug(atoms, target, values, eps, cutoff, ctx=self.ctx)
+        _, cnt, _, logs = evaluate_dual_debug(atoms, target, values, eps, cutoff, ctx=self.ctx, kind=kind)
         self.log_S = logs
         self.offsets = np.zeros(len(cnt) + 1, dtype=np.uint64)
         np.cumsum(cnt.astype(np.uint64), out=self.offsets[1:])
         self.idx = np.zeros(max(int(self.offsets[-1]), 1), dtype=np.uint64)
         _lib.check(self.ctx.lib.rsot_cuda_plan_candidates(self.ctx.handle, self._da.handle, self._dt.handle,
-                                                          float(cutoff), _ptr(self.offsets), _ptr(self.idx)))
+                                                          float(cutoff), _cost_code(kind), _ptr(self.offsets),
+                                                          _ptr(self.idx)))
         self.converged_known = False
         self.converged = False
 
@@ -559,7 +565,8 @@ class PlanView:
                    map=np.zeros((nq, 3)) if bary_map else None,
                    modal=np.zeros(nq, dtype=np.uint64) if modal else None)
         _lib.check(self.ctx.lib.rsot_cuda_plan_moments(
-            self.ctx.handle, self._da.handle, self._dt.handle, _ptr(self.psi), self.eps, _ptr(self.log_S),
+            self.ctx.handle, self._da.handle, self._dt.handle, _ptr(self.psi), self.eps, _cost_code(self.kind),
+            _ptr(self.log_S),
             _ptr(self.offsets), _ptr(self.idx), _ptr(out["marginal"]), _ptr(out["moment"]), _ptr(out["map"]),
             _ptr(out["modal"])))
         return out
@@ -569,7 +576,10 @@ class PlanView:
         x = _points3(self.atoms.points)[q]
         cand = self.candidates(q)
         y = _points3(self.target.points)[cand]
-        c = 0.5 * (((x[0] - y[:, 0]) ** 2 + (x[1] - y[:, 1]) ** 2) + (x[2] - y[:, 2]) ** 2)
+        if self.kind == CostKind.SqGeodesicSphere:
+            c = np.arccos(np.clip((x[0] * y[:, 0] + x[1] * y[:, 1]) + x[2] * y[:, 2], -1.0, 1.0)) ** 2
+        else:
+            c = 0.5 * (((x[0] - y[:, 0]) ** 2 + (x[1] - y[:, 1]) ** 2) + (x[2] - y[:, 2]) ** 2)
         e = (self.psi[cand] - c) / self.eps + np.log(np.asarray(self.target.weights)[cand])
         return list(zip(cand.tolist(), np.exp(e - self.log_S[q]).tolist()))
 

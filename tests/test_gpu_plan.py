@@ -83,16 +83,54 @@ def test_plan_view_starved_target(ctx):
             plan.all_conditional_barycenters()
 
 
-def test_plan_view_rejects_geodesic_and_bad_psi(ctx):
+def test_plan_view_rejects_bad_psi(ctx):
     rng = np.random.default_rng(6)
     A, M, T, W, psi = random_instance(rng, 3, 20, 100, 0.05)
     atoms = rs.SourceAtoms(dim=3, points=A, masses=M)
     tgt = rs.TargetMeasure(dim=3, points=T, weights=W)
-    with pytest.raises(ValueError):
-        rs.PlanView(atoms, tgt, rs.DualPotential(psi), 0.1, kind=rs.CostKind.SqGeodesicSphere, ctx=ctx)
     bad = psi.copy()
     bad[3] = np.nan
     with pytest.raises(ValueError):
         rs.PlanView(atoms, tgt, rs.DualPotential(bad), 0.1, ctx=ctx)
     with pytest.raises(ValueError):
         rs.PlanView(atoms, tgt, rs.DualPotential(psi[:-1]), 0.1, ctx=ctx)
+
+
+@pytest.mark.parametrize("cutoff", [math.inf, 0.05])
+def test_plan_view_geodesic(ctx, cutoff):
+    """PlanView with CostKind::SqGeodesicSphere (the blue-noise plan,
+    sphere.cpp:139): candidate counts and log_S from the geodesic oracle,
+    marginals = g + nu of the geodesic evaluation, maps against a numpy
+    restatement of plan.cpp over the same candidate sets."""
+    rng = np.random.default_rng(17)
+    v = rng.normal(size=(200, 3))
+    T = v / np.linalg.norm(v, axis=1, keepdims=True)
+    v = rng.normal(size=(1500, 3))
+    A = v / np.linalg.norm(v, axis=1, keepdims=True)
+    M = np.full(1500, 1 / 1500)
+    W = np.full(200, 1 / 200)
+    psi = rng.normal(0, 0.01, size=200)
+    eps = 0.05
+    atoms = rs.SourceAtoms(dim=3, points=A, masses=M)
+    tgt = rs.TargetMeasure(dim=3, points=T, weights=W)
+    plan = rs.PlanView(atoms, tgt, rs.DualPotential(psi), eps, kind=rs.CostKind.SqGeodesicSphere,
+                       cutoff=cutoff, ctx=ctx)
+    want = C.evaluate_dual_geodesic(A, M, T, W, psi, eps, cutoff, per_atom=True)
+    assert np.array_equal(np.diff(plan.offsets), want["count"])
+    assert np.max(np.abs(plan.log_S - want["log_s"])) <= 1e-12 * np.max(np.abs(want["log_s"]))
+    marg = plan.target_marginals()
+    assert np.max(np.abs(marg - (want["gradient"] + W))) <= 1e-12
+    dots = np.clip(A @ T.T, -1.0, 1.0)
+    cost = np.arccos(dots) ** 2
+    e = (psi[None, :] - cost) / eps + np.log(W)[None, :]
+    mask = np.zeros_like(e, dtype=bool)
+    for q in range(len(A)):
+        mask[q, plan.candidates(q)] = True
+    p = np.where(mask, np.exp(e - plan.log_S[:, None]), 0.0)
+    bary_map = p @ T
+    assert np.max(np.abs(rs.barycentric_map(plan).mapped - bary_map)) <= 1e-12
+    score = np.where(mask, psi[None, :] - cost + eps * np.log(W)[None, :], -np.inf)
+    assert np.array_equal(rs.modal_map(plan).target_index, np.argmax(score, axis=1))
+    if np.all((p * M[:, None]).sum(axis=0) >= 1e-30):
+        first = (p * M[:, None]).T @ A / (p * M[:, None]).sum(axis=0)[:, None]
+        assert np.max(np.abs(plan.all_conditional_barycenters() - first)) <= 1e-10

@@ -274,3 +274,26 @@ def test_plan_view_oracle_starved_equals_reference():
         r = ref.problem(3, A, M, T, W).plan_view(psi, 0.02, cutoff)
         assert o["starved"] == r["starved"] == 17
         assert np.array_equal(o["marginal"], r["marginal"]) and np.array_equal(o["map"], r["map"])
+
+
+@pytest.mark.parametrize("n,nq,eps,cutoff", [(300, 2000, 0.05, math.inf), (300, 2000, 0.05, 0.05),
+                                              (100, 500, 0.02, 0.0005), (50, 400, 0.1, -1.0)])
+def test_geodesic_oracle_equals_reference(n, nq, eps, cutoff):
+    """SqGeodesicSphere restatement vs the reference evaluate.cpp (cost kind
+    switched in SolverConfig), bit for bit."""
+    ref = _ref_or_skip()
+    rng = np.random.default_rng(n + nq)
+    v = rng.normal(size=(n, 3))
+    T = v / np.linalg.norm(v, axis=1, keepdims=True)
+    v = rng.normal(size=(nq, 3))
+    A = v / np.linalg.norm(v, axis=1, keepdims=True)
+    M = rng.uniform(size=nq) + 0.1
+    M /= M.sum()
+    W = rng.uniform(size=n) + 0.1
+    W /= W.sum()
+    psi = rng.normal(0, 0.01, size=n)
+    o = C.evaluate_dual_geodesic(A, M, T, W, psi, eps, cutoff)
+    r = ref.problem(3, A, M, T, W).evaluate_dual_geodesic(psi, eps, cutoff)
+    assert o["J"] == r["J"] and o["D"] == r["D"] and np.array_equal(o["gradient"], r["gradient"])
+    assert o["candidate_pairs"] == r["candidate_pairs"]
+    assert o["empty_candidate_atoms"] == r["empty_candidate_atoms"]

@@ -37,7 +37,9 @@ namespace rsot_cuda {
 namespace {
 
 constexpr int kT = 128;        // threads per CTA = points per chunk
-constexpr int kTileT = 256;    // staged points per tile
+constexpr int kTileT = 256;    // staged points per tile (fp64 kernel)
+constexpr int kTileT32 = 512;  // staged points per tile (fp32 kernel)
+using ListT = unsigned short;  // per-warp culled-list entry (tile index)
 constexpr int kMortonBits = 7; // per dim, position inside a cell
 double g_cells_per_radius = 3.0;  // grid cell side ~ r / 3 (env RSOT_CELLS_PER_RADIUS)
 
@@ -437,7 +439,7 @@ struct FusedSmem {
   int tJ[kTileT];                      // original target index
   int rowStart[kT];
   int rowPref[kT + 1];
-  unsigned char wlist[kT / 32][kTileT];
+  ListT wlist[kT / 32][kTileT];
   double colW[kT / 32][kTileT];
   Region R;                            // CTA-uniform scan region (kept out of registers)
   int2 tbl[kExpTab];
@@ -548,7 +550,7 @@ __device__ __forceinline__ void fused_stage(FusedSmem& sm, const FusedArgs& A, d
 
 template <class SM>
 __device__ __forceinline__ int fused_cull(const SM& sm, int cnt, const WarpBox& w,
-                                          float thr, unsigned char* __restrict__ list) {
+                                          float thr, ListT* __restrict__ list) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   int nsel = 0;
@@ -564,7 +566,7 @@ __device__ __forceinline__ int fused_cull(const SM& sm, int cnt, const WarpBox& 
       keep = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= thr;
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (keep) list[nsel + __popc(m & lt)] = static_cast<unsigned char>(t);
+    if (keep) list[nsel + __popc(m & lt)] = static_cast<ListT>(t);
     nsel += __popc(m);
   }
   __syncwarp();
@@ -758,7 +760,7 @@ __device__ __forceinline__ double2 step64(const FusedSmem& sm, const FusedArgs& 
 
 template <bool SAFE, bool DEBUG>
 __device__ __forceinline__ void batch64(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at,
-                                        const Step32& K, bool wide, const unsigned char* list,
+                                        const Step32& K, bool wide, const ListT* list,
                                         int b0, int nsel, double* col) {
   const int lane = threadIdx.x & 31;
   double v[16];
@@ -785,7 +787,7 @@ template <int PHASE, bool SAFE, bool DEBUG>
 __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb, float cull_thr,
                            double B, FusedAtoms& at) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* const list = sm.wlist[warp];
+  ListT* const list = sm.wlist[warp];
   const bool wide = SAFE && sm.R.wide;
   const Step32 K = make_step(at.lo_thr, at.hi_thr);
   const int ny = sm.R.c_hi[1] - sm.R.c_lo[1] + 1;
@@ -1010,14 +1012,14 @@ trunc_fused(FusedArgs A) {
 // exponent rounding); the tests assert 2e-5.
 
 struct Fused32Smem {
-  float4 tN0[kTileT];                  // {-y0', -y0', -y1', -y1'}
-  float4 tN1[kTileT];                  // {-y2', -y2', b2_j - B, b2_j - B}
-  int tK[kTileT];                      // cell-order target position
-  int tJ[kTileT];                      // original target index
+  float4 tN0[kTileT32];                  // {-y0', -y0', -y1', -y1'}
+  float4 tN1[kTileT32];                  // {-y2', -y2', b2_j - B, b2_j - B}
+  int tK[kTileT32];                      // cell-order target position
+  int tJ[kTileT32];                      // original target index
   int rowStart[kT];
   int rowPref[kT + 1];
-  unsigned char wlist[kT / 32][kTileT];
-  float colW[kT / 32][kTileT];
+  ListT wlist[kT / 32][kTileT32];
+  float colW[kT / 32][kTileT32];
   float wmax[kT / 32];
   Region R;
   double sh[200];
@@ -1055,20 +1057,21 @@ __device__ __forceinline__ float butterfly16f(float (&v)[16]) {
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
-// Stages tile [base, base + cnt) (kTileT = 2 kT: entries tid and tid + kT).
+// Stages tile [base, base + cnt) (entries tid + u kT, u < kTileT32 / kT).
 // The tile's b2 maximum is reduced before the tile is written, so the staged
 // exponent offsets are relative to the updated CTA shift.  Two barriers per
 // tile; the global loads are issued before the first one.
 template <int PHASE>
 __device__ __forceinline__ void fused_stage32(Fused32Smem& sm, const FusedArgs& A, int base,
                                               int cnt, double& Bc, Atoms32& at) {
-  static_assert(kTileT == 2 * kT, "two staged entries per thread");
-  double4 y[2];
-  double b2[2];
-  int k[2];
+  constexpr int kPer = kTileT32 / kT;
+  static_assert(kTileT32 % kT == 0, "whole staged entries per thread");
+  double4 y[kPer];
+  double b2[kPer];
+  int k[kPer];
   float mx = -INFINITY;
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
+  for (int u = 0; u < kPer; ++u) {
     const int t = threadIdx.x + u * kT;
     k[u] = 0;
     b2[u] = -INFINITY;
@@ -1100,7 +1103,7 @@ __device__ __forceinline__ void fused_stage32(Fused32Smem& sm, const FusedArgs& 
   }
   const double o0 = sm.R.o[0], o1 = sm.R.o[1], o2 = sm.R.o[2];
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
+  for (int u = 0; u < kPer; ++u) {
     const int t = threadIdx.x + u * kT;
     if (t < cnt) {
       const float f0 = -static_cast<float>(y[u].x - o0), f1 = -static_cast<float>(y[u].y - o1),
@@ -1190,7 +1193,7 @@ __device__ __forceinline__ float2 step32(const Fused32Smem& sm, const FusedArgs&
 
 template <bool FULL, bool DEBUG>
 __device__ __forceinline__ void batch32(const Fused32Smem& sm, const FusedArgs& A, Atoms32& at,
-                                        const Step32& K, const unsigned char* list, int b0, int nsel,
+                                        const Step32& K, const ListT* list, int b0, int nsel,
                                         float* col) {
   const int lane = threadIdx.x & 31;
   float v[16];
@@ -1215,7 +1218,7 @@ template <int PHASE, bool DEBUG>
 __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox& wb,
                              float cull_thr, double& Bc, Atoms32& at) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* const list = sm.wlist[warp];
+  ListT* const list = sm.wlist[warp];
   Step32 K = make_step(at.lo_thr, at.hi_thr);
   const float nc2f = static_cast<float>(-A.c2);
   K.nc2 = make_float2(nc2f, nc2f);
@@ -1230,8 +1233,8 @@ __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox&
     sm.rowStart[threadIdx.x] = st;
     sm.rowPref[threadIdx.x] = pre;
     if (threadIdx.x == 0) sm.rowPref[kT] = total;
-    for (int base = 0; base < total; base += kTileT) {
-      const int cnt = min(kTileT, total - base);
+    for (int base = 0; base < total; base += kTileT32) {
+      const int cnt = min(kTileT32, total - base);
       fused_stage32<PHASE>(sm, A, base, cnt, Bc, at);
       const int nsel = fused_cull(sm, cnt, wb, cull_thr, list);
       if (PHASE == 1) {

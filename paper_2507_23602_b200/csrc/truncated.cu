@@ -1233,6 +1233,7 @@ __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox&
     sm.rowStart[threadIdx.x] = st;
     sm.rowPref[threadIdx.x] = pre;
     if (threadIdx.x == 0) sm.rowPref[kT] = total;
+    __syncthreads();  // the staging loads read every thread's row range
     for (int base = 0; base < total; base += kTileT32) {
       const int cnt = min(kTileT32, total - base);
       fused_stage32<PHASE>(sm, A, base, cnt, Bc, at);

@@ -35,6 +35,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "dual obj+grad evals/sec"
 W_PAIR = 25  # FP64-pipe instructions per pair in the reference formula
+W32_PAIR = 10  # FP32-pipe instructions per pair of the fp32 path
 WORKLOADS = {
     "cfg1": "cfg1: 2D dense, 64x64 Q1 quads x 2x2 Gauss = 16,384 atoms, N=1,024 U[0,1]^2 targets, eps=1e-2",
     "cfg2": "cfg2: 3D dense, 32^3 hexes x 2^3 Gauss = 262,144 atoms (3-Gaussian mixture density), "
@@ -53,6 +54,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
+                    help="fp32: mixed-precision truncated path (FP32 exponent + ex2, fp64 sums; "
+                         "dense evaluations stay fp64)")
     return ap.parse_args()
 
 
@@ -124,7 +128,7 @@ def run_reference(args, rank):
         "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded; BASELINE shapes)", "impl": "reference",
         "config": {"workload": WORKLOADS[args.workload]},
-        "pairs_per_s": v * (prob.nq * prob.n if prob.truncation == "none" else float("nan")),
+        "pairs_per_s": v * prob.nq * prob.n if prob.truncation == "none" else None,
         "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": kind, "sample": desc},
         "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -192,6 +196,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     ctx = rs.Context(local_rank)
+    ctx.set_precision(args.precision)
     if world > 1:
         uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
@@ -297,11 +302,27 @@ def run_ours(args, rank, world, local_rank):
     dfma = ctx.fp64_dfma_rate()
     value = 1e3 / ms_step
     kern_ms = statistics.median(passA) + statistics.median(passB)
-    algo_flops = 2.0 * W_PAIR * pairs / world  # per GPU: DFMA-equivalent flops of the reference formula
+    mixed = args.precision == "fp32" and prob.truncation != "none"
+    if mixed:
+        # SURVEY.md §8d FP32 path: 10 FP32-pipe instr + 1 MUFU.EX2 per pair;
+        # peak = 128 FFMA/clk/SM x SMs x max SM clock (nominal: no FP32 probe)
+        sms = ctx.lib.rsot_cuda_ctx_num_sms(ctx.handle)
+        f_max = (clk or {}).get("sm_max_mhz") or 1965.0
+        algo_flops = 2.0 * W32_PAIR * pairs / world
+        peak = 2.0 * 128 * sms * f_max * 1e6 / 1e12
+        bound, definition = "fp32", (f"{W32_PAIR} FP32-pipe instr/pair (SURVEY.md §8d fp32 path) x 2 flop x "
+                                     "pairs / CUDA-event time; peak = 128 FFMA/clk/SM x SMs x max SM clock x 2")
+    else:
+        algo_flops = 2.0 * W_PAIR * pairs / world  # per GPU: DFMA-equivalent flops of the reference formula
+        peak = 2.0 * dfma / 1e12
+        bound, definition = "fp64", (f"{W_PAIR} FP64-pipe instr/pair (reference formula, one exp/pair) x 2 flop "
+                                     "x pairs / CUDA-event time of the hot kernels; peak = measured DFMA rate x 2 "
+                                     "(live probe)")
     achieved = algo_flops / (kern_ms * 1e-3) / 1e12
-    peak = 2.0 * dfma / 1e12
+    kernel_desc = ("pass A (LSE) + pass B (gradient gather), per GPU" if prob.truncation == "none" else
+                   "trunc_fused%s (both phases) + trunc_nearest_empty, per GPU" % ("32" if mixed else ""))
     traffic = None
-    prof = os.path.join(ROOT, "profiles", f"ncu_summary_{args.workload}.json")
+    prof = os.path.join(ROOT, "profiles", f"ncu_summary_{args.workload}{'_fp32' if mixed else ''}.json")
     if os.path.exists(prof):
         try:
             traffic = json.load(open(prof)).get("dram_bytes_per_eval")
@@ -310,19 +331,21 @@ def run_ours(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded generator with BASELINE shapes; no dataset exists)",
+        "dtype": "f32+f64" if mixed else "f64",
+        "data": "synthetic (seeded generator with BASELINE shapes; no dataset exists)",
         "config": {"workload": WORKLOADS[args.workload], "nq": prob.nq, "n": prob.n, "eps": prob.eps,
-                   "parallelism": f"atoms sharded over {world} GPU(s), targets replicated, 1 allreduce/eval",
+                   "parallelism": f"atoms sharded over {world} GPU(s), targets replicated, "
+                                  "1 allgather + rank-ordered sum / eval",
+                   "precision": args.precision,
                    "l2": "flushed between steps (256 MiB write, inside the timed region)"},
         "pairs_per_s": pairs * value,
         "candidate_pairs_per_eval": pairs,
         "roofline": {
-            "bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic,
-            "kernel": "pass A (LSE) + pass B (gradient gather), per GPU",
+            "kernel": kernel_desc,
             "kernel_ms": {"pass_a": statistics.median(passA), "pass_b": statistics.median(passB)},
-            "definition": f"{W_PAIR} FP64-pipe instr/pair (reference formula, one exp/pair) x 2 flop x pairs "
-                          "/ CUDA-event time of the two passes; peak = measured DFMA rate x 2 (live probe)",
+            "definition": definition,
         },
         "e2e": {"value": e2e_v, "unit": "evals/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n + 8 * 6},

@@ -1119,8 +1119,8 @@ __device__ __forceinline__ void fused_stage32(Fused32Smem& sm, const FusedArgs& 
 }
 
 // FP32x2 squared distances of item t to atoms (a, b) and the item's offset.
-__device__ __forceinline__ float2 fused_d2w(const Fused32Smem& sm, const Atoms32& at, int t,
-                                           float& w) {
+template <class SM>
+__device__ __forceinline__ float2 fused_d2w(const SM& sm, const Atoms32& at, int t, float& w) {
   const float4 n01 = sm.tN0[t];
   const float4 n2 = sm.tN1[t];
   const float2 dx = __fadd2_rn(at.F0, make_float2(n01.x, n01.y));
@@ -1138,8 +1138,8 @@ __device__ __forceinline__ float2 fused_d2w(const Fused32Smem& sm, const Atoms32
 // weighted column values of t0 and t1.  Pairs in the FP32 error band take
 // the exact fp64 predicate (warp-uniform slow path, also used in DEBUG
 // builds for the candidate hashes).
-template <int PHASE, bool PAIR, bool DEBUG>
-__device__ __forceinline__ float2 step32(const Fused32Smem& sm, const FusedArgs& A, Atoms32& at,
+template <int PHASE, bool PAIR, bool DEBUG, class SM>
+__device__ __forceinline__ float2 step32(const SM& sm, const FusedArgs& A, Atoms32& at,
                                          const Step32& K, int t0, int t1, float2& acc,
                                          float2& cnt) {
   float w0, w1 = 0.f;
@@ -1191,8 +1191,8 @@ __device__ __forceinline__ float2 step32(const Fused32Smem& sm, const FusedArgs&
   return out;
 }
 
-template <bool FULL, bool DEBUG>
-__device__ __forceinline__ void batch32(const Fused32Smem& sm, const FusedArgs& A, Atoms32& at,
+template <bool FULL, bool DEBUG, class SM>
+__device__ __forceinline__ void batch32(const SM& sm, const FusedArgs& A, Atoms32& at,
                                         const Step32& K, const ListT* list, int b0, int nsel,
                                         float* col) {
   const int lane = threadIdx.x & 31;

@@ -441,6 +441,10 @@ struct FusedSmem {
   int rowPref[kT + 1];
   ListT wlist[kT / 32][kTileT];
   double colW[kT / 32][kTileT];
+  double4 rawY[kTileT];                // cp.async landing zone of the next tile
+  double rawB2[kTileT];
+  int rawJ[kTileT];
+  int rawK[kTileT];
   Region R;                            // CTA-uniform scan region (kept out of registers)
   int2 tbl[kExpTab];
   double sh[200];
@@ -527,24 +531,56 @@ __device__ __forceinline__ double butterfly16(double (&v)[16]) {
 }
 
 // Stages tile [base, base + cnt) of the current row batch.
-__device__ __forceinline__ void fused_stage(FusedSmem& sm, const FusedArgs& A, double B,
-                                            int base, int cnt) {
-  const double o0 = sm.R.o[0], o1 = sm.R.o[1], o2 = sm.R.o[2];
+// Asynchronous copies global -> shared (LDGSTS): the next tile's raw target
+// data lands while the CTA computes the current one.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// Issues the copies of tile [base, base + cnt) of the current row batch
+// (each thread its entries tid + u kT; the same thread converts them).
+__device__ __forceinline__ void fused_prefetch(FusedSmem& sm, const FusedArgs& A, int base, int cnt) {
   for (int t = threadIdx.x; t < cnt; t += kT) {
     const int s = base + t;
     const int r = find_row(sm.rowPref, s);
     const int k = sm.rowStart[r] + (s - sm.rowPref[r]);
-    const double4 y = A.ys[k];
+    sm.rawK[t] = k;  // tK of the tile being computed is still in use
+    cp_async16(&sm.rawY[t], &A.ys[k]);
+    cp_async16(reinterpret_cast<char*>(&sm.rawY[t]) + 16, reinterpret_cast<const char*>(&A.ys[k]) + 16);
+    cp_async8(&sm.rawB2[t], &A.b2s[k]);
+    cp_async4(&sm.rawJ[t], &A.tperm[k]);
+  }
+  cp_async_commit();
+}
+
+// Converts the landed tile into the staged layout (local coordinates,
+// per-target exponent term, FP32 pre-test coordinates).
+__device__ __forceinline__ void fused_convert(FusedSmem& sm, const FusedArgs& A, double B, int cnt) {
+  cp_async_wait_all();
+  const double o0 = sm.R.o[0], o1 = sm.R.o[1], o2 = sm.R.o[2];
+  for (int t = threadIdx.x; t < cnt; t += kT) {
+    const double4 y = sm.rawY[t];
     const double y0 = y.x - o0, y1 = y.y - o1, y2 = y.z - o2;
     const double yy = fma(y2, y2, fma(y1, y1, y0 * y0));
-    const double w = fmax(fma(-A.c2, yy, A.b2s[k]) - B, -1.0e5);
+    const double w = fmax(fma(-A.c2, yy, sm.rawB2[t]) - B, -1.0e5);
     sm.tD[t] = make_double4(y0, y1, y2, w);
     const float f0 = -static_cast<float>(y0), f1 = -static_cast<float>(y1),
                 f2 = -static_cast<float>(y2);
     sm.tN0[t] = make_float4(f0, f0, f1, f1);
     sm.tN1[t] = make_float2(f2, f2);
-    sm.tK[t] = k;
-    sm.tJ[t] = A.tperm[k];
+    sm.tJ[t] = sm.rawJ[t];
+    sm.tK[t] = sm.rawK[t];
   }
 }
 
@@ -801,11 +837,14 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
     sm.rowStart[threadIdx.x] = st;
     sm.rowPref[threadIdx.x] = pre;
     if (threadIdx.x == 0) sm.rowPref[kT] = total;
+    __syncthreads();  // row ranges visible; previous batch fully consumed
+    if (total > 0) fused_prefetch(sm, A, 0, min(kTileT, total));
     for (int base = 0; base < total; base += kTileT) {
       const int cnt = min(kTileT, total - base);
-      __syncthreads();
-      fused_stage(sm, A, B, base, cnt);
-      __syncthreads();
+      __syncthreads();  // every warp is done with the previous tile
+      fused_convert(sm, A, B, cnt);
+      __syncthreads();  // staged tile visible, landing zone free
+      if (base + kTileT < total) fused_prefetch(sm, A, base + kTileT, min(kTileT, total - base - kTileT));
       const int nsel = fused_cull(sm, cnt, wb, cull_thr, list);
       if (PHASE == 1) {
         // software-pipelined: the next step's list entries and distances are

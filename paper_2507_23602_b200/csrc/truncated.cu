@@ -38,7 +38,7 @@ namespace {
 
 constexpr int kT = 128;        // threads per CTA = points per chunk
 constexpr int kTileT = 256;    // staged points per tile (fp64 kernel)
-constexpr int kTileT32 = 512;  // staged points per tile (fp32 kernel)
+constexpr int kTileT32 = 384;  // staged points per tile (fp32 kernel)
 using ListT = unsigned short;  // per-warp culled-list entry (tile index)
 constexpr int kMortonBits = 7; // per dim, position inside a cell
 double g_cells_per_radius = 3.0;  // grid cell side ~ r / 3 (env RSOT_CELLS_PER_RADIUS)
@@ -1055,6 +1055,10 @@ struct Fused32Smem {
   float4 tN1[kTileT32];                  // {-y2', -y2', b2_j - B, b2_j - B}
   int tK[kTileT32];                      // cell-order target position
   int tJ[kTileT32];                      // original target index
+  double4 rawY[kTileT32];                // cp.async landing zone of the next tile
+  double rawB2[kTileT32];
+  int rawJ[kTileT32];
+  int rawK[kTileT32];
   int rowStart[kT];
   int rowPref[kT + 1];
   ListT wlist[kT / 32][kTileT32];
@@ -1096,35 +1100,32 @@ __device__ __forceinline__ float butterfly16f(float (&v)[16]) {
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
-// Stages tile [base, base + cnt) (entries tid + u kT, u < kTileT32 / kT).
-// The tile's b2 maximum is reduced before the tile is written, so the staged
-// exponent offsets are relative to the updated CTA shift.  Two barriers per
-// tile; the global loads are issued before the first one.
-template <int PHASE>
-__device__ __forceinline__ void fused_stage32(Fused32Smem& sm, const FusedArgs& A, int base,
-                                              int cnt, double& Bc, Atoms32& at) {
-  constexpr int kPer = kTileT32 / kT;
-  static_assert(kTileT32 % kT == 0, "whole staged entries per thread");
-  double4 y[kPer];
-  double b2[kPer];
-  int k[kPer];
-  float mx = -INFINITY;
-#pragma unroll
-  for (int u = 0; u < kPer; ++u) {
-    const int t = threadIdx.x + u * kT;
-    k[u] = 0;
-    b2[u] = -INFINITY;
-    y[u] = make_double4(0, 0, 0, 0);
-    if (t < cnt) {
-      const int s = base + t;
-      const int r = find_row(sm.rowPref, s);
-      k[u] = sm.rowStart[r] + (s - sm.rowPref[r]);
-      y[u] = A.ys[k[u]];
-      b2[u] = A.b2s[k[u]];
-      mx = fmaxf(mx, __double2float_ru(b2[u]));
-    }
+// Next tile's raw target data (each thread its entries tid + u kT).
+__device__ __forceinline__ void fused_prefetch32(Fused32Smem& sm, const FusedArgs& A, int base,
+                                                 int cnt) {
+  for (int t = threadIdx.x; t < cnt; t += kT) {
+    const int s = base + t;
+    const int r = find_row(sm.rowPref, s);
+    const int k = sm.rowStart[r] + (s - sm.rowPref[r]);
+    sm.rawK[t] = k;
+    cp_async16(&sm.rawY[t], &A.ys[k]);
+    cp_async16(reinterpret_cast<char*>(&sm.rawY[t]) + 16, reinterpret_cast<const char*>(&A.ys[k]) + 16);
+    cp_async8(&sm.rawB2[t], &A.b2s[k]);
+    cp_async4(&sm.rawJ[t], &A.tperm[k]);
   }
+  cp_async_commit();
+}
+
+// Stages the landed tile: its b2 maximum is reduced first (phase 1 raises
+// the CTA shift and rescales the sums), then the staged exponent offsets are
+// written relative to the updated shift.  Two barriers per tile.
+template <int PHASE>
+__device__ __forceinline__ void fused_stage32(Fused32Smem& sm, const FusedArgs& A, int cnt,
+                                              double& Bc, Atoms32& at) {
+  cp_async_wait_all();
   if (PHASE == 1) {
+    float mx = -INFINITY;
+    for (int t = threadIdx.x; t < cnt; t += kT) mx = fmaxf(mx, __double2float_ru(sm.rawB2[t]));
     mx = warp_max(mx);
     if ((threadIdx.x & 31) == 0) sm.wmax[threadIdx.x >> 5] = mx;
   }
@@ -1141,20 +1142,17 @@ __device__ __forceinline__ void fused_stage32(Fused32Smem& sm, const FusedArgs& 
     }
   }
   const double o0 = sm.R.o[0], o1 = sm.R.o[1], o2 = sm.R.o[2];
-#pragma unroll
-  for (int u = 0; u < kPer; ++u) {
-    const int t = threadIdx.x + u * kT;
-    if (t < cnt) {
-      const float f0 = -static_cast<float>(y[u].x - o0), f1 = -static_cast<float>(y[u].y - o1),
-                  f2 = -static_cast<float>(y[u].z - o2);
-      const float w = static_cast<float>(b2[u] - Bc);
-      sm.tN0[t] = make_float4(f0, f0, f1, f1);
-      sm.tN1[t] = make_float4(f2, f2, w, w);
-      sm.tK[t] = k[u];
-      sm.tJ[t] = A.tperm[k[u]];
-    }
+  for (int t = threadIdx.x; t < cnt; t += kT) {
+    const double4 y = sm.rawY[t];
+    const float f0 = -static_cast<float>(y.x - o0), f1 = -static_cast<float>(y.y - o1),
+                f2 = -static_cast<float>(y.z - o2);
+    const float w = static_cast<float>(sm.rawB2[t] - Bc);
+    sm.tN0[t] = make_float4(f0, f0, f1, f1);
+    sm.tN1[t] = make_float4(f2, f2, w, w);
+    sm.tK[t] = sm.rawK[t];
+    sm.tJ[t] = sm.rawJ[t];
   }
-  __syncthreads();
+  __syncthreads();  // staged tile visible, landing zone free
 }
 
 // FP32x2 squared distances of item t to atoms (a, b) and the item's offset.
@@ -1272,10 +1270,13 @@ __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox&
     sm.rowStart[threadIdx.x] = st;
     sm.rowPref[threadIdx.x] = pre;
     if (threadIdx.x == 0) sm.rowPref[kT] = total;
-    __syncthreads();  // the staging loads read every thread's row range
+    __syncthreads();  // the prefetch reads every thread's row range
+    if (total > 0) fused_prefetch32(sm, A, 0, min(kTileT32, total));
     for (int base = 0; base < total; base += kTileT32) {
       const int cnt = min(kTileT32, total - base);
-      fused_stage32<PHASE>(sm, A, base, cnt, Bc, at);
+      fused_stage32<PHASE>(sm, A, cnt, Bc, at);
+      if (base + kTileT32 < total)
+        fused_prefetch32(sm, A, base + kTileT32, min(kTileT32, total - base - kTileT32));
       const int nsel = fused_cull(sm, cnt, wb, cull_thr, list);
       if (PHASE == 1) {
         float2 acc = make_float2(0.f, 0.f), cn = make_float2(0.f, 0.f);

@@ -725,8 +725,9 @@ template <int PHASE, bool PAIR, bool SAFE, bool DEBUG>
 __device__ __forceinline__ double2 step64d(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at,
                                            const Step32& K, bool wide, int t0, int t1, float2 d0,
                                            float2 d1, float2& cnt) {
+  // culled steps always hold accepted pairs (no all-out steps in practice):
+  // no vote on the work, masked pairs contribute +0
   bool k0a, k0b, k1a = false, k1b = false;
-  bool work;
   if (DEBUG || __any_sync(0xffffffffu, step_in_band<PAIR>(K, d0, d1))) {
     const unsigned in = slow_mask(sm, A, at.qa, at.qb, K, t0, t1, d0, d1, PAIR);
     k0a = in & 1u;
@@ -739,11 +740,7 @@ __device__ __forceinline__ double2 step64d(const FusedSmem& sm, const FusedArgs&
       if (k0b) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
       if (k1b) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
     }
-    work = __any_sync(0xffffffffu, in != 0u);
   } else {
-    float m = fminf(d0.x, d0.y);
-    if (PAIR) m = fminf(m, fminf(d1.x, d1.y));
-    work = __any_sync(0xffffffffu, m < K.lo);
     k0a = d0.x < K.lo;
     k0b = d0.y < K.lo;
     if (PAIR) {
@@ -752,7 +749,7 @@ __device__ __forceinline__ double2 step64d(const FusedSmem& sm, const FusedArgs&
     }
   }
   double2 out = make_double2(0.0, 0.0);
-  if (work) {
+  {
     const double4 y0 = sm.tD[t0];
     double sa0 = chain3(at.Xa, y0), sb0 = chain3(at.Xb, y0);
     if (wide) {
@@ -1183,7 +1180,6 @@ __device__ __forceinline__ float2 step32(const SM& sm, const FusedArgs& A, Atoms
   const float2 d0 = fused_d2w(sm, at, t0, w0);
   const float2 d1 = PAIR ? fused_d2w(sm, at, t1, w1) : d0;
   float2 i0, i1 = make_float2(0.f, 0.f);
-  bool work;
   if (DEBUG || __any_sync(0xffffffffu, step_in_band<PAIR>(K, d0, d1))) {
     const unsigned in = slow_mask(sm, A, at.qa, at.qb, K, t0, t1, d0, d1, PAIR);
     i0 = make_float2((in & 1u) ? 1.f : 0.f, (in & 2u) ? 1.f : 0.f);
@@ -1194,18 +1190,12 @@ __device__ __forceinline__ float2 step32(const SM& sm, const FusedArgs& A, Atoms
       if (in & 2u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
       if (in & 8u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
     }
-    work = __any_sync(0xffffffffu, in != 0u);
   } else {
-    float m = fminf(d0.x, d0.y);
-    if (PAIR) m = fminf(m, fminf(d1.x, d1.y));
-    work = __any_sync(0xffffffffu, m < K.lo);
-    if (work) {
-      i0 = make_float2(sat_fma(d0.x, K.nbig, K.lobig), sat_fma(d0.y, K.nbig, K.lobig));
-      if (PAIR) i1 = make_float2(sat_fma(d1.x, K.nbig, K.lobig), sat_fma(d1.y, K.nbig, K.lobig));
-    }
+    i0 = make_float2(sat_fma(d0.x, K.nbig, K.lobig), sat_fma(d0.y, K.nbig, K.lobig));
+    if (PAIR) i1 = make_float2(sat_fma(d1.x, K.nbig, K.lobig), sat_fma(d1.y, K.nbig, K.lobig));
   }
   float2 out = make_float2(0.f, 0.f);
-  if (work) {
+  {
     const float2 s0 = __ffma2_rn(K.nc2, d0, make_float2(w0, w0));
     const float2 e0 = __fmul2_rn(make_float2(fast_ex2(s0.x), fast_ex2(s0.y)), i0);
     float2 e1 = make_float2(0.f, 0.f);

@@ -721,14 +721,15 @@ __device__ __noinline__ unsigned slow_mask(const SM& sm, const FusedArgs& A, int
 // SAFE: CTA whose exponents may leave [-1020, 1000] (spread chunk or huge
 // psi range): per-atom shift carried in every exponent when wide, and the
 // exponent split clamped.
-template <int PHASE, bool PAIR, bool SAFE, bool DEBUG>
+template <int PHASE, bool PAIR, bool SAFE, bool DEBUG, bool CHECK = true>
 __device__ __forceinline__ double2 step64d(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at,
                                            const Step32& K, bool wide, int t0, int t1, float2 d0,
-                                           float2 d1, float2& cnt) {
+                                           float2 d1, float2& cnt, bool& hit) {
   // culled steps always hold accepted pairs (no all-out steps in practice):
   // no vote on the work, masked pairs contribute +0
   bool k0a, k0b, k1a = false, k1b = false;
-  if (DEBUG || __any_sync(0xffffffffu, step_in_band<PAIR>(K, d0, d1))) {
+  if (DEBUG || (CHECK && __any_sync(0xffffffffu, step_in_band<PAIR>(K, d0, d1)))) {
+    hit = true;
     const unsigned in = slow_mask(sm, A, at.qa, at.qb, K, t0, t1, d0, d1, PAIR);
     k0a = in & 1u;
     k0b = in & 2u;
@@ -782,22 +783,23 @@ __device__ __forceinline__ double2 step64d(const FusedSmem& sm, const FusedArgs&
   return out;
 }
 
-template <int PHASE, bool PAIR, bool SAFE, bool DEBUG>
+template <int PHASE, bool PAIR, bool SAFE, bool DEBUG, bool CHECK = true>
 __device__ __forceinline__ double2 step64(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at,
                                           const Step32& K, bool wide, int t0, int t1,
-                                          float2& cnt) {
+                                          float2& cnt, bool& hit) {
   const float2 d0 = fused_d2(sm, at, t0);
   const float2 d1 = PAIR ? fused_d2(sm, at, t1) : d0;
-  return step64d<PHASE, PAIR, SAFE, DEBUG>(sm, A, at, K, wide, t0, t1, d0, d1, cnt);
+  return step64d<PHASE, PAIR, SAFE, DEBUG, CHECK>(sm, A, at, K, wide, t0, t1, d0, d1, cnt, hit);
 }
 
-template <bool SAFE, bool DEBUG>
+template <bool SAFE, bool DEBUG, bool CHECK>
 __device__ __forceinline__ void batch64(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at,
                                         const Step32& K, bool wide, const ListT* list,
                                         int b0, int nsel, double* col) {
   const int lane = threadIdx.x & 31;
   double v[16];
   float2 dummy = make_float2(0.f, 0.f);
+  bool hit = false;
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
     const int i = b0 + 2 * p;
@@ -806,7 +808,7 @@ __device__ __forceinline__ void batch64(const FusedSmem& sm, const FusedArgs& A,
       // a lone last item pairs with itself; its second column is dropped
       const int t0 = list[i];
       const int t1 = i + 1 < nsel ? list[i + 1] : t0;
-      val = step64<2, true, SAFE, DEBUG>(sm, A, at, K, wide, t0, t1, dummy);
+      val = step64<2, true, SAFE, DEBUG, CHECK>(sm, A, at, K, wide, t0, t1, dummy, hit);
     }
     v[2 * p] = val.x;
     v[2 * p + 1] = i + 1 < nsel ? val.y : 0.0;
@@ -847,6 +849,7 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
         // software-pipelined: the next step's list entries and distances are
         // loaded before this step's exponentials (hides LDS latency)
         float2 cn = make_float2(0.f, 0.f);
+        bool hit = false;
         int i = 0;
         if (nsel >= 2) {
           int t0 = list[0], t1 = list[1];
@@ -860,17 +863,20 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
               d0 = fused_d2(sm, at, t0);
               d1 = fused_d2(sm, at, t1);
             }
-            step64d<1, true, SAFE, DEBUG>(sm, A, at, K, wide, c0, c1, e0, e1, cn);
+            step64d<1, true, SAFE, DEBUG>(sm, A, at, K, wide, c0, c1, e0, e1, cn, hit);
           }
         }
-        if (i < nsel) step64<1, false, SAFE, DEBUG>(sm, A, at, K, wide, list[i], list[i], cn);
+        if (i < nsel) step64<1, false, SAFE, DEBUG>(sm, A, at, K, wide, list[i], list[i], cn, hit);
         at.ca += static_cast<uint32_t>(cn.x);
         at.cb += static_cast<uint32_t>(cn.y);
       } else {
         double* const col = sm.colW[warp];
         for (int s = lane; s < cnt; s += 32) col[s] = 0.0;
         __syncwarp();
-        for (int b0 = 0; b0 < nsel; b0 += 16) batch64<SAFE, DEBUG>(sm, A, at, K, wide, list, b0, nsel, col);
+        // (a band-free second instantiation, as in fused_scan32, costs more in
+        // instruction-cache misses than it saves here: measured +6 %)
+        for (int b0 = 0; b0 < nsel; b0 += 16)
+          batch64<SAFE, DEBUG, true>(sm, A, at, K, wide, list, b0, nsel, col);
         __syncthreads();
         for (int s = threadIdx.x; s < cnt; s += kT) {
           const double c = ((sm.colW[0][s] + sm.colW[1][s]) + sm.colW[2][s]) + sm.colW[3][s];
@@ -1172,15 +1178,16 @@ __device__ __forceinline__ float2 fused_d2w(const SM& sm, const Atoms32& at, int
 // weighted column values of t0 and t1.  Pairs in the FP32 error band take
 // the exact fp64 predicate (warp-uniform slow path, also used in DEBUG
 // builds for the candidate hashes).
-template <int PHASE, bool PAIR, bool DEBUG, class SM>
+template <int PHASE, bool PAIR, bool DEBUG, bool CHECK, class SM>
 __device__ __forceinline__ float2 step32(const SM& sm, const FusedArgs& A, Atoms32& at,
                                          const Step32& K, int t0, int t1, float2& acc,
-                                         float2& cnt) {
+                                         float2& cnt, bool& hit) {
   float w0, w1 = 0.f;
   const float2 d0 = fused_d2w(sm, at, t0, w0);
   const float2 d1 = PAIR ? fused_d2w(sm, at, t1, w1) : d0;
   float2 i0, i1 = make_float2(0.f, 0.f);
-  if (DEBUG || __any_sync(0xffffffffu, step_in_band<PAIR>(K, d0, d1))) {
+  if (DEBUG || (CHECK && __any_sync(0xffffffffu, step_in_band<PAIR>(K, d0, d1)))) {
+    hit = true;
     const unsigned in = slow_mask(sm, A, at.qa, at.qb, K, t0, t1, d0, d1, PAIR);
     i0 = make_float2((in & 1u) ? 1.f : 0.f, (in & 2u) ? 1.f : 0.f);
     if (PAIR) i1 = make_float2((in & 4u) ? 1.f : 0.f, (in & 8u) ? 1.f : 0.f);
@@ -1218,21 +1225,22 @@ __device__ __forceinline__ float2 step32(const SM& sm, const FusedArgs& A, Atoms
   return out;
 }
 
-template <bool FULL, bool DEBUG, class SM>
+template <bool FULL, bool DEBUG, bool CHECK, class SM>
 __device__ __forceinline__ void batch32(const SM& sm, const FusedArgs& A, Atoms32& at,
                                         const Step32& K, const ListT* list, int b0, int nsel,
                                         float* col) {
   const int lane = threadIdx.x & 31;
   float v[16];
   float2 dummy = make_float2(0.f, 0.f), dummy2 = dummy;
+  bool hit = false;
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
     const int i = b0 + 2 * p;
     float2 val = make_float2(0.f, 0.f);
     if (FULL || i + 1 < nsel)
-      val = step32<2, true, DEBUG>(sm, A, at, K, list[i], list[i + 1], dummy, dummy2);
+      val = step32<2, true, DEBUG, CHECK>(sm, A, at, K, list[i], list[i + 1], dummy, dummy2, hit);
     else if (i < nsel)
-      val = step32<2, false, DEBUG>(sm, A, at, K, list[i], list[i], dummy, dummy2);
+      val = step32<2, false, DEBUG, CHECK>(sm, A, at, K, list[i], list[i], dummy, dummy2, hit);
     v[2 * p] = val.x;
     v[2 * p + 1] = val.y;
   }
@@ -1243,7 +1251,10 @@ __device__ __forceinline__ void batch32(const SM& sm, const FusedArgs& A, Atoms3
 
 template <int PHASE, bool DEBUG>
 __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox& wb,
-                             float cull_thr, double& Bc, Atoms32& at) {
+                             float cull_thr, double& Bc, Atoms32& at, unsigned& bandmask) {
+  // bandmask bit i: phase 1 met a pair in the FP32 error band in this warp's
+  // tile i; phase 2 re-tests only those tiles (same tiles, same lists)
+  int tix = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   ListT* const list = sm.wlist[warp];
   Step32 K = make_step(at.lo_thr, at.hi_thr);
@@ -1270,9 +1281,12 @@ __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox&
       const int nsel = fused_cull(sm, cnt, wb, cull_thr, list);
       if (PHASE == 1) {
         float2 acc = make_float2(0.f, 0.f), cn = make_float2(0.f, 0.f);
+        bool hit = false;
         int i = 0;
-        for (; i + 1 < nsel; i += 2) step32<1, true, DEBUG>(sm, A, at, K, list[i], list[i + 1], acc, cn);
-        if (i < nsel) step32<1, false, DEBUG>(sm, A, at, K, list[i], list[i], acc, cn);
+        for (; i + 1 < nsel; i += 2)
+          step32<1, true, DEBUG, true>(sm, A, at, K, list[i], list[i + 1], acc, cn, hit);
+        if (i < nsel) step32<1, false, DEBUG, true>(sm, A, at, K, list[i], list[i], acc, cn, hit);
+        if (hit && tix < 32) bandmask |= 1u << tix;
         at.Sa += static_cast<double>(acc.x);
         at.Sb += static_cast<double>(acc.y);
         at.ca += static_cast<uint32_t>(cn.x);
@@ -1282,8 +1296,13 @@ __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox&
         for (int s = lane; s < cnt; s += 32) col[s] = 0.f;
         __syncwarp();
         int b0 = 0;
-        for (; b0 + 16 <= nsel; b0 += 16) batch32<true, DEBUG>(sm, A, at, K, list, b0, nsel, col);
-        if (b0 < nsel) batch32<false, DEBUG>(sm, A, at, K, list, b0, nsel, col);
+        if (tix >= 32 || ((bandmask >> tix) & 1u)) {
+          for (; b0 + 16 <= nsel; b0 += 16) batch32<true, DEBUG, true>(sm, A, at, K, list, b0, nsel, col);
+          if (b0 < nsel) batch32<false, DEBUG, true>(sm, A, at, K, list, b0, nsel, col);
+        } else {
+          for (; b0 + 16 <= nsel; b0 += 16) batch32<true, DEBUG, false>(sm, A, at, K, list, b0, nsel, col);
+          if (b0 < nsel) batch32<false, DEBUG, false>(sm, A, at, K, list, b0, nsel, col);
+        }
         __syncthreads();
         for (int s = threadIdx.x; s < cnt; s += kT) {
           const double c = ((static_cast<double>(sm.colW[0][s]) + sm.colW[1][s]) + sm.colW[2][s]) +
@@ -1291,6 +1310,7 @@ __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox&
           if (c > 0.0) fp_add(A.gacc + 3 * static_cast<size_t>(sm.tJ[s]), c);
         }
       }
+      ++tix;
     }
     __syncthreads();
   }
@@ -1340,7 +1360,8 @@ trunc_fused32(FusedArgs A) {
   const float cull_thr = sm.R.hi_thr * 1.0001f;
   double Bc = -0x1p1000;  // running CTA shift (log2 units)
 
-  fused_scan32<1, DEBUG>(sm, A, wb, cull_thr, Bc, at);
+  unsigned bandmask = 0;
+  fused_scan32<1, DEBUG>(sm, A, wb, cull_thr, Bc, at, bandmask);
 
   double wa, wb2;
   fused_finalize<DEBUG>(A, Bc, true, va, at.ca != 0u, static_cast<double>(at.ca + at.cb), at.ca,
@@ -1350,7 +1371,7 @@ trunc_fused32(FusedArgs A) {
   at.wa = static_cast<float>(wa);
   at.wb = static_cast<float>(wb2);
 
-  fused_scan32<2, DEBUG>(sm, A, wb, cull_thr, Bc, at);
+  fused_scan32<2, DEBUG>(sm, A, wb, cull_thr, Bc, at, bandmask);
 }
 
 __global__ void trunc_assemble_fp(const unsigned long long* __restrict__ gacc, int n,

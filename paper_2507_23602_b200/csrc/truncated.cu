@@ -584,6 +584,45 @@ __device__ __forceinline__ void fused_convert(FusedSmem& sm, const FusedArgs& A,
   }
 }
 
+// Culling with full-in split: staged targets whose FARTHEST point of the
+// warp box is still inside lo (conservatively: far^2 < full_thr) are in for
+// every atom of the warp, with no per-pair test; they go to the back of the
+// list (list[cap - 1 - i], i < *nfull), the others to the front.
+template <class SM>
+__device__ __forceinline__ int fused_cull2(const SM& sm, int cnt, const WarpBox& w, float thr,
+                                           float full_thr, ListT* __restrict__ list, int cap,
+                                           int* nfull) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  int nsel = 0, nf = 0;
+  for (int g = 0; g < cnt; g += 32) {
+    const int t = g + lane;
+    bool keep = false, full = false;
+    if (t < cnt) {
+      const float4 a = sm.tN0[t];
+      const float bz = sm.tN1[t].x;
+      const float dx = fmaxf(fmaxf(w.lo0 + a.x, -a.x - w.hi0), 0.f);
+      const float dy = fmaxf(fmaxf(w.lo1 + a.z, -a.z - w.hi1), 0.f);
+      const float dz = fmaxf(fmaxf(w.lo2 + bz, -bz - w.hi2), 0.f);
+      keep = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= thr;
+      const float fx = fmaxf(-a.x - w.lo0, w.hi0 + a.x);
+      const float fy = fmaxf(-a.z - w.lo1, w.hi1 + a.z);
+      const float fz = fmaxf(-bz - w.lo2, w.hi2 + bz);
+      full = keep && fmaf(fz, fz, fmaf(fy, fy, fx * fx)) < full_thr;
+      keep = keep && !full;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    const unsigned mf = __ballot_sync(0xffffffffu, full);
+    if (keep) list[nsel + __popc(m & lt)] = static_cast<ListT>(t);
+    if (full) list[cap - 1 - (nf + __popc(mf & lt))] = static_cast<ListT>(t);
+    nsel += __popc(m);
+    nf += __popc(mf);
+  }
+  __syncwarp();
+  *nfull = nf;
+  return nsel;
+}
+
 template <class SM>
 __device__ __forceinline__ int fused_cull(const SM& sm, int cnt, const WarpBox& w,
                                           float thr, ListT* __restrict__ list) {
@@ -721,34 +760,12 @@ __device__ __noinline__ unsigned slow_mask(const SM& sm, const FusedArgs& A, int
 // SAFE: CTA whose exponents may leave [-1020, 1000] (spread chunk or huge
 // psi range): per-atom shift carried in every exponent when wide, and the
 // exponent split clamped.
-template <int PHASE, bool PAIR, bool SAFE, bool DEBUG, bool CHECK = true>
-__device__ __forceinline__ double2 step64d(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at,
-                                           const Step32& K, bool wide, int t0, int t1, float2 d0,
-                                           float2 d1, float2& cnt, bool& hit) {
-  // culled steps always hold accepted pairs (no all-out steps in practice):
-  // no vote on the work, masked pairs contribute +0
-  bool k0a, k0b, k1a = false, k1b = false;
-  if (DEBUG || (CHECK && __any_sync(0xffffffffu, step_in_band<PAIR>(K, d0, d1)))) {
-    hit = true;
-    const unsigned in = slow_mask(sm, A, at.qa, at.qb, K, t0, t1, d0, d1, PAIR);
-    k0a = in & 1u;
-    k0b = in & 2u;
-    k1a = in & 4u;
-    k1b = in & 8u;
-    if (DEBUG && PHASE == 1) {
-      if (k0a) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
-      if (k1a) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
-      if (k0b) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
-      if (k1b) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
-    }
-  } else {
-    k0a = d0.x < K.lo;
-    k0b = d0.y < K.lo;
-    if (PAIR) {
-      k1a = d1.x < K.lo;
-      k1b = d1.y < K.lo;
-    }
-  }
+// The exponential part of a step for given pair predicates (kxy: item x,
+// atom y).
+template <int PHASE, bool PAIR, bool SAFE>
+__device__ __forceinline__ double2 exp_part64(const FusedSmem& sm, FusedAtoms& at, bool wide,
+                                              int t0, int t1, bool k0a, bool k0b, bool k1a,
+                                              bool k1b, float2& cnt) {
   double2 out = make_double2(0.0, 0.0);
   {
     const double4 y0 = sm.tD[t0];
@@ -781,6 +798,37 @@ __device__ __forceinline__ double2 step64d(const FusedSmem& sm, const FusedArgs&
     }
   }
   return out;
+}
+
+template <int PHASE, bool PAIR, bool SAFE, bool DEBUG, bool CHECK = true>
+__device__ __forceinline__ double2 step64d(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at,
+                                           const Step32& K, bool wide, int t0, int t1, float2 d0,
+                                           float2 d1, float2& cnt, bool& hit) {
+  // culled steps always hold accepted pairs (no all-out steps in practice):
+  // no vote on the work, masked pairs contribute +0
+  bool k0a, k0b, k1a = false, k1b = false;
+  if (DEBUG || (CHECK && __any_sync(0xffffffffu, step_in_band<PAIR>(K, d0, d1)))) {
+    hit = true;
+    const unsigned in = slow_mask(sm, A, at.qa, at.qb, K, t0, t1, d0, d1, PAIR);
+    k0a = in & 1u;
+    k0b = in & 2u;
+    k1a = in & 4u;
+    k1b = in & 8u;
+    if (DEBUG && PHASE == 1) {
+      if (k0a) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
+      if (k1a) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
+      if (k0b) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
+      if (k1b) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
+    }
+  } else {
+    k0a = d0.x < K.lo;
+    k0b = d0.y < K.lo;
+    if (PAIR) {
+      k1a = d1.x < K.lo;
+      k1b = d1.y < K.lo;
+    }
+  }
+  return exp_part64<PHASE, PAIR, SAFE>(sm, at, wide, t0, t1, k0a, k0b, k1a, k1b, cnt);
 }
 
 template <int PHASE, bool PAIR, bool SAFE, bool DEBUG, bool CHECK = true>
@@ -818,6 +866,32 @@ __device__ __forceinline__ void batch64(const FusedSmem& sm, const FusedArgs& A,
   if (!(lane & 1) && item < nsel) col[list[item]] = tot;
 }
 
+// Phase-2 batch over full-in items (every pair of valid atoms taken).
+template <bool SAFE>
+__device__ __forceinline__ void batch64_full(const FusedSmem& sm, FusedAtoms& at, bool wide,
+                                             const ListT* full, int b0, int nfull, bool va, bool vb,
+                                             double* col) {
+  const int lane = threadIdx.x & 31;
+  double v[16];
+  float2 dummy = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int i = b0 + 2 * p;
+    double2 val = make_double2(0.0, 0.0);
+    if (i < nfull) {
+      const int t0 = full[-i];
+      const bool two = i + 1 < nfull;
+      const int t1 = two ? full[-(i + 1)] : t0;
+      val = exp_part64<2, true, SAFE>(sm, at, wide, t0, t1, va, vb, two && va, two && vb, dummy);
+    }
+    v[2 * p] = val.x;
+    v[2 * p + 1] = val.y;
+  }
+  const double tot = butterfly16(v);
+  const int item = b0 + (lane >> 1);
+  if (!(lane & 1) && item < nfull) col[full[-item]] = tot;
+}
+
 template <int PHASE, bool SAFE, bool DEBUG>
 __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb, float cull_thr,
                            double B, FusedAtoms& at) {
@@ -825,6 +899,18 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
   ListT* const list = sm.wlist[warp];
   const bool wide = SAFE && sm.R.wide;
   const Step32 K = make_step(at.lo_thr, at.hi_thr);
+  // Full-in split only when the ball is large against the warp box (r > 7
+  // half-diagonals, e.g. cfg3: ~half the culled targets are full-in, -6 %);
+  // for smaller ratios (cfg5) the split list handling costs more than the
+  // skipped pre-tests (+5 %).
+  float full_thr = -1.0f;
+  if (!DEBUG && at.lo_thr > 0.f) {
+    const float hx = wb.hi0 - wb.lo0, hy = wb.hi1 - wb.lo1, hz = wb.hi2 - wb.lo2;
+    const float hd2 = 0.25f * fmaf(hz, hz, fmaf(hy, hy, hx * hx));
+    if (at.lo_thr > 49.0f * hd2) full_thr = at.lo_thr * (1.0f - 1e-5f);
+  }
+  const ListT* const full = list + (kTileT - 1);  // full-in items: full[-i]
+  const bool va = at.qa < A.nq, vb = at.qb < A.nq;
   const int ny = sm.R.c_hi[1] - sm.R.c_lo[1] + 1;
   const int nrows = ny * (sm.R.c_hi[2] - sm.R.c_lo[2] + 1);
   for (int rb = 0; rb < nrows; rb += kT) {
@@ -844,7 +930,8 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
       fused_convert(sm, A, B, cnt);
       __syncthreads();  // staged tile visible, landing zone free
       if (base + kTileT < total) fused_prefetch(sm, A, base + kTileT, min(kTileT, total - base - kTileT));
-      const int nsel = fused_cull(sm, cnt, wb, cull_thr, list);
+      int nfull = 0;
+      const int nsel = fused_cull2(sm, cnt, wb, cull_thr, full_thr, list, kTileT, &nfull);
       if (PHASE == 1) {
         // software-pipelined: the next step's list entries and distances are
         // loaded before this step's exponentials (hides LDS latency)
@@ -867,6 +954,11 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
           }
         }
         if (i < nsel) step64<1, false, SAFE, DEBUG>(sm, A, at, K, wide, list[i], list[i], cn, hit);
+        int f = 0;
+        for (; f + 1 < nfull; f += 2)
+          exp_part64<1, true, SAFE>(sm, at, wide, full[-f], full[-(f + 1)], va, vb, va, vb, cn);
+        if (f < nfull)
+          exp_part64<1, false, SAFE>(sm, at, wide, full[-f], full[-f], va, vb, false, false, cn);
         at.ca += static_cast<uint32_t>(cn.x);
         at.cb += static_cast<uint32_t>(cn.y);
       } else {
@@ -877,6 +969,7 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
         // instruction-cache misses than it saves here: measured +6 %)
         for (int b0 = 0; b0 < nsel; b0 += 16)
           batch64<SAFE, DEBUG, true>(sm, A, at, K, wide, list, b0, nsel, col);
+        for (int b0 = 0; b0 < nfull; b0 += 16) batch64_full<SAFE>(sm, at, wide, full, b0, nfull, va, vb, col);
         __syncthreads();
         for (int s = threadIdx.x; s < cnt; s += kT) {
           const double c = ((sm.colW[0][s] + sm.colW[1][s]) + sm.colW[2][s]) + sm.colW[3][s];

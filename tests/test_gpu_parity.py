@@ -302,3 +302,33 @@ def test_nccl_collective_path_single_rank():
         b = gpu_eval(rs.Context.default(0), A, M, T, W, psi, 0.01, cutoff)
         assert a["J"] == b["J"] and a["D"] == b["D"] and a["candidate_pairs"] == b["candidate_pairs"]
         assert np.array_equal(a["gradient"], b["gradient"])
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_full_in_split_parity(precision):
+    """Dense atom cluster with a ball much larger than a warp's atom box
+    (r ~ 8 half-diagonals): most culled targets are full-in for the whole
+    warp and skip the per-pair pre-test (truncated.cu fused_cull2); counts,
+    hashes and values must still match the oracle."""
+    ctx = rs.Context(0)
+    ctx.set_precision(precision)
+    rng = np.random.default_rng(2024)
+    A = 0.45 + 0.1 * rng.uniform(size=(60000, 3))  # warp boxes ~0.01 wide, r = 0.15
+    M = rng.uniform(size=60000) + 0.1
+    M /= M.sum()
+    T = rng.uniform(size=(5000, 3))
+    W = np.full(5000, 1 / 5000)
+    psi = rng.normal(0, 1e-3, size=5000)
+    eps, cutoff = 2e-3, 0.01125
+    atoms = rs.SourceAtoms(dim=3, points=A, masses=M)
+    tgt = rs.TargetMeasure(dim=3, points=T, weights=W)
+    res, cnt, hsh, _ = rs.evaluate_dual_debug(atoms, tgt, psi, eps, cutoff, ctx=ctx)
+    r = rs.evaluate_dual(atoms, tgt, rs.DualPotential(psi), rs.SolverConfig(epsilon=eps),
+                         rs.TruncationState(cutoff=cutoff), ctx=ctx)  # non-debug kernel (split active)
+    want = C.evaluate_dual(A, M, T, W, psi, eps, cutoff, per_atom=True, workers=8)
+    assert np.array_equal(cnt, want["count"]) and np.array_equal(hsh, want["hash"])
+    tol = TOL if precision == "fp64" else 2e-5
+    for got in (res, r):
+        g = dict(J=got.J, D=got.D, gradient=got.gradient, atoms_visited=got.atoms_visited,
+                 candidate_pairs=got.candidate_pairs, empty_candidate_atoms=got.empty_candidate_atoms)
+        assert_parity(g, want, marginal_scale(W, want["gradient"]), tol)

@@ -211,7 +211,8 @@ int rsot_cuda_plan_moments(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
  * relative of the reference.  RSOT_CUDA_PRECISION_FP32: truncated
  * evaluations form the exponent in FP32 and exponentiate with the hardware
  * ex2 (sums, J, D and the gradient accumulate in fp64; candidate sets stay
- * exact); deviation from fp64 ~1e-6 relative, asserted <= 2e-5 in the tests.
+ * exact); observed deviation from fp64 at the BASELINE configs: J 3e-9 - 1.5e-8
+ * relative, gradient 7e-8 of the marginal scale; asserted <= 2e-5 in the tests.
  * Dense evaluations (cutoff = +inf) always run in fp64.  BASELINE cfg5 asks
  * for both precisions; the reference has fp64 only. */
 #define RSOT_CUDA_PRECISION_FP64 0

@@ -1142,9 +1142,9 @@ trunc_fused(FusedArgs A) {
 // fp64 per-atom sums.  The shift B is per CTA: the running max of the staged
 // b2 (phase 1 rescales its sums when a tile raises it), so any psi range
 // keeps the sums in range.  Atoms whose sum falls below 2^-80 take the exact
-// fp64 path; empty sets use the same exact nearest kernel.  Expected
-// deviation from the fp64 result: ~1e-6 relative (FP32 distance and
-// exponent rounding); the tests assert 2e-5.
+// fp64 path; empty sets use the same exact nearest kernel.  Observed
+// deviation from the fp64 result (tools/fp32_error.py, cfg3/cfg5): J 3e-9 -
+// 1.5e-8 relative, gradient 7e-8 of the marginal scale; the tests assert 2e-5.
 
 struct Fused32Smem {
   float4 tN0[kTileT32];                  // {-y0', -y0', -y1', -y1'}

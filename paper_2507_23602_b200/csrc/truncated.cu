@@ -623,7 +623,9 @@ __device__ __forceinline__ int fused_cull2(const SM& sm, int cnt, const WarpBox&
   return nsel;
 }
 
-template <class SM>
+// SHIFT > 0: list entries are t << SHIFT (byte offsets into 16-byte arrays,
+// so the step's shared loads need no address arithmetic).
+template <class SM, int SHIFT = 0>
 __device__ __forceinline__ int fused_cull(const SM& sm, int cnt, const WarpBox& w,
                                           float thr, ListT* __restrict__ list) {
   const int lane = threadIdx.x & 31;
@@ -641,7 +643,7 @@ __device__ __forceinline__ int fused_cull(const SM& sm, int cnt, const WarpBox& 
       keep = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= thr;
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (keep) list[nsel + __popc(m & lt)] = static_cast<ListT>(t);
+    if (keep) list[nsel + __popc(m & lt)] = static_cast<ListT>(t << SHIFT);
     nsel += __popc(m);
   }
   __syncwarp();
@@ -1252,10 +1254,11 @@ __device__ __forceinline__ void fused_stage32(Fused32Smem& sm, const FusedArgs& 
 }
 
 // FP32x2 squared distances of item t to atoms (a, b) and the item's offset.
+// o: byte offset of the item (t << 4) into the 16-byte staged arrays.
 template <class SM>
-__device__ __forceinline__ float2 fused_d2w(const SM& sm, const Atoms32& at, int t, float& w) {
-  const float4 n01 = sm.tN0[t];
-  const float4 n2 = sm.tN1[t];
+__device__ __forceinline__ float2 fused_d2w(const SM& sm, const Atoms32& at, int o, float& w) {
+  const float4 n01 = *reinterpret_cast<const float4*>(reinterpret_cast<const char*>(sm.tN0) + o);
+  const float4 n2 = *reinterpret_cast<const float4*>(reinterpret_cast<const char*>(sm.tN1) + o);
   const float2 dx = __fadd2_rn(at.F0, make_float2(n01.x, n01.y));
   const float2 dy = __fadd2_rn(at.F1, make_float2(n01.z, n01.w));
   const float2 dz = __fadd2_rn(at.F2, make_float2(n2.x, n2.y));
@@ -1273,11 +1276,13 @@ __device__ __forceinline__ float2 fused_d2w(const SM& sm, const Atoms32& at, int
 // builds for the candidate hashes).
 template <int PHASE, bool PAIR, bool DEBUG, bool CHECK, class SM>
 __device__ __forceinline__ float2 step32(const SM& sm, const FusedArgs& A, Atoms32& at,
-                                         const Step32& K, int t0, int t1, float2& acc,
+                                         const Step32& K, int o0, int o1, float2& acc,
                                          float2& cnt, bool& hit) {
+  // o0, o1: byte offsets (t << 4) of the two items
   float w0, w1 = 0.f;
-  const float2 d0 = fused_d2w(sm, at, t0, w0);
-  const float2 d1 = PAIR ? fused_d2w(sm, at, t1, w1) : d0;
+  const float2 d0 = fused_d2w(sm, at, o0, w0);
+  const float2 d1 = PAIR ? fused_d2w(sm, at, o1, w1) : d0;
+  const int t0 = o0 >> 4, t1 = o1 >> 4;
   float2 i0, i1 = make_float2(0.f, 0.f);
   if (DEBUG || (CHECK && __any_sync(0xffffffffu, step_in_band<PAIR>(K, d0, d1)))) {
     hit = true;
@@ -1339,7 +1344,7 @@ __device__ __forceinline__ void batch32(const SM& sm, const FusedArgs& A, Atoms3
   }
   const float tot = butterfly16f(v);
   const int item = b0 + (lane >> 1);
-  if (!(lane & 1) && item < nsel) col[list[item]] = tot;
+  if (!(lane & 1) && item < nsel) col[list[item] >> 4] = tot;
 }
 
 template <int PHASE, bool DEBUG>
@@ -1371,7 +1376,7 @@ __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox&
       fused_stage32<PHASE>(sm, A, cnt, Bc, at);
       if (base + kTileT32 < total)
         fused_prefetch32(sm, A, base + kTileT32, min(kTileT32, total - base - kTileT32));
-      const int nsel = fused_cull(sm, cnt, wb, cull_thr, list);
+      const int nsel = fused_cull<Fused32Smem, 4>(sm, cnt, wb, cull_thr, list);
       if (PHASE == 1) {
         float2 acc = make_float2(0.f, 0.f), cn = make_float2(0.f, 0.f);
         bool hit = false;

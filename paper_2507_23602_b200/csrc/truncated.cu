@@ -1619,11 +1619,15 @@ int build_hilbert(TruncWorkspace& ws, const double4* pts, int n, PointOrders& po
   TCK(realloc_exact(po.ph, n));
   TCK(realloc_exact(po.perm_h, n));
   if (n > 0) {
+    // isotropic scale (the largest extent spans the curve): chunks of a flat
+    // point set (e.g. one rank's slab) stay compact in space instead of
+    // being squashed along the thin axis
+    double ext = 0.0;
+    for (int d = 0; d < 3; ++d) ext = std::max(ext, po.bbox_hi[d] - po.bbox_lo[d]);
     double sc[3];
-    for (int d = 0; d < 3; ++d) {
-      const double ext = po.bbox_hi[d] - po.bbox_lo[d];
-      sc[d] = ext > 0.0 ? static_cast<double>(1u << kHilBits) / ext : 0.0;
-    }
+    for (int d = 0; d < 3; ++d)
+      sc[d] = (ext > 0.0 && po.bbox_hi[d] > po.bbox_lo[d]) ? static_cast<double>(1u << kHilBits) / ext
+                                                           : 0.0;
     (note_launch(), hilbert_keys_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, n, po.bbox_lo[0], po.bbox_lo[1],
                                                         po.bbox_lo[2], sc[0], sc[1], sc[2],
                                                         ws.keys, ws.idx));

@@ -474,6 +474,7 @@ struct FusedArgs {
   unsigned long long* gacc;              // [3 N] fixed point, original index
   uint32_t* dbg_cnt; uint64_t* dbg_hash; double* dbg_logs;  // Hilbert order
   uint32_t* cnt_out;                     // 0 = empty candidate set (Hilbert order)
+  const int* chunk_order;                // CTA -> atom chunk (heaviest first) or null
 };
 
 __device__ __forceinline__ double chain3(const double (&X)[3], const double4& y) {
@@ -1070,7 +1071,8 @@ trunc_fused(FusedArgs A) {
   load_exp2_table(sm.tbl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   FusedAtoms at;
-  at.qa = blockIdx.x * kFA + warp * 64 + lane;
+  const int chunk = A.chunk_order ? A.chunk_order[blockIdx.x] : static_cast<int>(blockIdx.x);
+  at.qa = chunk * kFA + warp * 64 + lane;
   at.qb = at.qa + 32;
   const bool va = at.qa < A.nq, vb = at.qb < A.nq;
   double4 pa = va ? A.xs[at.qa] : make_double4(0, 0, 0, 0);
@@ -1420,7 +1422,8 @@ trunc_fused32(FusedArgs A) {
   __shared__ Fused32Smem sm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   Atoms32 at;
-  at.qa = blockIdx.x * kFA + warp * 64 + lane;
+  const int chunk = A.chunk_order ? A.chunk_order[blockIdx.x] : static_cast<int>(blockIdx.x);
+  at.qa = chunk * kFA + warp * 64 + lane;
   at.qb = at.qa + 32;
   const bool va = at.qa < A.nq, vb = at.qb < A.nq;
   const double4 pa = va ? A.xs[at.qa] : make_double4(0, 0, 0, 0);
@@ -1470,6 +1473,20 @@ trunc_fused32(FusedArgs A) {
   at.wb = static_cast<float>(wb2);
 
   fused_scan32<2, DEBUG>(sm, A, wb, cull_thr, Bc, at, bandmask);
+}
+
+// Chunk cost = the chunk's candidate pairs of the last evaluation; key =
+// (~cost << 32 | chunk) so an ascending sort puts the heaviest first.
+__global__ void chunk_cost_kernel(const double* __restrict__ cntd, int nq, int chunks,
+                                  uint64_t* __restrict__ keys, int* __restrict__ idx) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= chunks) return;
+  double s = 0.0;
+  const int q1 = min(nq, (c + 1) * kFA);
+  for (int q = c * kFA; q < q1; ++q) s += cntd[q];
+  const uint32_t cost = static_cast<uint32_t>(fmin(s, 4.0e9));
+  keys[c] = (static_cast<uint64_t>(~cost) << 32) | static_cast<uint32_t>(c);
+  idx[c] = c;
 }
 
 __global__ void trunc_assemble_fp(const unsigned long long* __restrict__ gacc, int n,
@@ -1880,6 +1897,14 @@ __global__ void plan_assemble_kernel(const unsigned long long* __restrict__ acc,
 
 }  // namespace
 
+void AtomCells::release() {
+  if (chunk_order) cudaFree(chunk_order);
+  chunk_order = nullptr;
+  chunks = 0;
+  order_valid = false;
+  PointOrders::release();
+}
+
 void PointOrders::release() {
   void* ptrs[] = {ph, perm_h, pc, perm_c, cell_start};
   for (void* p : ptrs)
@@ -1978,6 +2003,7 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
     A.dbg_cnt = reinterpret_cast<uint32_t*>(ws.S); A.dbg_hash = ws.hash; A.dbg_logs = ws.atomL;
     A.cnt_out = ws.cnt;
     const int nblk = (nq + kFA - 1) / kFA;
+    A.chunk_order = (ac.order_valid && ac.chunks == nblk) ? ac.chunk_order : nullptr;
     if (b.timing) cudaEventRecord(b.timing[1], s);
     if (fp32) {
       if (dbg)
@@ -2008,6 +2034,20 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
     launch_det_sum(ws.atomJ, nq, ws.red, b.res + n + kResJ, s);
     launch_det_sum(ws.atomD, nq, ws.red + 1024, b.res + n + kResD, s);
     launch_det_sum(ws.cntd, nq, ws.red + 2048, b.res + n + kResPairs, s);
+    // heaviest-first chunk schedule for the next evaluation of these atoms
+    if (nblk > 1) {
+      if (ac.chunks != nblk) {
+        if (ac.chunk_order) cudaFree(ac.chunk_order);
+        ac.chunk_order = nullptr;
+        TCK(cudaMalloc(&ac.chunk_order, sizeof(int) * nblk));
+        ac.chunks = nblk;
+      }
+      if (ensure_key_buffers(ws, nblk, err)) return 1;
+      (note_launch(), chunk_cost_kernel<<<(nblk + 255) / 256, 256, 0, s>>>(ws.cntd, nq, nblk, ws.keys, ws.idx));
+      if (radix_sort(ws, nblk, 64, s, err)) return 1;
+      TCK(cudaMemcpyAsync(ac.chunk_order, ws.idx2, sizeof(int) * nblk, cudaMemcpyDeviceToDevice, s));
+      ac.order_valid = true;
+    }
     launch_det_sum(ws.emptyd, nq, ws.red + 3072, b.res + n + kResEmpty, s);
     if (dbg) {
       (note_launch(), scatter_debug<uint32_t><<<(nq + 255) / 256, 256, 0, s>>>(

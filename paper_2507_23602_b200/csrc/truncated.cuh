@@ -55,7 +55,15 @@ struct TargetCells : PointOrders {
   double built_r = -1.0;
 };
 
-struct AtomCells : PointOrders {};
+struct AtomCells : PointOrders {
+  // CTA chunk schedule, heaviest first (from the previous evaluation's
+  // candidate counts): the longest chunks start in the first wave instead of
+  // forming the tail.  Scheduling only; results do not depend on it.
+  int* chunk_order = nullptr;
+  int chunks = 0;
+  bool order_valid = false;
+  void release();  // also frees the schedule
+};
 
 struct DebugOut {
   uint32_t* count = nullptr;  // [nq] original atom order

@@ -354,14 +354,27 @@ dense_passB(const double4* __restrict__ atoms, const double* __restrict__ atomLa
   }
   double o[3];
   block_bbox_center<kThreads>(lo[0], lo[1], lo[2], hi[0], hi[1], hi[2], sh, o);
+  double tmax = -INFINITY, tmin = INFINITY;
 #pragma unroll
   for (int k = 0; k < TPT; ++k) {
     const int j = j0 + k * kThreads;
     y[k][0] -= o[0]; y[k][1] -= o[1]; y[k][2] -= o[2];
     const double yy = fma(y[k][2], y[k][2], fma(y[k][1], y[k][1], y[k][0] * y[k][0]));
     T[k] = (j < n) ? fmax(fma(-c2, yy, b2[j]), -1.0e5) : -1.0e5;
+    if (j < n) {
+      tmax = fmax(tmax, T[k]);
+      tmin = fmin(tmin, T[k]);
+    }
     G[k] = 0.0;
   }
+  // Per-target factor out of the atom sum: G_k = 2^(T_k - Tc) sum_q
+  // 2^(x.y + lam_q + Tc) saves the per-pair DADD T_k + lam_q.  Safe when the
+  // CTA's T spread is bounded (the partial exponents then stay within
+  // [s, s + 900] of the full ones, s <= log2 m); CTA-uniform choice.
+  tmax = block_max<kThreads>(tmax, sh);
+  tmin = -block_max<kThreads>(-tmin, sh);
+  const bool fact = tmax > -1.0e300 && tmax - tmin <= 900.0;
+  const double Tc = fact ? tmax : 0.0;
   const double c2x2 = 2.0 * c2;
   const int q0 = blockIdx.y * per_split;
   const int q1 = min(nq, q0 + per_split);
@@ -385,7 +398,7 @@ dense_passB(const double4* __restrict__ atoms, const double* __restrict__ atomLa
       if (base + t < q1) {
         const double x0 = pre_x[u].x - o[0], x1 = pre_x[u].y - o[1], x2 = pre_x[u].z - o[2];
         const double xx = fma(x2, x2, fma(x1, x1, x0 * x0));
-        dst[t] = make_double4(c2x2 * x0, c2x2 * x1, c2x2 * x2, fma(-c2, xx, pre_l[u]));
+        dst[t] = make_double4(c2x2 * x0, c2x2 * x1, c2x2 * x2, fma(-c2, xx, pre_l[u]) + Tc);
       }
     }
   };
@@ -400,13 +413,25 @@ dense_passB(const double4* __restrict__ atoms, const double* __restrict__ atomLa
     const bool more = base + kTile < q1;
     if (more) fetch(base + kTile);
     const double4* cur = buf ? tile2 : tile;
+    if (fact) {
 #pragma unroll 4
-    for (int t = 0; t < cnt; ++t) {
-      const double4 X = cur[t];
+      for (int t = 0; t < cnt; ++t) {
+        const double4 X = cur[t];
 #pragma unroll
-      for (int k = 0; k < TPT; ++k) {
-        const double s = fma(X.x, y[k][0], fma(X.y, y[k][1], fma(X.z, y[k][2], T[k] + X.w)));
-        G[k] = exp2_acc(s, G[k], tbl);
+        for (int k = 0; k < TPT; ++k) {
+          const double s = fma(X.x, y[k][0], fma(X.y, y[k][1], fma(X.z, y[k][2], X.w)));
+          G[k] = exp2_acc(s, G[k], tbl);
+        }
+      }
+    } else {
+#pragma unroll 4
+      for (int t = 0; t < cnt; ++t) {
+        const double4 X = cur[t];
+#pragma unroll
+        for (int k = 0; k < TPT; ++k) {
+          const double s = fma(X.x, y[k][0], fma(X.y, y[k][1], fma(X.z, y[k][2], T[k] + X.w)));
+          G[k] = exp2_acc(s, G[k], tbl);
+        }
       }
     }
     if (more) stage(buf ? tile : tile2, base + kTile);
@@ -416,6 +441,7 @@ dense_passB(const double4* __restrict__ atoms, const double* __restrict__ atomLa
 #pragma unroll
   for (int k = 0; k < TPT; ++k) {
     const int j = j0 + k * kThreads;
+    if (fact) G[k] *= exp2_acc(T[k] - Tc, 0.0, tbl);  // 2^(T_k - Tc), T_k - Tc in [-900, 0]
     if (j < n) partG[(size_t)blockIdx.y * n + j] = G[k];
   }
 }

@@ -523,19 +523,20 @@ DenseLaunch plan_dense(int nq, int n, int num_sms) {
     return p;
   }
   // Enough CTAs for ~16 waves of ~6 resident CTAs per SM, while keeping
-  // at least 512 targets (pass A) / 1024 atoms (pass B) per CTA.
+  // at least 256 targets (pass A) / 256 atoms (pass B) per CTA (small
+  // shards, e.g. 1/8 of cfg2 per GPU, otherwise leave a one-wave tail).
   const long want = 16L * num_sms * 6;
-  p.apt = (nq >= 2L * 256 * num_sms) ? 2 : 1;
+  p.apt = (nq >= 16L * 256) ? 2 : 1;
   const long ablocks = (nq + kThreads * p.apt - 1) / (kThreads * p.apt);
   long sa = (want + ablocks - 1) / ablocks;
-  long max_sa = (n + 511) / 512;
+  long max_sa = (n + 255) / 256;
   if (sa > max_sa) sa = max_sa;
   if (sa < 1) sa = 1;
   p.splitsA = static_cast<int>(sa);
   p.tpt = (n >= 16L * 256) ? 2 : 1;
   const long tblocks = (n + kThreads * p.tpt - 1) / (kThreads * p.tpt);
   long sb = (want + tblocks - 1) / tblocks;
-  long max_sb = (nq + 1023) / 1024;
+  long max_sb = (nq + 255) / 256;
   if (sb > max_sb) sb = max_sb;
   if (sb < 1) sb = 1;
   p.splitsB = static_cast<int>(sb);

@@ -332,3 +332,47 @@ def test_full_in_split_parity(precision):
         g = dict(J=got.J, D=got.D, gradient=got.gradient, atoms_visited=got.atoms_visited,
                  candidate_pairs=got.candidate_pairs, empty_candidate_atoms=got.empty_candidate_atoms)
         assert_parity(g, want, marginal_scale(W, want["gradient"]), tol)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_edge_geometries(precision):
+    """Duplicate targets (nearest ties -> lowest index), atoms far outside the
+    target box (clamped cells), a cutoff that empties most candidate sets,
+    and a 2D instance: selection and values against the oracle."""
+    ctx = rs.Context(0)
+    ctx.set_precision(precision)
+    tol = TOL if precision == "fp64" else 2e-5
+    rng = np.random.default_rng(77)
+    T = rng.uniform(size=(800, 3))
+    T[400:] = T[:400]  # every target duplicated
+    A = np.vstack([rng.uniform(size=(3000, 3)), rng.uniform(-2.0, 3.0, size=(500, 3))])
+    M = rng.uniform(size=3500) + 0.1
+    M /= M.sum()
+    W = rng.uniform(size=800) + 0.1
+    W /= W.sum()
+    psi = rng.normal(0, 0.02, size=800)
+    for eps, cutoff in ((0.01, 0.002), (0.01, 1e-5), (0.05, 0.05)):
+        atoms = rs.SourceAtoms(dim=3, points=A, masses=M)
+        tgt = rs.TargetMeasure(dim=3, points=T, weights=W)
+        res, cnt, hsh, _ = rs.evaluate_dual_debug(atoms, tgt, psi, eps, cutoff, ctx=ctx)
+        want = C.evaluate_dual(A, M, T, W, psi, eps, cutoff, per_atom=True)
+        assert np.array_equal(cnt, want["count"]) and np.array_equal(hsh, want["hash"])
+        got = dict(J=res.J, D=res.D, gradient=res.gradient, atoms_visited=res.atoms_visited,
+                   candidate_pairs=res.candidate_pairs, empty_candidate_atoms=res.empty_candidate_atoms)
+        assert_parity(got, want, marginal_scale(W, want["gradient"]), tol)
+    # 2D, larger
+    A2 = np.zeros((40000, 3))
+    A2[:, :2] = rng.uniform(size=(40000, 2))
+    T2 = np.zeros((6000, 3))
+    T2[:, :2] = rng.uniform(size=(6000, 2)) ** 2  # skewed
+    M2 = np.full(40000, 1 / 40000)
+    W2 = np.full(6000, 1 / 6000)
+    psi2 = rng.normal(0, 1e-3, size=6000)
+    atoms = rs.SourceAtoms(dim=2, points=A2, masses=M2)
+    tgt = rs.TargetMeasure(dim=2, points=T2, weights=W2)
+    res, cnt, hsh, _ = rs.evaluate_dual_debug(atoms, tgt, psi2, 1e-3, 0.004, ctx=ctx)
+    want = C.evaluate_dual(A2, M2, T2, W2, psi2, 1e-3, 0.004, per_atom=True, workers=8)
+    assert np.array_equal(cnt, want["count"]) and np.array_equal(hsh, want["hash"])
+    got = dict(J=res.J, D=res.D, gradient=res.gradient, atoms_visited=res.atoms_visited,
+               candidate_pairs=res.candidate_pairs, empty_candidate_atoms=res.empty_candidate_atoms)
+    assert_parity(got, want, marginal_scale(W2, want["gradient"]), tol)

@@ -364,7 +364,8 @@ int rsot_cuda_ctx_set_comm(rsot_cuda_ctx* c, int rank, int world,
     return fail(RSOT_CUDA_INVALID_ARGUMENT, "bad rank/world");
   c->rank = rank;
   c->world = world;
-  if (world == 1) return RSOT_CUDA_OK;
+  // (a 1-rank communicator is created too: it runs the same gather +
+  // rank-ordered sum, which lets a single GPU exercise the collective path)
   NcclApi& api = nccl();
   if (!api.ok) return fail(RSOT_CUDA_RUNTIME_ERROR, "libnccl.so.2 not loadable");
   const int rc = set_device(c);

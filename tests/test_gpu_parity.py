@@ -302,6 +302,9 @@ def test_nccl_collective_path_single_rank():
         b = gpu_eval(rs.Context.default(0), A, M, T, W, psi, 0.01, cutoff)
         assert a["J"] == b["J"] and a["D"] == b["D"] and a["candidate_pairs"] == b["candidate_pairs"]
         assert np.array_equal(a["gradient"], b["gradient"])
+    atoms = rs.SourceAtoms(dim=3, points=A, masses=M)
+    tgt = rs.TargetMeasure(dim=3, points=T, weights=W)
+    assert rs.covering_cost(atoms, tgt, ctx=ctx1) == rs.covering_cost(atoms, tgt)  # max-allreduce path
 
 
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])

@@ -88,6 +88,13 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         raise ImportError(
             f"{path} is missing: build the sm_100a extension with "
             "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+    try:
+        # one NCCL per process: with torch loaded first, the library's lazy
+        # dlopen("libnccl.so.2") binds torch's bundled NCCL; the other order
+        # would bind the system one and break a later `import torch`
+        import torch  # noqa: F401
+    except ImportError:
+        pass
     lib = ctypes.CDLL(path)
     for name, restype, argtypes in _SIGNATURES:
         fn = getattr(lib, name)

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -61,7 +62,10 @@ NcclApi& nccl() {
   static NcclApi api;
   static std::once_flag once;
   std::call_once(once, [] {
-    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    // RSOT_NCCL_LIBRARY picks a library explicitly; otherwise the soname,
+    // which resolves to an NCCL the process has already loaded (e.g. torch's)
+    const char* env = std::getenv("RSOT_NCCL_LIBRARY");
+    const char* names[] = {env && *env ? env : "libnccl.so.2", "libnccl.so.2", "libnccl.so"};
     for (const char* nm : names) {
       api.handle = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
       if (api.handle) break;
@@ -118,6 +122,19 @@ struct rsot_cuda_ctx {
   int precision = RSOT_CUDA_PRECISION_FP64;
   cudaEvent_t ev[8] = {};
   double last_ms[3] = {0, 0, 0};
+  // CUDA graph of one dense device evaluation (prologue, both passes, split
+  // reductions, the collective, finalisation: ~13 launches -> 1), replayed
+  // while atoms, targets, eps and the workspace stay the same
+  struct DenseGraph {
+    cudaGraphExec_t exec = nullptr;
+    const void* atoms = nullptr;
+    const void* targets = nullptr;
+    double eps = 0.0;
+    size_t nq = 0, n = 0;
+    uint64_t ws_key = 0;
+    unsigned long long launches = 0;
+    bool broken = false;  // capture failed once: stay on direct launches
+  } graph;
 };
 
 struct rsot_cuda_targets {
@@ -326,6 +343,7 @@ int rsot_cuda_ctx_destroy(rsot_cuda_ctx* c) {
   c->trunc.release();
   c->refine.release();
   c->geo.release();
+  if (c->graph.exec) cudaGraphExecDestroy(c->graph.exec);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
@@ -364,6 +382,8 @@ int rsot_cuda_ctx_set_comm(rsot_cuda_ctx* c, int rank, int world,
     return fail(RSOT_CUDA_INVALID_ARGUMENT, "bad rank/world");
   c->rank = rank;
   c->world = world;
+  if (c->graph.exec) cudaGraphExecDestroy(c->graph.exec);
+  c->graph = rsot_cuda_ctx::DenseGraph();
   // (a 1-rank communicator is created too: it runs the same gather +
   // rank-ordered sum, which lets a single GPU exercise the collective path)
   NcclApi& api = nccl();
@@ -488,6 +508,91 @@ int rsot_cuda_atoms_destroy(rsot_cuda_atoms* a) {
 
 size_t rsot_cuda_atoms_size(const rsot_cuda_atoms* a) { return a ? a->nq : 0; }
 
+namespace {
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RSOT_CUDA_GRAPHS");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
+// everything a captured dense evaluation bakes in besides (atoms, targets,
+// eps, sizes): workspace and data pointers, the communicator, the bbox
+uint64_t workspace_key(const rsot_cuda_ctx* c, const rsot_cuda_atoms* a, const rsot_cuda_targets* t) {
+  const void* ptrs[] = {a->x, t->y, t->nu, static_cast<const void*>(c->comm),
+                        c->psi.p, c->b2.p, c->scal.p, c->part.p, c->partS.p, c->shiftA.p, c->atomL.p, c->atomLam.p, c->atomJ.p, c->atomD.p, c->partG.p,
+                        c->res.p, c->g_out.p, c->scalars_out.p, c->gathered.p, c->flagged.p};
+  uint64_t h = 1469598103934665603ull;
+  for (const void* p : ptrs) h = (h ^ reinterpret_cast<uintptr_t>(p)) * 1099511628211ull;
+  for (int k = 0; k < 3; ++k) {
+    uint64_t u, v;
+    std::memcpy(&u, &t->cells.bbox_lo[k], 8);
+    std::memcpy(&v, &t->cells.bbox_hi[k], 8);
+    h = (h ^ u) * 1099511628211ull;
+    h = (h ^ v) * 1099511628211ull;
+  }
+  return h;
+}
+
+// Dense device evaluation through a captured CUDA graph: psi is copied into
+// the context's buffer, the graph replays, the results are copied out.
+// Outputs stay in the context's g_out / scalars_out when d_g_out is null.
+int eval_dense_graph(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
+                     const double* h_psi, const double* d_psi, double eps, double* d_g_out,
+                     double* d_scalars) {
+  int rc = 0;
+  auto& G = c->graph;
+  const uint64_t key = workspace_key(c, a, t);
+  if (!(G.exec && G.atoms == a && G.targets == t && G.eps == eps && G.nq == a->nq && G.n == t->n &&
+        G.ws_key == key)) {
+    if (G.exec) cudaGraphExecDestroy(G.exec);
+    G.exec = nullptr;
+    EvalBuffers b = buffers(c, nullptr, nullptr);
+    b.timing = nullptr;
+    cudaGraph_t graph = nullptr;
+    RSOT_CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const unsigned long long l0 = g_kernel_launches.load();
+    rc = enqueue_eval(c, a, t, b, eps, INFINITY, nullptr);
+    const cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+    const unsigned long long captured = g_kernel_launches.load() - l0;
+    g_kernel_launches.fetch_sub(captured);  // counted again at every replay
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    cudaError_t ei = e;
+    if (ei == cudaSuccess) ei = cudaGraphInstantiate(&G.exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+      // e.g. a communicator that refuses capture: same kernels, launched directly
+      cudaGetLastError();
+      G.exec = nullptr;
+      G.broken = true;
+      return -1;  // caller launches directly
+    }
+    G.atoms = a;
+    G.targets = t;
+    G.eps = eps;
+    G.nq = a->nq;
+    G.n = t->n;
+    G.ws_key = key;
+    G.launches = captured;
+  }
+  RSOT_CK(cudaMemcpyAsync(c->psi.p, h_psi ? h_psi : d_psi, sizeof(double) * t->n,
+                          h_psi ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c->stream));
+  RSOT_CK(cudaGraphLaunch(G.exec, c->stream));
+  g_kernel_launches.fetch_add(G.launches);
+  if (d_g_out) {
+    RSOT_CK(cudaMemcpyAsync(d_g_out, c->g_out.p, sizeof(double) * t->n, cudaMemcpyDeviceToDevice,
+                            c->stream));
+    RSOT_CK(cudaMemcpyAsync(d_scalars, c->scalars_out.p, sizeof(double) * kResTail,
+                            cudaMemcpyDeviceToDevice, c->stream));
+  }
+  return RSOT_CUDA_OK;
+}
+}  // namespace
+
 static int eval_common(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
                        const double* psi_host, const double* psi_dev, double eps,
                        double cutoff, double* g_dev, double* scal_dev,
@@ -497,6 +602,13 @@ static int eval_common(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* 
   const DenseLaunch plan = plan_dense(static_cast<int>(a->nq), static_cast<int>(t->n), c->num_sms);
   int rc = ensure_workspace(c, a->nq, t->n, plan);
   if (rc) return rc;
+  // dense evaluations without debug outputs or per-kernel timing replay a
+  // captured graph
+  if (!std::isfinite(cutoff) && cost == RSOT_CUDA_COST_SQEUCLIDEAN && !dbg && !c->timing && a->nq > 0 &&
+      !c->graph.broken && graphs_enabled()) {
+    rc = eval_dense_graph(c, a, t, psi_host, psi_dev, eps, g_dev, scal_dev);
+    if (rc != -1) return rc;
+  }
   EvalBuffers b = buffers(c, g_dev, scal_dev);
   if (psi_host)
     RSOT_CK(cudaMemcpyAsync(b.psi, psi_host, sizeof(double) * t->n,
@@ -529,6 +641,7 @@ int rsot_cuda_eval_cost(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets*
   if (rc) return rc;
   return finish_host_eval(c, t, g_out, out);
 }
+
 
 int rsot_cuda_eval_device(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
                           const double* d_psi, double eps, double cutoff,

@@ -86,6 +86,13 @@ int rsot_cuda_ctx_set_comm(rsot_cuda_ctx* ctx, int rank, int world,
 void rsot_cuda_shard_range(size_t nq, int rank, int world, size_t* lo,
                            size_t* hi);
 
+/* Testing / load-balance diagnostics on one GPU: a context WITHOUT a
+ * communicator evaluates partitioned atom handles as rank `rank` of `world`
+ * and finalises that rank's partial alone (g_r = partial - nu,
+ * J_r = partial - sum psi nu; so g = sum_r g_r + (world-1) nu,
+ * J = sum_r J_r + (world-1) sum psi nu, D and the counters add). */
+int rsot_cuda_ctx_set_virtual_rank(rsot_cuda_ctx* ctx, int rank, int world);
+
 /* ---- resident data ------------------------------------------------------- */
 /* TargetMeasure{points, weights} (measures.hpp:13-19); n >= 1 else
  * RSOT_CUDA_INVALID_ARGUMENT ("spatial index: empty point set"). */
@@ -100,6 +107,19 @@ size_t rsot_cuda_targets_size(const rsot_cuda_targets* t);
 int rsot_cuda_atoms_create(rsot_cuda_ctx* ctx, const double* xyz,
                            const double* mass, size_t nq,
                            rsot_cuda_atoms** out);
+/* The same for ALL atoms on every rank of a multi-rank context: each
+ * evaluation then splits the work itself, truncated evaluations by a
+ * work-balanced cut of the Hilbert-ordered atom chunks (per-chunk scan cost
+ * from the geometry and cutoff, identical on every rank; heavy chunks run
+ * split across a CTA cluster), dense and geodesic ones by
+ * rsot_cuda_shard_range.  Replaces parallel_blocks' equal atom ranges
+ * (parallel.hpp:14-31), which leave clustered truncated problems (BASELINE
+ * cfg3) with a 20x spread of work between ranks.  Results are bitwise
+ * identical on every rank and run to run.  On a 1-rank context it behaves
+ * like rsot_cuda_atoms_create. */
+int rsot_cuda_atoms_create_partitioned(rsot_cuda_ctx* ctx, const double* xyz,
+                                       const double* mass, size_t nq,
+                                       rsot_cuda_atoms** out);
 int rsot_cuda_atoms_destroy(rsot_cuda_atoms* a);
 size_t rsot_cuda_atoms_size(const rsot_cuda_atoms* a);
 

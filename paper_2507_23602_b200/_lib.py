@@ -46,6 +46,9 @@ _SIGNATURES = [
     ("rsot_cuda_targets_destroy", c_int, [c_void_p]),
     ("rsot_cuda_targets_size", c_size_t, [c_void_p]),
     ("rsot_cuda_atoms_create", c_int, [c_void_p, c_void_p, c_void_p, c_size_t, POINTER(c_void_p)]),
+    ("rsot_cuda_atoms_create_partitioned", c_int,
+     [c_void_p, c_void_p, c_void_p, c_size_t, POINTER(c_void_p)]),
+    ("rsot_cuda_ctx_set_virtual_rank", c_int, [c_void_p, c_int, c_int]),
     ("rsot_cuda_atoms_destroy", c_int, [c_void_p]),
     ("rsot_cuda_atoms_size", c_size_t, [c_void_p]),
     ("rsot_cuda_eval", c_int,

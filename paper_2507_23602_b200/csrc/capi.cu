@@ -135,6 +135,7 @@ struct rsot_cuda_ctx {
     unsigned long long launches = 0;
     bool broken = false;  // capture failed once: stay on direct launches
   } graph;
+  int vrank = 0, vworld = 1;  // rsot_cuda_ctx_set_virtual_rank (no communicator)
 };
 
 struct rsot_cuda_targets {
@@ -150,6 +151,7 @@ struct rsot_cuda_atoms {
   size_t nq = 0;
   double4* x = nullptr;  // {x0, x1, x2, m}
   AtomCells cells;       // Hilbert order (built on first truncated use)
+  bool partitioned = false;  // every atom on every rank; evaluations split the work
 };
 
 namespace {
@@ -218,6 +220,24 @@ int enqueue_eval(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
   const cudaStream_t s = c->stream;
   const DeviceTargets dt = make_dt(t);
   DeviceAtoms da{a->x, static_cast<int>(a->nq)};
+  // partitioned atoms: this rank's share of the work (truncated: balanced
+  // chunk ranges chosen on the device; dense / geodesic: equal atom ranges)
+  int prank = 0, pworld = 1;
+  if (a->partitioned) {
+    if (c->comm && c->world > 1) {
+      prank = c->rank;
+      pworld = c->world;
+    } else if (!c->comm && c->vworld > 1) {
+      prank = c->vrank;
+      pworld = c->vworld;
+    }
+  }
+  const bool trunc_path = cost != RSOT_CUDA_COST_SQGEODESIC && std::isfinite(cutoff);
+  if (pworld > 1 && !trunc_path) {
+    size_t lo = 0, hi = 0;
+    rsot_cuda_shard_range(a->nq, prank, pworld, &lo, &hi);
+    da = DeviceAtoms{a->x + lo, static_cast<int>(hi - lo)};
+  }
   if (b.timing) cudaEventRecord(b.timing[0], s);
   launch_prologue(dt, b, eps, s);
   if (cost == RSOT_CUDA_COST_SQGEODESIC) {
@@ -228,7 +248,7 @@ int enqueue_eval(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
   } else if (std::isfinite(cutoff)) {
     const int rc = run_truncated(c->trunc, da, a->cells, dt, t->cells, b, eps,
                                  cutoff, c->num_sms, dbg, s, g_last_error,
-                                 c->precision == RSOT_CUDA_PRECISION_FP32);
+                                 c->precision == RSOT_CUDA_PRECISION_FP32, prank, pworld);
     if (rc != 0) return fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error);
   } else {
     const DenseLaunch plan = plan_dense(da.nq, dt.n, c->num_sms);
@@ -496,6 +516,22 @@ int rsot_cuda_atoms_create(rsot_cuda_ctx* c, const double* xyz, const double* ma
   return RSOT_CUDA_OK;
 }
 
+int rsot_cuda_atoms_create_partitioned(rsot_cuda_ctx* c, const double* xyz, const double* mass,
+                                       size_t nq, rsot_cuda_atoms** out) {
+  const int rc = rsot_cuda_atoms_create(c, xyz, mass, nq, out);
+  if (rc == RSOT_CUDA_OK) (*out)->partitioned = true;
+  return rc;
+}
+
+int rsot_cuda_ctx_set_virtual_rank(rsot_cuda_ctx* c, int rank, int world) {
+  if (!c) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null context");
+  if (world < 1 || rank < 0 || rank >= world) return fail(RSOT_CUDA_INVALID_ARGUMENT, "bad rank/world");
+  if (c->comm) return fail(RSOT_CUDA_INVALID_ARGUMENT, "context has a communicator");
+  c->vrank = rank;
+  c->vworld = world;
+  return RSOT_CUDA_OK;
+}
+
 int rsot_cuda_atoms_destroy(rsot_cuda_atoms* a) {
   if (!a) return RSOT_CUDA_OK;
   cudaSetDevice(a->ctx->device);
@@ -525,6 +561,8 @@ uint64_t workspace_key(const rsot_cuda_ctx* c, const rsot_cuda_atoms* a, const r
                         c->res.p, c->g_out.p, c->scalars_out.p, c->gathered.p, c->flagged.p};
   uint64_t h = 1469598103934665603ull;
   for (const void* p : ptrs) h = (h ^ reinterpret_cast<uintptr_t>(p)) * 1099511628211ull;
+  h = (h ^ static_cast<uint64_t>(c->vrank * 65536 + c->vworld * 2 + (a->partitioned ? 1 : 0))) *
+      1099511628211ull;
   for (int k = 0; k < 3; ++k) {
     uint64_t u, v;
     std::memcpy(&u, &t->cells.bbox_lo[k], 8);

@@ -475,6 +475,45 @@ __global__ void det_sum_final(const double* __restrict__ part, int nblk,
   if (threadIdx.x == 0) *out = s;
 }
 
+// Four fixed-order sums at once (same blocking and trees as det_sum_blocks /
+// det_sum_final, so each result is bitwise what launch_det_sum gives);
+// range (device {lo, hi}, or null = all): entries outside count as zero.
+__global__ void det_sum4_blocks(const double* __restrict__ x0, const double* __restrict__ x1,
+                                const double* __restrict__ x2, const double* __restrict__ x3, size_t n,
+                                size_t chunk, const int* __restrict__ range, double* __restrict__ part) {
+  __shared__ double sh[256];
+  const size_t lo = blockIdx.x * chunk;
+  const size_t hi = min(n, lo + chunk);
+  const size_t rl = range ? static_cast<size_t>(range[0]) : 0, rh = range ? static_cast<size_t>(range[1]) : n;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  for (size_t i = max(lo, rl) + ((threadIdx.x + blockDim.x - (max(lo, rl) - lo) % blockDim.x) % blockDim.x);
+       i < min(hi, rh); i += blockDim.x) {
+    s0 += x0[i];
+    s1 += x1[i];
+    s2 += x2[i];
+    s3 += x3[i];
+  }
+  s0 = block_sum<256>(s0, sh);
+  s1 = block_sum<256>(s1, sh);
+  s2 = block_sum<256>(s2, sh);
+  s3 = block_sum<256>(s3, sh);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s0;
+    part[kRedBlocks + blockIdx.x] = s1;
+    part[2 * kRedBlocks + blockIdx.x] = s2;
+    part[3 * kRedBlocks + blockIdx.x] = s3;
+  }
+}
+
+__global__ void det_sum4_final(const double* __restrict__ part, int nblk, double* __restrict__ out) {
+  __shared__ double sh[256];
+  const double* p = part + blockIdx.x * kRedBlocks;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) s += p[i];
+  s = block_sum<256>(s, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
 __global__ void set_dense_counts(double* __restrict__ res, int n, double nq) {
   res[n + kResPairs] = nq * static_cast<double>(n);
   res[n + kResEmpty] = 0.0;
@@ -549,6 +588,14 @@ void launch_det_sum(const double* x, size_t n, double* partials, double* out,
   const size_t chunk = (n + nb - 1) / nb;
   (note_launch(), det_sum_blocks<<<nb, 256, 0, s>>>(x, n, chunk, partials));
   (note_launch(), det_sum_final<<<1, 256, 0, s>>>(partials, nb, out));
+}
+
+void launch_det_sum4(const double* x0, const double* x1, const double* x2, const double* x3, size_t n,
+                     const int* range, double* partials, double* out, cudaStream_t s) {
+  const int nb = red_blocks(n);
+  const size_t chunk = (n + nb - 1) / nb;
+  (note_launch(), det_sum4_blocks<<<nb, 256, 0, s>>>(x0, x1, x2, x3, n, chunk, range, partials));
+  (note_launch(), det_sum4_final<<<4, 256, 0, s>>>(partials, nb, out));
 }
 
 void launch_prologue(const DeviceTargets& t, EvalBuffers& b, double eps,

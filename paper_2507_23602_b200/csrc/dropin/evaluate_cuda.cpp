@@ -193,13 +193,14 @@ struct State {
         atoms.splice(atoms.begin(), atoms, it);
         return atoms.front().second;
       }
-    size_t lo = 0, hi = a.points.size();
-    if (world_eff > 1) rsot_cuda_shard_range(a.points.size(), rank, world, &lo, &hi);
+    // multi-rank: every rank holds all atoms and each evaluation takes its
+    // work-balanced share (rsot_cuda_atoms_create_partitioned)
+    const size_t nq = a.points.size();
     rsot_cuda_atoms* h = nullptr;
-    const double* xyz = a.points.empty() ? nullptr : a.points[lo].data();
-    const double* m = a.masses.empty() ? nullptr : a.masses.data() + lo;
-    const int rc = rsot_cuda_atoms_create(context(), hi > lo ? xyz : nullptr, hi > lo ? m : nullptr,
-                                          hi - lo, &h);
+    const double* xyz = nq ? a.points[0].data() : nullptr;
+    const double* m = nq ? a.masses.data() : nullptr;
+    const int rc = world_eff > 1 ? rsot_cuda_atoms_create_partitioned(context(), xyz, m, nq, &h)
+                                 : rsot_cuda_atoms_create(context(), xyz, m, nq, &h);
     if (rc) raise(rc, "rsot_cuda_atoms_create");
     atoms.emplace_front(k, h);
     while (atoms.size() > kKeep) {

@@ -101,6 +101,11 @@ void launch_finalize(const DeviceTargets& t, EvalBuffers& b, cudaStream_t s);
 // Deterministic fixed-order sum of x[0..n) into out[0] (two launches).
 void launch_det_sum(const double* x, size_t n, double* partials, double* out,
                     cudaStream_t s);
+// launch_det_sum of four arrays into out[0..3] (bitwise the same results);
+// range = device {lo, hi} or null (entries outside count as zero);
+// partials holds 4 x 1024 doubles.
+void launch_det_sum4(const double* x0, const double* x1, const double* x2, const double* x3, size_t n,
+                     const int* range, double* partials, double* out, cudaStream_t s);
 
 // Dense target-major gather (softmax_refine phase 2), see dense.cu.
 void launch_dense_gather(const double4* atoms, const double* lam, int nq, const double4* ty,

@@ -20,11 +20,13 @@
 //   pass B  (CTA = 128 sorted targets): same scan over atom cells; gather of
 //           2^(e2_qj - log2 S_q + log2 m_q) into the thread's own target.
 //   assemble: res[j] = G[j] + empty[j]; fixed-order sums of J, D, counts.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -373,6 +375,52 @@ __device__ void warp_nearest(const GridDev& g, const double4* __restrict__ ys,
   best_k = bk;
 }
 
+// Nearest target given a candidate (cell-order position seed_k, e.g. a
+// neighbouring query's answer): every target that beats it, (d2, j)
+// lexicographically, lies in the ball through the seed, so one sweep of the
+// cell rows meeting that ball (row_range, as the candidate scan) finds the
+// minimum -- O(K^2) row visits instead of the rings' O(K^3).  Balls wider than
+// kSeedRows rows fall back to the ring search.
+constexpr int kSeedRows = 512;
+
+__device__ void warp_nearest_seeded(const GridDev& g, const double4* __restrict__ ys,
+                                    const int* __restrict__ tperm, const int* __restrict__ cell_start,
+                                    double x0, double x1, double x2, int seed_k, double& best_d2,
+                                    int& best_j, int& best_k) {
+  const double4 ys0 = ys[seed_k];
+  double bd = exact_sqdist(x0, x1, x2, ys0.x, ys0.y, ys0.z);
+  int bj = tperm[seed_k], bk = seed_k;
+  const double rad = sqrt(bd) * (1.0 + 1e-9) + 1e-300;
+  Region R;
+  R.box[0] = R.box[3] = x0;
+  R.box[1] = R.box[4] = x1;
+  R.box[2] = R.box[5] = x2;
+  for (int d = 0; d < 3; ++d) {
+    R.c_lo[d] = cell_of(g, d, R.box[d] - rad);
+    R.c_hi[d] = cell_of(g, d, R.box[d + 3] + rad);
+  }
+  const int nrows = (R.c_hi[1] - R.c_lo[1] + 1) * (R.c_hi[2] - R.c_lo[2] + 1);
+  if (nrows > kSeedRows) {
+    warp_nearest(g, ys, tperm, cell_start, x0, x1, x2, best_d2, best_j, best_k);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  for (int r0 = 0; r0 < nrows; r0 += 32) {
+    int st = 0, ln = 0;
+    if (r0 + lane < nrows) row_range(g, R, rad, cell_start, r0 + lane, st, ln);
+    scan_range(st, st + ln, x0, x1, x2, ys, tperm, bd, bj, bk);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+    const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+    const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+    if (od < bd || (od == bd && oj < bj)) { bd = od; bj = oj; bk = ok; }
+  }
+  best_d2 = bd;
+  best_j = bj;
+  best_k = bk;
+}
+
 template <bool DEBUG>
 __global__ void trunc_nearest_empty(const double4* __restrict__ xs, int nq,
                                     const uint32_t* __restrict__ cnt,
@@ -384,14 +432,16 @@ __global__ void trunc_nearest_empty(const double4* __restrict__ xs, int nq,
                                     double* __restrict__ atomJ,
                                     double* __restrict__ atomD,
                                     unsigned long long* __restrict__ empty_fp,
-                                    uint64_t* __restrict__ hash_out) {
+                                    uint64_t* __restrict__ hash_out, const int* __restrict__ range) {
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int base = warp * 32; base < nq; base += nwarps * 32) {
+  const int lo = range ? range[0] : 0, hi = range ? range[1] : nq;  // this rank's atoms
+  for (int base = (lo & ~31) + warp * 32; base < hi; base += nwarps * 32) {
     const int q = base + lane;
-    const bool empty = q < nq && cnt[q] == 0;
+    const bool empty = q >= lo && q < hi && cnt[q] == 0;
     unsigned mask = __ballot_sync(0xffffffffu, empty);
+    int seed = -1;  // empty atoms of a Hilbert group are neighbours: seed each with the last answer
     while (mask) {
       const int l = __ffs(mask) - 1;
       mask &= mask - 1;
@@ -399,7 +449,11 @@ __global__ void trunc_nearest_empty(const double4* __restrict__ xs, int nq,
       const double4 a = xs[qq];
       double bd;
       int bj, bk;
-      warp_nearest(g, ys, tperm, cell_start, a.x, a.y, a.z, bd, bj, bk);
+      if (seed >= 0)
+        warp_nearest_seeded(g, ys, tperm, cell_start, a.x, a.y, a.z, seed, bd, bj, bk);
+      else
+        warp_nearest(g, ys, tperm, cell_start, a.x, a.y, a.z, bd, bj, bk);
+      seed = bk;
       if (lane == 0) {
         const double L = reference_exponent(psi[bj], bd, eps, ys[bk].w);
         atomL[qq] = L;
@@ -475,7 +529,37 @@ struct FusedArgs {
   uint32_t* dbg_cnt; uint64_t* dbg_hash; double* dbg_logs;  // Hilbert order
   uint32_t* cnt_out;                     // 0 = empty candidate set (Hilbert order)
   const int* chunk_order;                // CTA -> atom chunk (heaviest first) or null
+  const unsigned char* role;             // per chunk: kRoleOther / kRoleMine / kRoleSplit, or null
+  const int* heavy_count;                // split chunks: chunk_order[0, heavy_count)
+  int* queue;                            // trunc_fused_split work counter
 };
+
+// chunk roles (chunk_role)
+constexpr unsigned char kRoleOther = 0, kRoleMine = 1, kRoleSplit = 2;
+// Chunk work model, in units of one scanned target (cfg3 per-rank times fit
+// 7.4e-8 ms per scanned target + 3.8e-9 ms per accepted pair; the chunk's
+// pairs are ~256 x the targets within reach of its centre, so a centre-ball
+// target weighs 256 x 0.051 = 13; fixed cost per chunk ~0.25 us per slot; an
+// empty-set atom's nearest search ~105 units: cfg3 3 ms for 3.8e5 of them
+// against 58 ms for 7.8e8 units)
+constexpr unsigned long long kChunkBase = 128;
+constexpr unsigned long long kPairWeight = 13;
+constexpr unsigned long long kEmptyAtomCost = 105;
+
+// Another rank's chunk: nothing to do (the sums and trunc_nearest_empty
+// only read this rank's atom range); the debug outputs are zeroed.
+template <bool DEBUG>
+__device__ __forceinline__ void fused_skip_chunk(const FusedArgs& A, int chunk) {
+  if constexpr (DEBUG) {
+    for (int t = threadIdx.x; t < kFA; t += kT) {
+      const int q = chunk * kFA + t;
+      if (q >= A.nq) break;
+      A.dbg_cnt[q] = 0u;
+      A.dbg_hash[q] = 0u;
+      A.dbg_logs[q] = 0.0;
+    }
+  }
+}
 
 __device__ __forceinline__ double chain3(const double (&X)[3], const double4& y) {
   return fma(X[0], y.x, fma(X[1], y.y, fma(X[2], y.z, y.w)));
@@ -895,9 +979,15 @@ __device__ __forceinline__ void batch64_full(const FusedSmem& sm, FusedAtoms& at
   if (!(lane & 1) && item < nfull) col[full[-item]] = tot;
 }
 
-template <int PHASE, bool SAFE, bool DEBUG>
+// KS > 1: this CTA is split `split` of KS sharing one chunk (heavy chunks,
+// trunc_fused_split): every split walks all row batches and takes the tiles
+// split, split + KS, ... of each batch's concatenated targets (tile size
+// shrunk for small batches so every split gets several), which balances the
+// splits to within a tile (every-KS-th-row interleaving left the cluster
+// waiting on its longest rows: 14 % of the samples at the cluster barrier).
+template <int PHASE, bool SAFE, bool DEBUG, int KS = 1>
 __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb, float cull_thr,
-                           double B, FusedAtoms& at) {
+                           double B, FusedAtoms& at, int split = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   ListT* const list = sm.wlist[warp];
   const bool wide = SAFE && sm.R.wide;
@@ -926,13 +1016,19 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
     sm.rowPref[threadIdx.x] = pre;
     if (threadIdx.x == 0) sm.rowPref[kT] = total;
     __syncthreads();  // row ranges visible; previous batch fully consumed
-    if (total > 0) fused_prefetch(sm, A, 0, min(kTileT, total));
-    for (int base = 0; base < total; base += kTileT) {
-      const int cnt = min(kTileT, total - base);
+    int tile = kTileT, start = 0, step = kTileT;
+    if (KS > 1) {
+      tile = min(kTileT, max(32, (total + 4 * KS - 1) / (4 * KS)));
+      start = split * tile;
+      step = KS * tile;
+    }
+    if (start < total) fused_prefetch(sm, A, start, min(tile, total - start));
+    for (int base = start; base < total; base += step) {
+      const int cnt = min(tile, total - base);
       __syncthreads();  // every warp is done with the previous tile
       fused_convert(sm, A, B, cnt);
       __syncthreads();  // staged tile visible, landing zone free
-      if (base + kTileT < total) fused_prefetch(sm, A, base + kTileT, min(kTileT, total - base - kTileT));
+      if (base + step < total) fused_prefetch(sm, A, base + step, min(tile, total - base - step));
       int nfull = 0;
       const int nsel = fused_cull2(sm, cnt, wb, cull_thr, full_thr, list, kTileT, &nfull);
       if (PHASE == 1) {
@@ -1020,12 +1116,15 @@ __device__ __noinline__ void warp_exact_atom(const FusedArgs& A, double x0, doub
 }
 
 // Per-atom finalisation between the phases (all lanes of the warp call it:
-// empty and flagged atoms are resolved warp-cooperatively).
+// empty and flagged atoms are resolved warp-cooperatively).  Of the CTAs
+// sharing a split chunk only the primary writes the per-atom results and
+// runs the exact path; the others just take its phase-2 weights.
 template <bool DEBUG>
 __device__ __forceinline__ void fused_finalize(const FusedArgs& A, double B, bool wide, bool valid,
                                                bool nonempty, double cnt_contrib, uint32_t dbg_count,
                                                double S, double xsq, int q, uint64_t hash,
-                                               double& W, double smin = 0x1p-960) {
+                                               double& W, double smin = 0x1p-960,
+                                               bool primary = true) {
   const int lane = threadIdx.x & 31;
   const double4 p = valid ? A.xs[q] : make_double4(0, 0, 0, 0);
   const double shift = wide ? 0.0 : xsq;
@@ -1037,7 +1136,11 @@ __device__ __forceinline__ void fused_finalize(const FusedArgs& A, double B, boo
   // Empty candidate sets: resolved after this kernel by trunc_nearest_empty
   // (warp per empty atom over the whole GPU, no CTA barrier in the way);
   // their phase-2 weight is 0 and their J/D/L are written there.
-  if (valid) A.cnt_out[q] = empty ? 0u : 1u;
+  if (valid && primary) A.cnt_out[q] = empty ? 0u : 1u;
+  if (!primary) {
+    W = flag ? 0.0 : w;
+    return;
+  }
   unsigned mf = __ballot_sync(0xffffffffu, flag);
   while (mf) {
     const int l = __ffs(mf) - 1;
@@ -1064,14 +1167,24 @@ __device__ __forceinline__ void fused_finalize(const FusedArgs& A, double B, boo
   }
 }
 
-template <bool DEBUG>
-__global__ void __launch_bounds__(kT, 4)
-trunc_fused(FusedArgs A) {
-  __shared__ FusedSmem sm;
+// Phase-1 partials of one split CTA, read by its cluster peers through
+// distributed shared memory (aliases colW, which phase 1 does not use).
+struct SplitXchg {
+  double S[2][kT];
+  uint64_t H[2][kT];
+  uint32_t C[2][kT];
+};
+static_assert(sizeof(SplitXchg) <= sizeof(double) * (kT / 32) * kTileT, "exchange fits colW");
+
+// One chunk of kFA Hilbert-consecutive atoms; KS > 1: split `split` of a
+// cluster of KS CTAs sharing the chunk (each scans every KS-th target row;
+// the phase-1 sums, counts and hashes are combined in rank order, so every
+// CTA of the cluster holds the same S_q and the result is deterministic).
+template <bool DEBUG, int KS>
+__device__ __forceinline__ void fused_body(FusedSmem& sm, const FusedArgs& A, int chunk, int split) {
   load_exp2_table(sm.tbl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   FusedAtoms at;
-  const int chunk = A.chunk_order ? A.chunk_order[blockIdx.x] : static_cast<int>(blockIdx.x);
   at.qa = chunk * kFA + warp * 64 + lane;
   at.qb = at.qa + 32;
   const bool va = at.qa < A.nq, vb = at.qb < A.nq;
@@ -1122,20 +1235,94 @@ trunc_fused(FusedArgs A) {
   const bool safe = wide || (A.scal[kSlotBmin] - B) - A.c2 * A.r2 < -1000.0;
 
   if (safe)
-    fused_scan<1, true, DEBUG>(sm, A, wb, cull_thr, B, at);
+    fused_scan<1, true, DEBUG, KS>(sm, A, wb, cull_thr, B, at, split);
   else
-    fused_scan<1, false, DEBUG>(sm, A, wb, cull_thr, B, at);
+    fused_scan<1, false, DEBUG, KS>(sm, A, wb, cull_thr, B, at, split);
+
+  if constexpr (KS > 1) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    SplitXchg* x = reinterpret_cast<SplitXchg*>(&sm.colW[0][0]);
+    const int t = threadIdx.x;
+    x->S[0][t] = at.Sa; x->S[1][t] = at.Sb;
+    x->C[0][t] = at.ca; x->C[1][t] = at.cb;
+    if (DEBUG) { x->H[0][t] = at.ha; x->H[1][t] = at.hb; }
+    cl.sync();  // partials of every split visible cluster-wide
+    double sa = 0.0, sb = 0.0;
+    uint32_t ca = 0, cb = 0;
+    uint64_t ha = 0, hb = 0;
+#pragma unroll
+    for (int r = 0; r < KS; ++r) {  // rank order: identical in every CTA
+      const SplitXchg* xr = cl.map_shared_rank(x, r);
+      sa += xr->S[0][t]; sb += xr->S[1][t];
+      ca += xr->C[0][t]; cb += xr->C[1][t];
+      if (DEBUG) { ha += xr->H[0][t]; hb += xr->H[1][t]; }
+    }
+    cl.sync();  // no CTA reuses colW (phase 2) while a peer still reads it
+    at.Sa = sa; at.Sb = sb; at.ca = ca; at.cb = cb; at.ha = ha; at.hb = hb;
+  }
 
   // pair counter: the lane's accepted pairs are booked on atom a
+  const bool primary = split == 0;
   fused_finalize<DEBUG>(A, B, wide, va, at.ca != 0u, static_cast<double>(at.ca + at.cb), at.ca,
-                        at.Sa, at.xsqa, at.qa, at.ha, at.wa);
+                        at.Sa, at.xsqa, at.qa, at.ha, at.wa, 0x1p-960, primary);
   fused_finalize<DEBUG>(A, B, wide, vb, at.cb != 0u, 0.0, at.cb, at.Sb, at.xsqb, at.qb, at.hb,
-                        at.wb);
+                        at.wb, 0x1p-960, primary);
 
   if (safe)
-    fused_scan<2, true, DEBUG>(sm, A, wb, cull_thr, B, at);
+    fused_scan<2, true, DEBUG, KS>(sm, A, wb, cull_thr, B, at, split);
   else
-    fused_scan<2, false, DEBUG>(sm, A, wb, cull_thr, B, at);
+    fused_scan<2, false, DEBUG, KS>(sm, A, wb, cull_thr, B, at, split);
+}
+
+template <bool DEBUG>
+__global__ void __launch_bounds__(kT, 4)
+trunc_fused(FusedArgs A) {
+  __shared__ FusedSmem sm;
+  int chunk = static_cast<int>(blockIdx.x);
+  if (A.chunk_order) {  // the split chunks lead the order (trunc_fused_split)
+    const int pos = *A.heavy_count + chunk;
+    if (pos >= (A.nq + kFA - 1) / kFA) return;
+    chunk = A.chunk_order[pos];
+  }
+  if (A.role) {
+    const unsigned char r = A.role[chunk];
+    if (r == kRoleOther) return fused_skip_chunk<DEBUG>(A, chunk);
+    if (r == kRoleSplit) return;  // run by trunc_fused_split
+  }
+  fused_body<DEBUG, 1>(sm, A, chunk, 0);
+}
+
+// Heavy chunks (chunk_role_kernel): a cluster of kSplit CTAs per chunk, so
+// the longest chunks no longer bound the kernel (cfg3: one chunk held ~the
+// whole GPU's per-slot share of pairs).  Persistent: one resident wave of
+// clusters pulls the split chunks heaviest first from a queue (any count,
+// no host round trip).
+constexpr int kSplit = 8;
+
+template <bool DEBUG>
+__global__ void __cluster_dims__(kSplit, 1, 1) __launch_bounds__(kT, 4)
+trunc_fused_split(FusedArgs A) {
+  __shared__ FusedSmem sm;
+  __shared__ int next;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int split = static_cast<int>(cl.block_rank());
+  const int count = *A.heavy_count;
+  for (;;) {
+    // dynamic queue over the heaviest-first split list: the cluster's rank 0
+    // takes the next chunk; its peers read it through distributed shared
+    // memory (rank 0 writes again only after fused_body's cluster barriers)
+    if (split == 0 && threadIdx.x == 0) next = atomicAdd(A.queue, 1);
+    cl.sync();
+    const int h = *cl.map_shared_rank(&next, 0);
+    if (h >= count) {  // uniform across the cluster
+      cl.sync();       // rank 0's shared memory stays alive until every peer has read it
+      break;
+    }
+    fused_body<DEBUG, kSplit>(sm, A, A.chunk_order[h], split);
+    __syncthreads();  // shared memory free for the next chunk
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1423,6 +1610,7 @@ trunc_fused32(FusedArgs A) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   Atoms32 at;
   const int chunk = A.chunk_order ? A.chunk_order[blockIdx.x] : static_cast<int>(blockIdx.x);
+  if (A.role && A.role[chunk] == kRoleOther) return fused_skip_chunk<DEBUG>(A, chunk);
   at.qa = chunk * kFA + warp * 64 + lane;
   at.qb = at.qa + 32;
   const bool va = at.qa < A.nq, vb = at.qb < A.nq;
@@ -1477,15 +1665,127 @@ trunc_fused32(FusedArgs A) {
 
 // Chunk cost = the chunk's candidate pairs of the last evaluation; key =
 // (~cost << 32 | chunk) so an ascending sort puts the heaviest first.
-__global__ void chunk_cost_kernel(const double* __restrict__ cntd, int nq, int chunks,
-                                  uint64_t* __restrict__ keys, int* __restrict__ idx) {
+// Bounding box of every Hilbert chunk (warp per chunk; cached with the order).
+__global__ void chunk_box_kernel(const double4* __restrict__ xs, int nq, int nblk, double* __restrict__ box) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (c >= nblk) return;
+  double v[6] = {INFINITY, INFINITY, INFINITY, INFINITY, INFINITY, INFINITY};  // lo, -hi
+  for (int k = lane; k < kFA; k += 32) {
+    const int q = c * kFA + k;
+    if (q >= nq) break;
+    const double4 p = xs[q];
+    v[0] = fmin(v[0], p.x); v[1] = fmin(v[1], p.y); v[2] = fmin(v[2], p.z);
+    v[3] = fmin(v[3], -p.x); v[4] = fmin(v[4], -p.y); v[5] = fmin(v[5], -p.z);
+  }
+#pragma unroll
+  for (int d = 0; d < 6; ++d) v[d] = warp_min(v[d]);
+  if (lane == 0) {
+    double* o = box + 6 * static_cast<size_t>(c);
+    o[0] = v[0]; o[1] = v[1]; o[2] = v[2];
+    o[3] = -v[3]; o[4] = -v[4]; o[5] = -v[5];
+  }
+}
+
+// Targets within reach of a box (its cell rows, as fused_scan forms them).
+__device__ __forceinline__ unsigned warp_rows_count(const GridDev& g, const double* bx, double r,
+                                                    const int* __restrict__ cell_start, int lane) {
+  Region R;
+  for (int d = 0; d < 6; ++d) R.box[d] = bx[d];
+  for (int d = 0; d < 3; ++d) {
+    R.c_lo[d] = cell_of(g, d, R.box[d] - r);
+    R.c_hi[d] = cell_of(g, d, R.box[d + 3] + r);
+  }
+  const int nrows = (R.c_hi[1] - R.c_lo[1] + 1) * (R.c_hi[2] - R.c_lo[2] + 1);
+  unsigned acc = 0;
+  for (int ri = lane; ri < nrows; ri += 32) {
+    int st, ln;
+    row_range(g, R, r, cell_start, ri, st, ln);
+    acc += static_cast<unsigned>(ln);
+  }
+  return __reduce_add_sync(0xffffffffu, acc);
+}
+
+// Work estimate per chunk (warp per chunk): the targets its CTA scans (rows
+// within reach of the chunk box: pre-tests, staging) plus kPairWeight x the
+// targets within reach of the chunk centre (~ accepted pairs / 256), plus a
+// fixed cost and, when nothing is within reach of the centre, the nearest
+// searches of its atoms.  Depends only on the atoms, targets and cutoff, so the roles
+// below (and with them the summation order of the result) are deterministic.
+__global__ void chunk_scan_cost(const double* __restrict__ box, int nblk, GridDev g, double r_scan,
+                                const int* __restrict__ cell_start, unsigned long long* __restrict__ cost,
+                                unsigned long long* __restrict__ w) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (c >= nblk) return;
+  double bx[6], ctr[6];
+  for (int d = 0; d < 6; ++d) bx[d] = box[6 * static_cast<size_t>(c) + d];
+  for (int d = 0; d < 3; ++d) ctr[d] = ctr[d + 3] = 0.5 * (bx[d] + bx[d + 3]);
+  const unsigned scan = warp_rows_count(g, bx, r_scan, cell_start, lane);
+  const unsigned ball = warp_rows_count(g, ctr, r_scan, cell_start, lane);
+  if (lane == 0) {
+    // (an empty centre ball: most atoms of the chunk take the nearest path)
+    const unsigned long long wc = scan + kPairWeight * ball + kChunkBase + (ball == 0 ? kFA * kEmptyAtomCost : 0);
+    cost[c] = wc;
+    w[c] = wc;
+  }
+}
+
+// Per-chunk role for this rank.  Multi-rank partitioned atoms: the Hilbert
+// chunk sequence is cut into `world` contiguous ranges of equal weight
+// (scan cost + kChunkBase; a chunk goes to the rank holding the midpoint of
+// its interval in the exclusive prefix `pre`), the same on every rank since
+// the costs are.  This rank's chunks whose scan exceeds max(alpha x its
+// per-slot share, floor) run split.  range = {first atom, end atom, atom
+// count, split count, split queue} of this rank.
+__global__ void chunk_role_kernel(const unsigned long long* __restrict__ cost,
+                                  const unsigned long long* __restrict__ w,
+                                  const unsigned long long* __restrict__ pre, int nblk, int nq, int rank,
+                                  int world, double slots, double alpha, double floor_t,
+                                  unsigned char* __restrict__ role, int* __restrict__ range) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= chunks) return;
-  double s = 0.0;
-  const int q1 = min(nq, (c + 1) * kFA);
-  for (int q = c * kFA; q < q1; ++q) s += cntd[q];
-  const uint32_t cost = static_cast<uint32_t>(fmin(s, 4.0e9));
-  keys[c] = (static_cast<uint64_t>(~cost) << 32) | static_cast<uint32_t>(c);
+  if (c >= nblk) return;
+  const double tot = static_cast<double>(pre[nblk - 1] + w[nblk - 1]);
+  const double wc = static_cast<double>(w[c]);
+  const bool mine = world == 1 ||
+                    min(world - 1, static_cast<int>((static_cast<double>(pre[c]) + 0.5 * wc) / tot * world)) == rank;
+  const double thr = fmax(alpha * tot / (static_cast<double>(world) * slots), floor_t);
+  const bool heavy = mine && alpha >= 0.0 && static_cast<double>(cost[c]) > thr;
+  role[c] = !mine ? kRoleOther : heavy ? kRoleSplit : kRoleMine;
+  if (heavy) atomicAdd(range + 3, 1);
+  if (mine) {
+    const int q1 = min(nq, (c + 1) * kFA);
+    atomicMin(range, c * kFA);
+    atomicMax(range + 1, q1);
+    atomicAdd(range + 2, q1 - c * kFA);
+  }
+}
+
+__global__ void chunk_range_init(int* __restrict__ range, int nq) {
+  range[0] = nq;
+  range[1] = 0;
+  range[2] = 0;
+  range[3] = 0;
+  range[4] = 0;
+}
+
+__global__ void chunk_range_final(int* __restrict__ range, double* __restrict__ visited) {
+  if (range[2] == 0) range[0] = range[1] = 0;  // (no atoms: empty range)
+  if (visited) *visited = static_cast<double>(range[2]);
+}
+
+// The schedule (chunk_order): this rank's split chunks, then its other
+// chunks, each heaviest first by scan cost (inverted log2 bucket in key bits
+// 32-47, the class in bits 48-49; stable, so ties keep chunk order), then
+// the other ranks' chunks.  Scheduling only; results do not depend on it.
+__global__ void chunk_order_keys(const unsigned long long* __restrict__ cost,
+                                 const unsigned char* __restrict__ role, int nblk,
+                                 uint64_t* __restrict__ keys, int* __restrict__ idx) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nblk) return;
+  const unsigned char r = role[c];
+  const uint32_t cls = r == kRoleSplit ? 0u : r == kRoleMine ? 1u : 2u;
+  const uint32_t bucket =
+      0xFFFFu - min(0xFFFFu, static_cast<uint32_t>(log2(static_cast<double>(cost[c]) + 1.0) * 1024.0));
+  keys[c] = (static_cast<uint64_t>((cls << 16) | bucket) << 32) | static_cast<uint32_t>(c);
   idx[c] = c;
 }
 
@@ -1613,9 +1913,10 @@ int ensure_key_buffers(TruncWorkspace& ws, int n, std::string& err) {
 
 // Stable radix sort of ws.keys/ws.idx (n entries, end_bit key bits); the
 // sorted permutation lands in ws.idx2 and the sorted keys in ws.keys2.
-int radix_sort(TruncWorkspace& ws, int n, int end_bit, cudaStream_t s, std::string& err) {
+int radix_sort(TruncWorkspace& ws, int n, int end_bit, cudaStream_t s, std::string& err,
+               int begin_bit = 0) {
   size_t bytes = 0;
-  TCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, ws.keys, ws.keys2, ws.idx, ws.idx2, n, 0,
+  TCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, ws.keys, ws.keys2, ws.idx, ws.idx2, n, begin_bit,
                                       end_bit, s));
   if (bytes > ws.cub_bytes) {
     if (ws.cub_tmp) cudaFree(ws.cub_tmp);
@@ -1623,8 +1924,9 @@ int radix_sort(TruncWorkspace& ws, int n, int end_bit, cudaStream_t s, std::stri
     TCK(cudaMalloc(&ws.cub_tmp, bytes));
     ws.cub_bytes = bytes;
   }
+  bytes = ws.cub_bytes;
   TCK(cub::DeviceRadixSort::SortPairs(ws.cub_tmp, bytes, ws.keys, ws.keys2, ws.idx, ws.idx2, n,
-                                      0, end_bit, s));
+                                      begin_bit, end_bit, s));
   return 0;
 }
 
@@ -1898,10 +2200,9 @@ __global__ void plan_assemble_kernel(const unsigned long long* __restrict__ acc,
 }  // namespace
 
 void AtomCells::release() {
-  if (chunk_order) cudaFree(chunk_order);
-  chunk_order = nullptr;
-  chunks = 0;
-  order_valid = false;
+  if (chunk_box) cudaFree(chunk_box);
+  chunk_box = nullptr;
+  box_chunks = 0;
   PointOrders::release();
 }
 
@@ -1916,10 +2217,22 @@ void PointOrders::release() {
 
 void TruncWorkspace::release() {
   void* ptrs[] = {cub_tmp, keys, keys2, idx, idx2, b2s, S, atomL, atomJ, atomD, cntd, emptyd, cnt,
-                  hash, empty_fp, pts, near_out, red};
+                  hash, empty_fp, pts, near_out, red, chunk_cost, heavy_flag,
+                  chunk_w, chunk_pre, part_range};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (fork_ev) cudaEventDestroy(fork_ev);
+  if (join_ev) cudaEventDestroy(join_ev);
+  if (side) cudaStreamDestroy(side);
   *this = TruncWorkspace();
+}
+
+static double env_double(const char* name, double dflt) {
+  const char* e = std::getenv(name);
+  if (!e || !*e) return dflt;
+  char* end = nullptr;
+  const double v = std::strtod(e, &end);
+  return end != e ? v : dflt;
 }
 
 static int ensure_target_cells(TruncWorkspace& ws, const DeviceTargets& t, TargetCells& tc,
@@ -1946,7 +2259,14 @@ static int ensure_atom_order(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells
     err = "atom bounding box not set";
     return 1;
   }
-  return build_hilbert(ws, a.x, a.nq, ac, s, err);
+  if (build_hilbert(ws, a.x, a.nq, ac, s, err)) return 1;
+  const int nblk = (a.nq + kFA - 1) / kFA;
+  if (ac.box_chunks != nblk && nblk > 0) {
+    TCK(realloc_exact(ac.chunk_box, 6 * static_cast<size_t>(nblk)));
+    (note_launch(), chunk_box_kernel<<<(nblk + 7) / 8, 256, 0, s>>>(ac.ph, a.nq, nblk, ac.chunk_box));
+    ac.box_chunks = nblk;
+  }
+  return 0;
 }
 
 static int ensure_trunc_ws(TruncWorkspace& ws, int nq, int n, std::string& err) {
@@ -1969,13 +2289,45 @@ static int ensure_trunc_ws(TruncWorkspace& ws, int nq, int n, std::string& err) 
     ws.tgt_cap = c;
   }
   if (!ws.red) TCK(cudaMalloc(&ws.red, sizeof(double) * 4096));
+  const size_t nblk = (static_cast<size_t>(nq) + kFA - 1) / kFA;
+  if (nblk > ws.chunk_cap || !ws.chunk_cost) {
+    const size_t c = std::max<size_t>(nblk, 1);
+    TCK(realloc_exact(ws.chunk_cost, c));
+    TCK(realloc_exact(ws.chunk_w, c));
+    TCK(realloc_exact(ws.chunk_pre, c));
+    TCK(realloc_exact(ws.heavy_flag, c));
+    if (!ws.part_range) TCK(cudaMalloc(&ws.part_range, 5 * sizeof(int)));
+    ws.chunk_cap = c;
+  }
+  if (ws.split_clusters == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kSplit);
+    cfg.blockDim = dim3(kT);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kSplit;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    TCK(cudaOccupancyMaxActiveClusters(&ncl, trunc_fused_split<false>, &cfg));
+    ws.split_clusters = std::max(1, ncl);
+  }
+  if (!ws.side) {
+    int least = 0, greatest = 0;
+    TCK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    TCK(cudaStreamCreateWithPriority(&ws.side, cudaStreamNonBlocking, greatest));
+    TCK(cudaEventCreateWithFlags(&ws.fork_ev, cudaEventDisableTiming));
+    TCK(cudaEventCreateWithFlags(&ws.join_ev, cudaEventDisableTiming));
+  }
   return 0;
 }
 
 int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
                   const DeviceTargets& t, TargetCells& tc, EvalBuffers& b,
                   double eps, double cutoff, int num_sms, DebugOut* dbg,
-                  cudaStream_t s, std::string& err, bool fp32) {
+                  cudaStream_t s, std::string& err, bool fp32, int part_rank, int part_world) {
   // cost.hpp:38-42 and spatial_index.cpp:50,54, evaluated on the host exactly
   // as the reference does.
   const double radius = cutoff < 0.0 ? 0.0 : std::sqrt(2.0 * cutoff);
@@ -2003,7 +2355,51 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
     A.dbg_cnt = reinterpret_cast<uint32_t*>(ws.S); A.dbg_hash = ws.hash; A.dbg_logs = ws.atomL;
     A.cnt_out = ws.cnt;
     const int nblk = (nq + kFA - 1) / kFA;
-    A.chunk_order = (ac.order_valid && ac.chunks == nblk) ? ac.chunk_order : nullptr;
+    A.chunk_order = nullptr;
+    A.role = nullptr;
+    A.heavy_count = ws.part_range + 3;
+    A.queue = ws.part_range + 4;
+    // Scan costs of the chunks -> roles (partitioned atoms: this rank's
+    // work-balanced range; heavy chunks run split across a CTA cluster) and a
+    // heaviest-first schedule.  RSOT_CUDA_SPLIT_ALPHA / RSOT_CUDA_SPLIT_FLOOR
+    // override the split threshold (alpha < 0: off).
+    // (one GPU: the heaviest-first order already hides chunks below a slot's
+    // share, and split CTAs cost ~10 % more per target)
+    const bool part = part_world > 1;
+    const double alpha = fp32 ? -1.0 : env_double("RSOT_CUDA_SPLIT_ALPHA", part ? 0.5 : 1.0);
+    const double floor_t = env_double("RSOT_CUDA_SPLIT_FLOOR", 131072.0);
+    const bool split = alpha >= 0.0;
+    const int* range = nullptr;
+    if (nblk > 1 || part) {
+      if (ensure_key_buffers(ws, nblk, err)) return 1;
+      (note_launch(), chunk_scan_cost<<<(nblk + 7) / 8, 256, 0, s>>>(ac.chunk_box, nblk, g, r_scan, tc.cell_start,
+                                                                    ws.chunk_cost, ws.chunk_w));
+      size_t scan_bytes = 0, sort_bytes = 0;  // (sized together: no reallocation between the uses)
+      TCK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, ws.chunk_w, ws.chunk_pre, nblk, s));
+      TCK(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, ws.keys, ws.keys2, ws.idx, ws.idx2, nblk, 32, 50,
+                                          s));
+      if (std::max(scan_bytes, sort_bytes) > ws.cub_bytes) {
+        if (ws.cub_tmp) cudaFree(ws.cub_tmp);
+        ws.cub_tmp = nullptr;
+        ws.cub_bytes = std::max(scan_bytes, sort_bytes);
+        TCK(cudaMalloc(&ws.cub_tmp, ws.cub_bytes));
+      }
+      scan_bytes = ws.cub_bytes;
+      TCK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp, scan_bytes, ws.chunk_w, ws.chunk_pre, nblk, s));
+      (note_launch(), chunk_range_init<<<1, 1, 0, s>>>(ws.part_range, nq));
+      (note_launch(), chunk_role_kernel<<<(nblk + 255) / 256, 256, 0, s>>>(
+          ws.chunk_cost, ws.chunk_w, ws.chunk_pre, nblk, nq, part_rank, part_world, 4.0 * num_sms, alpha,
+          floor_t, ws.heavy_flag, ws.part_range));
+      (note_launch(), chunk_range_final<<<1, 1, 0, s>>>(ws.part_range, part ? b.res + n + kResVisited : nullptr));
+      (note_launch(), chunk_order_keys<<<(nblk + 255) / 256, 256, 0, s>>>(ws.chunk_cost, ws.heavy_flag, nblk,
+                                                                         ws.keys, ws.idx));
+      if (radix_sort(ws, nblk, 50, s, err, 32)) return 1;  // (class + bucket fields only)
+      A.role = ws.heavy_flag;
+      A.chunk_order = ws.idx2;
+      if (part) range = ws.part_range;
+    } else {
+      (note_launch(), chunk_range_init<<<1, 1, 0, s>>>(ws.part_range, nq));  // (split count 0)
+    }
     if (b.timing) cudaEventRecord(b.timing[1], s);
     if (fp32) {
       if (dbg)
@@ -2011,44 +2407,41 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
       else
         (note_launch(), trunc_fused32<false><<<nblk, kT, 0, s>>>(A));
     } else {
+      if (split && A.role) {
+        // the split clusters go first on a high-priority stream, the rest
+        // fill the GPU around them
+        TCK(cudaEventRecord(ws.fork_ev, s));
+        TCK(cudaStreamWaitEvent(ws.side, ws.fork_ev, 0));
+        const int grid = ws.split_clusters * kSplit;
+        if (dbg)
+          (note_launch(), trunc_fused_split<true><<<grid, kT, 0, ws.side>>>(A));
+        else
+          (note_launch(), trunc_fused_split<false><<<grid, kT, 0, ws.side>>>(A));
+        TCK(cudaEventRecord(ws.join_ev, ws.side));
+      }
       if (dbg)
         (note_launch(), trunc_fused<true><<<nblk, kT, 0, s>>>(A));
       else
         (note_launch(), trunc_fused<false><<<nblk, kT, 0, s>>>(A));
+      if (split && A.role) TCK(cudaStreamWaitEvent(s, ws.join_ev, 0));
     }
     if (b.timing) cudaEventRecord(b.timing[2], s);
     const int nb_near = std::min(4 * num_sms, (nq + 255) / 256 * 8 + 1);
     if (dbg)
       (note_launch(), trunc_nearest_empty<true><<<nb_near, 256, 0, s>>>(ac.ph, nq, ws.cnt, tc.pc, tc.perm_c,
                                                         tc.cell_start, g, b.psi, eps, ws.atomL,
-                                                        ws.atomJ, ws.atomD, ws.empty_fp, ws.hash));
+                                                        ws.atomJ, ws.atomD, ws.empty_fp, ws.hash, range));
     else
       (note_launch(), trunc_nearest_empty<false><<<nb_near, 256, 0, s>>>(ac.ph, nq, ws.cnt, tc.pc, tc.perm_c,
                                                          tc.cell_start, g, b.psi, eps, ws.atomL,
-                                                         ws.atomJ, ws.atomD, ws.empty_fp, ws.hash));
+                                                         ws.atomJ, ws.atomD, ws.empty_fp, ws.hash, range));
     if (b.timing) {
       cudaEventRecord(b.timing[3], s);
       cudaEventRecord(b.timing[4], s);
     }
     (note_launch(), trunc_assemble_fp<<<(n + 255) / 256, 256, 0, s>>>(ws.empty_fp, n, b.res));
-    launch_det_sum(ws.atomJ, nq, ws.red, b.res + n + kResJ, s);
-    launch_det_sum(ws.atomD, nq, ws.red + 1024, b.res + n + kResD, s);
-    launch_det_sum(ws.cntd, nq, ws.red + 2048, b.res + n + kResPairs, s);
-    // heaviest-first chunk schedule for the next evaluation of these atoms
-    if (nblk > 1) {
-      if (ac.chunks != nblk) {
-        if (ac.chunk_order) cudaFree(ac.chunk_order);
-        ac.chunk_order = nullptr;
-        TCK(cudaMalloc(&ac.chunk_order, sizeof(int) * nblk));
-        ac.chunks = nblk;
-      }
-      if (ensure_key_buffers(ws, nblk, err)) return 1;
-      (note_launch(), chunk_cost_kernel<<<(nblk + 255) / 256, 256, 0, s>>>(ws.cntd, nq, nblk, ws.keys, ws.idx));
-      if (radix_sort(ws, nblk, 64, s, err)) return 1;
-      TCK(cudaMemcpyAsync(ac.chunk_order, ws.idx2, sizeof(int) * nblk, cudaMemcpyDeviceToDevice, s));
-      ac.order_valid = true;
-    }
-    launch_det_sum(ws.emptyd, nq, ws.red + 3072, b.res + n + kResEmpty, s);
+    // J, D, pairs, empty in res[n + 0..3] (fixed-order sums of this rank's atoms)
+    launch_det_sum4(ws.atomJ, ws.atomD, ws.cntd, ws.emptyd, nq, range, ws.red, b.res + n + kResJ, s);
     if (dbg) {
       (note_launch(), scatter_debug<uint32_t><<<(nq + 255) / 256, 256, 0, s>>>(
           reinterpret_cast<uint32_t*>(ws.S), ac.perm_h, nq, dbg->count));
@@ -2061,7 +2454,8 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
   } else {
     TCK(cudaMemsetAsync(b.res, 0, sizeof(double) * (n + kResTail), s));
   }
-  (note_launch(), set_visited<<<1, 1, 0, s>>>(b.res, n, static_cast<double>(nq)));
+  if (!(part_world > 1 && nq > 0))  // (partitioned: chunk_role counted this rank's atoms)
+    (note_launch(), set_visited<<<1, 1, 0, s>>>(b.res, n, static_cast<double>(nq)));
   TCK(cudaGetLastError());
   return 0;
 }

@@ -56,13 +56,11 @@ struct TargetCells : PointOrders {
 };
 
 struct AtomCells : PointOrders {
-  // CTA chunk schedule, heaviest first (from the previous evaluation's
-  // candidate counts): the longest chunks start in the first wave instead of
-  // forming the tail.  Scheduling only; results do not depend on it.
-  int* chunk_order = nullptr;
-  int chunks = 0;
-  bool order_valid = false;
-  void release();  // also frees the schedule
+  // bounding box of every Hilbert chunk {lo0, lo1, lo2, hi0, hi1, hi2}
+  // (radius independent: built with the order; feeds the scan-cost pass)
+  double* chunk_box = nullptr;
+  int box_chunks = 0;
+  void release();  // also frees the boxes
 };
 
 struct DebugOut {
@@ -84,16 +82,27 @@ struct TruncWorkspace {
   unsigned long long* empty_fp = nullptr; size_t tgt_cap = 0;
   double* pts = nullptr; unsigned long long* near_out = nullptr; size_t pts_cap = 0;
   double* red = nullptr;  // reduction partials
+  // heavy-chunk split (trunc_fused_split): scanned targets per chunk, flags,
+  // the compacted list and its length; the side stream it runs on
+  unsigned long long* chunk_cost = nullptr; unsigned char* heavy_flag = nullptr;  // (role per chunk)
+  size_t chunk_cap = 0;
+  unsigned long long* chunk_w = nullptr; unsigned long long* chunk_pre = nullptr;
+  int* part_range = nullptr;                  // [5]: this rank's atoms [lo, hi), atom count, split count, queue
+  int split_clusters = 0;                     // resident clusters of trunc_fused_split
+  cudaStream_t side = nullptr; cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   void release();
 };
 
 // Full truncated evaluation of this rank's atoms (after launch_prologue);
+// part_world > 1: `a` holds every atom and this call evaluates the chunks
+// chunk_role assigns to rank part_rank (work-balanced over the Hilbert order);
 // leaves the packed partial result in b.res like launch_dense.  Returns 0
 // or nonzero with err set.
 int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
                   const DeviceTargets& t, TargetCells& tc, EvalBuffers& b,
                   double eps, double cutoff, int num_sms, DebugOut* dbg,
-                  cudaStream_t s, std::string& err, bool fp32 = false);
+                  cudaStream_t s, std::string& err, bool fp32 = false,
+                  int part_rank = 0, int part_world = 1);
 
 // Dense-path debug outputs (count = N, hash over all targets, ln S_q).
 void launch_dense_debug(const DeviceAtoms& a, const DeviceTargets& t,

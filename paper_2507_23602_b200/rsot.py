@@ -255,6 +255,7 @@ class Context:
         self.device = int(device)
         self.rank = 0
         self.world = 1
+        self.vworld = 1
 
     @classmethod
     def default(cls, device: int = 0) -> "Context":
@@ -273,6 +274,13 @@ class Context:
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         _lib.check(self.lib.rsot_cuda_ctx_set_comm(self.handle, int(rank), int(world), buf))
         self.rank, self.world = int(rank), int(world)
+
+    def set_virtual_rank(self, rank: int, world: int) -> None:
+        """Testing / diagnostics without a communicator: evaluate partitioned
+        atoms as rank `rank` of `world` (the result is that rank's partial,
+        finalised alone; include/rsot_cuda.h)."""
+        _lib.check(self.lib.rsot_cuda_ctx_set_virtual_rank(self.handle, int(rank), int(world)))
+        self.vworld = int(world)
 
     def shard_range(self, nq: int):
         lo, hi = ctypes.c_size_t(), ctypes.c_size_t()
@@ -338,18 +346,27 @@ class DeviceTargets:
 
 
 class DeviceAtoms:
-    """Resident shard of SourceAtoms (points, masses) on one context."""
+    """Resident SourceAtoms (points, masses) on one context.
 
-    def __init__(self, ctx: Context, points, masses, shard: bool = True):
+    shard=True on a multi-rank context: balanced=True (default) keeps every
+    atom on every rank and lets each evaluation split the work (truncated:
+    work-balanced Hilbert chunk ranges; rsot_cuda_atoms_create_partitioned),
+    balanced=False uploads only this rank's contiguous parallel_blocks range
+    (parallel.hpp:14-31).  shard=False: every rank evaluates every atom."""
+
+    def __init__(self, ctx: Context, points, masses, shard: bool = True, balanced: bool = True):
         self.ctx = ctx
         pts = _points3(points)
         m = np.ascontiguousarray(np.asarray(masses, dtype=np.float64))
-        lo, hi = ctx.shard_range(len(pts)) if shard else (0, len(pts))
+        multi = ctx.world > 1 or getattr(ctx, "vworld", 1) > 1
+        partitioned = shard and balanced and multi
+        lo, hi = ctx.shard_range(len(pts)) if shard and not partitioned else (0, len(pts))
         pts = np.ascontiguousarray(pts[lo:hi])
         m = np.ascontiguousarray(m[lo:hi])
         h = ctypes.c_void_p()
-        _lib.check(ctx.lib.rsot_cuda_atoms_create(ctx.handle, _ptr(pts), _ptr(m), len(pts),
-                                                  ctypes.byref(h)))
+        create = ctx.lib.rsot_cuda_atoms_create_partitioned if partitioned else ctx.lib.rsot_cuda_atoms_create
+        _lib.check(create(ctx.handle, _ptr(pts), _ptr(m), len(pts), ctypes.byref(h)))
+        self.partitioned = partitioned
         self.handle = h
         self.nq = len(pts)
         self.lo, self.hi = lo, hi
@@ -410,7 +427,8 @@ def _device_targets(target: TargetMeasure, ctx: Context) -> DeviceTargets:
 
 
 def _device_atoms(atoms: SourceAtoms, ctx: Context) -> DeviceAtoms:
-    key = (id(ctx), atoms.points.ctypes.data, atoms.masses.ctypes.data, atoms.size(), ctx.world)
+    key = (id(ctx), atoms.points.ctypes.data, atoms.masses.ctypes.data, atoms.size(), ctx.world,
+           getattr(ctx, "vworld", 1))
     dev = getattr(atoms, "_rsot_dev", None)
     if dev is None or dev[0] != key:
         dev = (key, DeviceAtoms(ctx, atoms.points, atoms.masses))

@@ -431,3 +431,112 @@ def test_dense_graph_replay_matches_direct_launches():
     for k in range(2):
         for o in outs[1:]:
             assert np.array_equal(outs[0][k][0], o[k][0]) and np.array_equal(outs[0][k][1], o[k][1])
+
+
+@pytest.mark.parametrize("mode", ["all", "default", "off"])
+def test_heavy_chunk_split_parity(mode, monkeypatch):
+    """Heavy chunks run split across a cluster of 8 CTAs (truncated.cu
+    trunc_fused_split: every 8th target row per CTA, phase-1 sums / counts /
+    hashes combined through distributed shared memory in rank order).  A dense
+    atom cluster over a dense target cluster makes the heavy chunks; `all`
+    forces every chunk (up to one per SM) through the split kernel.  Candidate
+    sets exact, values within 1e-10, bitwise deterministic."""
+    if mode == "all":
+        monkeypatch.setenv("RSOT_CUDA_SPLIT_ALPHA", "0")
+        monkeypatch.setenv("RSOT_CUDA_SPLIT_FLOOR", "0")
+    elif mode == "off":
+        monkeypatch.setenv("RSOT_CUDA_SPLIT_ALPHA", "-1")
+    ctx = rs.Context(0)
+    rng = np.random.default_rng(3031)
+    A = np.vstack([0.48 + 0.04 * rng.uniform(size=(3000, 3)), rng.uniform(size=(20000, 3))])
+    T = np.vstack([0.45 + 0.1 * rng.uniform(size=(120000, 3)), rng.uniform(size=(30000, 3))])
+    M = rng.uniform(size=len(A)) + 0.1
+    M /= M.sum()
+    W = rng.uniform(size=len(T)) + 0.1
+    W /= W.sum()
+    psi = rng.normal(0, 2e-3, size=len(T))
+    eps, cutoff = 2e-3, 0.004
+    atoms = rs.SourceAtoms(dim=3, points=A, masses=M)
+    tgt = rs.TargetMeasure(dim=3, points=T, weights=W)
+    res, cnt, hsh, _ = rs.evaluate_dual_debug(atoms, tgt, psi, eps, cutoff, ctx=ctx)
+    want = C.evaluate_dual(A, M, T, W, psi, eps, cutoff, per_atom=True, workers=8)
+    assert np.array_equal(cnt, want["count"]) and np.array_equal(hsh, want["hash"])
+    runs = [gpu_eval(ctx, A, M, T, W, psi, eps, cutoff) for _ in range(2)]
+    assert runs[0]["J"] == runs[1]["J"] and np.array_equal(runs[0]["gradient"], runs[1]["gradient"])
+    dbg = dict(J=res.J, D=res.D, gradient=res.gradient, atoms_visited=res.atoms_visited,
+               candidate_pairs=res.candidate_pairs, empty_candidate_atoms=res.empty_candidate_atoms)
+    for got in (dbg, runs[0]):
+        assert_parity(got, want, marginal_scale(W, want["gradient"]), TOL)
+
+
+def _clustered_instance(rng, nq_side=40, n=30000, background=0):
+    g = (np.arange(nq_side) + 0.5) / nq_side
+    A = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
+    means = rng.uniform(0.3, 0.7, size=(3, 3))
+    T = np.concatenate([m + 0.06 * rng.standard_normal((n // 3, 3)) for m in means] +
+                       [rng.uniform(size=(background, 3))])
+    M = rng.uniform(size=len(A)) + 0.1
+    M /= M.sum()
+    W = np.full(len(T), 1.0 / len(T))
+    psi = rng.normal(0, 1e-3, size=len(T))
+    return A, M, T, W, psi
+
+
+def _virtual_rank_sum(A, M, T, W, psi, eps, cutoff, world, precision):
+    ctx = rs.Context(0)
+    ctx.set_precision(precision)
+    parts = []
+    for r in range(world):
+        ctx.set_virtual_rank(r, world)
+        parts.append(gpu_eval(ctx, A, M, T, W, psi, eps, cutoff))
+    psinu = float(np.dot(psi, W))
+    got = dict(J=sum(p["J"] for p in parts) + (world - 1) * psinu, D=sum(p["D"] for p in parts),
+               gradient=sum(p["gradient"] for p in parts) + (world - 1) * W,
+               atoms_visited=sum(p["atoms_visited"] for p in parts),
+               candidate_pairs=sum(p["candidate_pairs"] for p in parts),
+               empty_candidate_atoms=sum(p["empty_candidate_atoms"] for p in parts))
+    return ctx, parts, got
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_partitioned_atoms_virtual_ranks(precision):
+    """Partitioned atoms (rsot_cuda_atoms_create_partitioned): every rank
+    holds all atoms and a truncated evaluation takes the work-balanced
+    Hilbert chunk range chunk_role_kernel assigns it (dense: equal atom
+    ranges).  On one GPU the ranks are virtual (rsot_cuda_ctx_set_virtual_rank):
+    the per-rank partials, summed as the collective would, must reproduce the
+    oracle (candidate counts exact) and cover every atom once; each rank's
+    partial is bitwise reproducible."""
+    rng = np.random.default_rng(555)
+    A, M, T, W, psi = _clustered_instance(rng)
+    tol = TOL if precision == "fp64" else 2e-5
+    for eps, cutoff in ((2e-3, 0.004), (0.01, math.inf)):
+        want = C.evaluate_dual(A, M, T, W, psi, eps, cutoff, workers=8)
+        for world in (2, 3, 8):
+            ctx, parts, got = _virtual_rank_sum(A, M, T, W, psi, eps, cutoff, world, precision)
+            assert got["atoms_visited"] == len(A)
+            assert all(p["atoms_visited"] > 0 for p in parts)
+            assert_parity(got, want, marginal_scale(W, want["gradient"]), tol)
+            if math.isfinite(cutoff):
+                ctx.set_virtual_rank(world - 1, world)
+                again = gpu_eval(ctx, A, M, T, W, psi, eps, cutoff)
+                assert again["J"] == parts[-1]["J"] and np.array_equal(again["gradient"], parts[-1]["gradient"])
+
+
+def test_partitioned_atoms_balance():
+    """Without empty candidate sets the chunk weights track the accepted
+    pairs: 8 virtual ranks stay within 1.5x of the mean pairs on a clustered
+    instance (with a uniform background: no empty sets) where equal atom
+    ranges reach 2.5x."""
+    rng = np.random.default_rng(555)
+    A, M, T, W, psi = _clustered_instance(rng, background=8000)
+    eps, cutoff = 5e-3, 0.008
+    want = C.evaluate_dual(A, M, T, W, psi, eps, cutoff, per_atom=True, workers=8)
+    assert want["empty_candidate_atoms"] == 0
+    _, parts, got = _virtual_rank_sum(A, M, T, W, psi, eps, cutoff, 8, "fp64")
+    assert_parity(got, want, marginal_scale(W, want["gradient"]), TOL)
+    pairs = np.array([p["candidate_pairs"] for p in parts], dtype=float)
+    assert pairs.max() / pairs.mean() < 1.5, pairs
+    cnt = want["count"].astype(float)
+    contiguous = np.array([cnt[len(A) * r // 8:len(A) * (r + 1) // 8].sum() for r in range(8)])
+    assert contiguous.max() / contiguous.mean() > 2.0

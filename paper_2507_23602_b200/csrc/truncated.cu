@@ -540,11 +540,11 @@ constexpr unsigned char kRoleOther = 0, kRoleMine = 1, kRoleSplit = 2;
 // 7.4e-8 ms per scanned target + 3.8e-9 ms per accepted pair; the chunk's
 // pairs are ~256 x the targets within reach of its centre, so a centre-ball
 // target weighs 256 x 0.051 = 13; fixed cost per chunk ~0.25 us per slot; an
-// empty-set atom's nearest search ~105 units: cfg3 3 ms for 3.8e5 of them
+// empty-set atom's nearest search ~32 units: cfg3 0.9 ms for 3.8e5 of them
 // against 58 ms for 7.8e8 units)
 constexpr unsigned long long kChunkBase = 128;
 constexpr unsigned long long kPairWeight = 13;
-constexpr unsigned long long kEmptyAtomCost = 105;
+constexpr unsigned long long kEmptyAtomCost = 32;
 
 // Another rank's chunk: nothing to do (the sums and trunc_nearest_empty
 // only read this rank's atom range); the debug outputs are zeroed.
@@ -1298,7 +1298,7 @@ trunc_fused(FusedArgs A) {
 // whole GPU's per-slot share of pairs).  Persistent: one resident wave of
 // clusters pulls the split chunks heaviest first from a queue (any count,
 // no host round trip).
-constexpr int kSplit = 8;
+constexpr int kSplit = 8;  // (16, non-portable: +40 % at cfg3 8-way)
 
 template <bool DEBUG>
 __global__ void __cluster_dims__(kSplit, 1, 1) __launch_bounds__(kT, 4)
@@ -1349,7 +1349,7 @@ struct Fused32Smem {
   int rowStart[kT];
   int rowPref[kT + 1];
   ListT wlist[kT / 32][kTileT32];
-  float colW[kT / 32][kTileT32];
+  alignas(16) float colW[kT / 32][kTileT32];  // (also the split exchange: 8-byte fields)
   float wmax[kT / 32];
   Region R;
   double sh[200];
@@ -1536,9 +1536,10 @@ __device__ __forceinline__ void batch32(const SM& sm, const FusedArgs& A, Atoms3
   if (!(lane & 1) && item < nsel) col[list[item] >> 4] = tot;
 }
 
-template <int PHASE, bool DEBUG>
+template <int PHASE, bool DEBUG, int KS = 1>
 __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox& wb,
-                             float cull_thr, double& Bc, Atoms32& at, unsigned& bandmask) {
+                             float cull_thr, double& Bc, Atoms32& at, unsigned& bandmask,
+                             int split = 0) {
   // bandmask bit i: phase 1 met a pair in the FP32 error band in this warp's
   // tile i; phase 2 re-tests only those tiles (same tiles, same lists)
   int tix = 0;
@@ -1559,12 +1560,17 @@ __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox&
     sm.rowPref[threadIdx.x] = pre;
     if (threadIdx.x == 0) sm.rowPref[kT] = total;
     __syncthreads();  // the prefetch reads every thread's row range
-    if (total > 0) fused_prefetch32(sm, A, 0, min(kTileT32, total));
-    for (int base = 0; base < total; base += kTileT32) {
-      const int cnt = min(kTileT32, total - base);
+    int tile = kTileT32, start = 0, step = kTileT32;  // (split: as fused_scan)
+    if (KS > 1) {
+      tile = min(kTileT32, max(32, (total + 4 * KS - 1) / (4 * KS)));
+      start = split * tile;
+      step = KS * tile;
+    }
+    if (start < total) fused_prefetch32(sm, A, start, min(tile, total - start));
+    for (int base = start; base < total; base += step) {
+      const int cnt = min(tile, total - base);
       fused_stage32<PHASE>(sm, A, cnt, Bc, at);
-      if (base + kTileT32 < total)
-        fused_prefetch32(sm, A, base + kTileT32, min(kTileT32, total - base - kTileT32));
+      if (base + step < total) fused_prefetch32(sm, A, base + step, min(tile, total - base - step));
       const int nsel = fused_cull<Fused32Smem, 4>(sm, cnt, wb, cull_thr, list);
       if (PHASE == 1) {
         float2 acc = make_float2(0.f, 0.f), cn = make_float2(0.f, 0.f);
@@ -1603,14 +1609,22 @@ __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox&
   }
 }
 
-template <bool DEBUG>
-__global__ void __launch_bounds__(kT, 4)
-trunc_fused32(FusedArgs A) {
-  __shared__ Fused32Smem sm;
+// Phase-1 partials of one fp32 split CTA (aliases colW; see SplitXchg).
+struct SplitXchg32 {
+  double S[2][kT];
+  uint64_t H[2][kT];
+  uint32_t C[2][kT];
+  double B;  // the CTA's running shift
+};
+static_assert(sizeof(SplitXchg32) <= sizeof(float) * (kT / 32) * kTileT32, "exchange fits colW");
+
+// fp32 chunk body (fused_body's counterpart).  KS > 1: the splits' shifts
+// combine to B = max_r B_r and S = sum_r S_r 2^(B_r - B) in rank order, the
+// shift an unsplit CTA would have reached; phase 2 runs at B.
+template <bool DEBUG, int KS>
+__device__ __forceinline__ void fused32_body(Fused32Smem& sm, const FusedArgs& A, int chunk, int split) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   Atoms32 at;
-  const int chunk = A.chunk_order ? A.chunk_order[blockIdx.x] : static_cast<int>(blockIdx.x);
-  if (A.role && A.role[chunk] == kRoleOther) return fused_skip_chunk<DEBUG>(A, chunk);
   at.qa = chunk * kFA + warp * 64 + lane;
   at.qb = at.qa + 32;
   const bool va = at.qa < A.nq, vb = at.qb < A.nq;
@@ -1650,17 +1664,87 @@ trunc_fused32(FusedArgs A) {
   double Bc = -0x1p1000;  // running CTA shift (log2 units)
 
   unsigned bandmask = 0;
-  fused_scan32<1, DEBUG>(sm, A, wb, cull_thr, Bc, at, bandmask);
+  fused_scan32<1, DEBUG, KS>(sm, A, wb, cull_thr, Bc, at, bandmask, split);
 
+  if constexpr (KS > 1) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    SplitXchg32* x = reinterpret_cast<SplitXchg32*>(&sm.colW[0][0]);
+    const int t = threadIdx.x;
+    x->S[0][t] = at.Sa; x->S[1][t] = at.Sb;
+    x->C[0][t] = at.ca; x->C[1][t] = at.cb;
+    if (DEBUG) { x->H[0][t] = at.ha; x->H[1][t] = at.hb; }
+    if (t == 0) x->B = Bc;
+    cl.sync();  // partials of every split visible cluster-wide
+    double Bm = -0x1p1000;
+#pragma unroll
+    for (int r = 0; r < KS; ++r) Bm = fmax(Bm, cl.map_shared_rank(x, r)->B);
+    double sa = 0.0, sb = 0.0;
+    uint32_t ca = 0, cb = 0;
+    uint64_t ha = 0, hb = 0;
+#pragma unroll
+    for (int r = 0; r < KS; ++r) {  // rank order: identical in every CTA
+      const SplitXchg32* xr = cl.map_shared_rank(x, r);
+      const double f = exp2(xr->B - Bm);
+      sa += xr->S[0][t] * f; sb += xr->S[1][t] * f;
+      ca += xr->C[0][t]; cb += xr->C[1][t];
+      if (DEBUG) { ha += xr->H[0][t]; hb += xr->H[1][t]; }
+    }
+    cl.sync();  // no CTA reuses colW (phase 2) while a peer still reads it
+    at.Sa = sa; at.Sb = sb; at.ca = ca; at.cb = cb; at.ha = ha; at.hb = hb;
+    Bc = Bm;
+  }
+
+  const bool primary = split == 0;
   double wa, wb2;
   fused_finalize<DEBUG>(A, Bc, true, va, at.ca != 0u, static_cast<double>(at.ca + at.cb), at.ca,
-                        at.Sa, 0.0, at.qa, at.ha, wa, 0x1p-80);
+                        at.Sa, 0.0, at.qa, at.ha, wa, 0x1p-80, primary);
   fused_finalize<DEBUG>(A, Bc, true, vb, at.cb != 0u, 0.0, at.cb, at.Sb, 0.0, at.qb, at.hb, wb2,
-                        0x1p-80);
+                        0x1p-80, primary);
   at.wa = static_cast<float>(wa);
   at.wb = static_cast<float>(wb2);
 
-  fused_scan32<2, DEBUG>(sm, A, wb, cull_thr, Bc, at, bandmask);
+  fused_scan32<2, DEBUG, KS>(sm, A, wb, cull_thr, Bc, at, bandmask, split);
+}
+
+template <bool DEBUG>
+__global__ void __launch_bounds__(kT, 4)
+trunc_fused32(FusedArgs A) {
+  __shared__ Fused32Smem sm;
+  int chunk = static_cast<int>(blockIdx.x);
+  if (A.chunk_order) {  // the split chunks lead the order (trunc_fused32_split)
+    const int pos = *A.heavy_count + chunk;
+    if (pos >= (A.nq + kFA - 1) / kFA) return;
+    chunk = A.chunk_order[pos];
+  }
+  if (A.role) {
+    const unsigned char r = A.role[chunk];
+    if (r == kRoleOther) return fused_skip_chunk<DEBUG>(A, chunk);
+    if (r == kRoleSplit) return;  // run by trunc_fused32_split
+  }
+  fused32_body<DEBUG, 1>(sm, A, chunk, 0);
+}
+
+template <bool DEBUG>
+__global__ void __cluster_dims__(kSplit, 1, 1) __launch_bounds__(kT, 4)
+trunc_fused32_split(FusedArgs A) {
+  __shared__ Fused32Smem sm;
+  __shared__ int next;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int split = static_cast<int>(cl.block_rank());
+  const int count = *A.heavy_count;
+  for (;;) {  // as trunc_fused_split
+    if (split == 0 && threadIdx.x == 0) next = atomicAdd(A.queue, 1);
+    cl.sync();
+    const int h = *cl.map_shared_rank(&next, 0);
+    if (h >= count) {
+      cl.sync();
+      break;
+    }
+    fused32_body<DEBUG, kSplit>(sm, A, A.chunk_order[h], split);
+    __syncthreads();
+  }
 }
 
 // Chunk cost = the chunk's candidate pairs of the last evaluation; key =
@@ -2310,9 +2394,11 @@ static int ensure_trunc_ws(TruncWorkspace& ws, int nq, int n, std::string& err) 
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    int ncl = 0;
+    int ncl = 0, ncl32 = 0;
     TCK(cudaOccupancyMaxActiveClusters(&ncl, trunc_fused_split<false>, &cfg));
+    TCK(cudaOccupancyMaxActiveClusters(&ncl32, trunc_fused32_split<false>, &cfg));
     ws.split_clusters = std::max(1, ncl);
+    ws.split_clusters32 = std::max(1, ncl32);
   }
   if (!ws.side) {
     int least = 0, greatest = 0;
@@ -2366,7 +2452,7 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
     // (one GPU: the heaviest-first order already hides chunks below a slot's
     // share, and split CTAs cost ~10 % more per target)
     const bool part = part_world > 1;
-    const double alpha = fp32 ? -1.0 : env_double("RSOT_CUDA_SPLIT_ALPHA", part ? 0.5 : 1.0);
+    const double alpha = env_double("RSOT_CUDA_SPLIT_ALPHA", part ? 0.5 : 1.0);
     const double floor_t = env_double("RSOT_CUDA_SPLIT_FLOOR", 131072.0);
     const bool split = alpha >= 0.0;
     const int* range = nullptr;
@@ -2402,10 +2488,21 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
     }
     if (b.timing) cudaEventRecord(b.timing[1], s);
     if (fp32) {
+      if (split && A.role) {
+        TCK(cudaEventRecord(ws.fork_ev, s));
+        TCK(cudaStreamWaitEvent(ws.side, ws.fork_ev, 0));
+        const int grid = ws.split_clusters32 * kSplit;
+        if (dbg)
+          (note_launch(), trunc_fused32_split<true><<<grid, kT, 0, ws.side>>>(A));
+        else
+          (note_launch(), trunc_fused32_split<false><<<grid, kT, 0, ws.side>>>(A));
+        TCK(cudaEventRecord(ws.join_ev, ws.side));
+      }
       if (dbg)
         (note_launch(), trunc_fused32<true><<<nblk, kT, 0, s>>>(A));
       else
         (note_launch(), trunc_fused32<false><<<nblk, kT, 0, s>>>(A));
+      if (split && A.role) TCK(cudaStreamWaitEvent(s, ws.join_ev, 0));
     } else {
       if (split && A.role) {
         // the split clusters go first on a high-priority stream, the rest

@@ -88,7 +88,7 @@ struct TruncWorkspace {
   size_t chunk_cap = 0;
   unsigned long long* chunk_w = nullptr; unsigned long long* chunk_pre = nullptr;
   int* part_range = nullptr;                  // [5]: this rank's atoms [lo, hi), atom count, split count, queue
-  int split_clusters = 0;                     // resident clusters of trunc_fused_split
+  int split_clusters = 0, split_clusters32 = 0;  // resident clusters of trunc_fused(32)_split
   cudaStream_t side = nullptr; cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   void release();
 };

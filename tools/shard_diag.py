@@ -20,6 +20,7 @@ psi = p.psi(0)
 cut = p.cutoff(psi)
 ctx = rs.Context(0)
 ctx.set_timing(True)
+ctx.set_precision(os.environ.get("RSOT_PRECISION", "fp64"))
 lib = _lib.load()
 dev_t = rs.rsot.DeviceTargets(ctx, p.targets, p.nu)
 

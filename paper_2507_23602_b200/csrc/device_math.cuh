@@ -205,6 +205,41 @@ __device__ inline double fp_to_double(const unsigned long long* acc) {
          static_cast<double>(acc[0]) * 0x1p-150;
 }
 
+// Gradient accumulator of the truncated kernels: 5 limbs of 32 bits at
+// weights 2^(32 i - 150), each limb word a u64 with 2^32 adds of headroom,
+// so contributions are added with fire-and-forget reductions (RED, no
+// returned value, no carry chain: fp_add's ATOM round trips stalled the
+// phase-2 warps on their results).  Integer sums are order independent, so
+// the total is deterministic; bits below 2^-150 are dropped as in fp_add.
+constexpr int kLimbs = 5;
+__device__ __forceinline__ void fp_red(unsigned long long* acc, double m) {
+  if (!(m > 0.0)) return;
+  int e;
+  const double fr = frexp(m, &e);
+  unsigned long long mant = static_cast<unsigned long long>(ldexp(fr, 53));
+  int sh = e - 53 + 150;  // value = mant * 2^sh (units of 2^-150)
+  if (sh < 0) {
+    if (sh <= -64) return;
+    mant >>= -sh;
+    sh = 0;
+  }
+  const int i0 = sh >> 5;
+  const unsigned __int128 w = static_cast<unsigned __int128>(mant) << (sh & 31);  // < 2^85
+  const unsigned long long l0 = static_cast<unsigned long long>(w) & 0xffffffffull;
+  const unsigned long long l1 = static_cast<unsigned long long>(w >> 32) & 0xffffffffull;
+  const unsigned long long l2 = static_cast<unsigned long long>(w >> 64);
+  if (l0 && i0 < kLimbs) atomicAdd(acc + i0, l0);
+  if (l1 && i0 + 1 < kLimbs) atomicAdd(acc + i0 + 1, l1);
+  if (l2 && i0 + 2 < kLimbs) atomicAdd(acc + i0 + 2, l2);
+}
+
+__device__ __forceinline__ double fp_limbs_to_double(const unsigned long long* acc) {
+  return (((static_cast<double>(acc[4]) * 0x1p-22 + static_cast<double>(acc[3]) * 0x1p-54) +
+           static_cast<double>(acc[2]) * 0x1p-86) +
+          static_cast<double>(acc[1]) * 0x1p-118) +
+         static_cast<double>(acc[0]) * 0x1p-150;
+}
+
 // cost.hpp:19-33: dot(p, q) = (p0 q0 + p1 q1) + p2 q2, clamp, acos, square.
 __device__ __forceinline__ double geo_cost(double x0, double x1, double x2, double y0, double y1,
                                            double y2) {

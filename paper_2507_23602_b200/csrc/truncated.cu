@@ -240,6 +240,45 @@ __device__ __forceinline__ int find_row(const int* pref, int s) {
   return lo;
 }
 
+// Interleaved tiles (load balance between the CTA's warps): a row batch's
+// `total` positions form ng = ceil(total / kGroup) groups of kGroup
+// consecutive (cell-ordered, hence close) targets, and tile k holds groups
+// k, k + ntile, k + 2 ntile, ...  Every tile then samples the whole scanned
+// region, so each warp's culled share of a tile tracks its share of the
+// batch; contiguous tiles (a few cell rows each) loaded the warps whose box
+// is nearest those rows and left the others waiting at the tile barrier
+// (ncu: 15 % of the cfg5 warp samples at the two per-tile barriers).
+// Groups keep the staging loads coalesced (8 x 32 B of target records).
+// Measured: fp64 cfg5 -2 %, cfg3 unchanged; the fp32 kernel keeps contiguous
+// tiles (+1-3 % there: its shorter steps feel the scattered staging loads).
+constexpr int kGroup = 8;
+struct TileMap {
+  int total, tile, ng, ntile;
+  bool inter;  // interleaved groups (fp64 kernel) or contiguous tiles (fp32 kernel)
+};
+__device__ __forceinline__ TileMap tile_map(int total, int tile, bool inter) {
+  TileMap m;
+  m.total = total;
+  m.tile = tile;
+  m.inter = inter;
+  m.ng = (total + kGroup - 1) / kGroup;
+  const int gpt = tile / kGroup;
+  m.ntile = inter ? (m.ng + gpt - 1) / gpt : (total + tile - 1) / tile;
+  return m;
+}
+// Positions in tile k (< ntile); at most `tile`.
+__device__ __forceinline__ int tile_count(const TileMap& m, int k) {
+  if (!m.inter) return min(m.tile, m.total - k * m.tile);
+  const int nu = (m.ng - k + m.ntile - 1) / m.ntile;
+  const int last = k + (nu - 1) * m.ntile;
+  return (nu - 1) * kGroup + min(kGroup, m.total - last * kGroup);
+}
+// Batch position of entry t of tile k.
+__device__ __forceinline__ int tile_pos(const TileMap& m, int k, int t) {
+  if (!m.inter) return k * m.tile + t;
+  return (k + (t / kGroup) * m.ntile) * kGroup + (t % kGroup);
+}
+
 // Warp bounding box (local fp32 coordinates) of the warp's own points.
 struct WarpBox {
   float lo0, lo1, lo2, hi0, hi1, hi2;
@@ -459,7 +498,7 @@ __global__ void trunc_nearest_empty(const double4* __restrict__ xs, int nq,
         atomL[qq] = L;
         atomJ[qq] = eps * L * a.w;
         atomD[qq] = a.w * exp(-L);
-        fp_add(empty_fp + 3 * static_cast<size_t>(bj), a.w);
+        fp_red(empty_fp + kLimbs * static_cast<size_t>(bj), a.w);
         if (DEBUG) hash_out[qq] = candidate_hash_term(static_cast<uint64_t>(bj));
       }
     }
@@ -525,7 +564,7 @@ struct FusedArgs {
   const double* scal; const double* psi;
   double c2, r2, r_scan, eps;
   double* atomJ; double* atomD; double* cntd; double* emptyd;
-  unsigned long long* gacc;              // [3 N] fixed point, original index
+  unsigned long long* gacc;              // [kLimbs N] fixed point (fp_red), original index
   uint32_t* dbg_cnt; uint64_t* dbg_hash; double* dbg_logs;  // Hilbert order
   uint32_t* cnt_out;                     // 0 = empty candidate set (Hilbert order)
   const int* chunk_order;                // CTA -> atom chunk (heaviest first) or null
@@ -635,9 +674,10 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // Issues the copies of tile [base, base + cnt) of the current row batch
 // (each thread its entries tid + u kT; the same thread converts them).
-__device__ __forceinline__ void fused_prefetch(FusedSmem& sm, const FusedArgs& A, int base, int cnt) {
+__device__ __forceinline__ void fused_prefetch(FusedSmem& sm, const FusedArgs& A, const TileMap& m,
+                                               int tk, int cnt) {
   for (int t = threadIdx.x; t < cnt; t += kT) {
-    const int s = base + t;
+    const int s = tile_pos(m, tk, t);
     const int r = find_row(sm.rowPref, s);
     const int k = sm.rowStart[r] + (s - sm.rowPref[r]);
     sm.rawK[t] = k;  // tK of the tile being computed is still in use
@@ -666,6 +706,17 @@ __device__ __forceinline__ void fused_convert(FusedSmem& sm, const FusedArgs& A,
     sm.tN1[t] = make_float2(f2, f2);
     sm.tJ[t] = sm.rawJ[t];
     sm.tK[t] = sm.rawK[t];
+  }
+}
+
+// Phase 2: the CTA's column sums of the last computed tile (its `cnt`
+// entries), added once per target into the fixed-point accumulator.  Called
+// after a barrier, with the thread -> entry map of fused_convert, so the
+// same thread reads an entry's tJ before converting the next tile over it.
+__device__ __forceinline__ void fused_flush_cols(const FusedSmem& sm, const FusedArgs& A, int cnt) {
+  for (int s = threadIdx.x; s < cnt; s += kT) {
+    const double c = ((sm.colW[0][s] + sm.colW[1][s]) + sm.colW[2][s]) + sm.colW[3][s];
+    if (c > 0.0) fp_red(A.gacc + kLimbs * static_cast<size_t>(sm.tJ[s]), c);
   }
 }
 
@@ -1006,6 +1057,7 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
   const bool va = at.qa < A.nq, vb = at.qb < A.nq;
   const int ny = sm.R.c_hi[1] - sm.R.c_lo[1] + 1;
   const int nrows = ny * (sm.R.c_hi[2] - sm.R.c_lo[2] + 1);
+  int pend = 0;  // phase 2: entries of the previous tile with pending column sums
   for (int rb = 0; rb < nrows; rb += kT) {
     int st = 0, ln = 0;
     if (rb + threadIdx.x < nrows)
@@ -1016,19 +1068,20 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
     sm.rowPref[threadIdx.x] = pre;
     if (threadIdx.x == 0) sm.rowPref[kT] = total;
     __syncthreads();  // row ranges visible; previous batch fully consumed
-    int tile = kTileT, start = 0, step = kTileT;
-    if (KS > 1) {
-      tile = min(kTileT, max(32, (total + 4 * KS - 1) / (4 * KS)));
-      start = split * tile;
-      step = KS * tile;
-    }
-    if (start < total) fused_prefetch(sm, A, start, min(tile, total - start));
-    for (int base = start; base < total; base += step) {
-      const int cnt = min(tile, total - base);
+    int tile = kTileT;
+    if (KS > 1) tile = min(kTileT, max(32, (total + 4 * KS - 1) / (4 * KS))) & ~(kGroup - 1);
+    const TileMap tm = tile_map(total, tile, true);
+    if (split < tm.ntile) fused_prefetch(sm, A, tm, split, tile_count(tm, split));
+    for (int tk = split; tk < tm.ntile; tk += KS) {
+      const int cnt = tile_count(tm, tk);
       __syncthreads();  // every warp is done with the previous tile
+      if (PHASE == 2) {  // its column sums, before its entries are overwritten
+        fused_flush_cols(sm, A, pend);
+        pend = 0;
+      }
       fused_convert(sm, A, B, cnt);
       __syncthreads();  // staged tile visible, landing zone free
-      if (base + step < total) fused_prefetch(sm, A, base + step, min(tile, total - base - step));
+      if (tk + KS < tm.ntile) fused_prefetch(sm, A, tm, tk + KS, tile_count(tm, tk + KS));
       int nfull = 0;
       const int nsel = fused_cull2(sm, cnt, wb, cull_thr, full_thr, list, kTileT, &nfull);
       if (PHASE == 1) {
@@ -1069,14 +1122,14 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
         for (int b0 = 0; b0 < nsel; b0 += 16)
           batch64<SAFE, DEBUG, true>(sm, A, at, K, wide, list, b0, nsel, col);
         for (int b0 = 0; b0 < nfull; b0 += 16) batch64_full<SAFE>(sm, at, wide, full, b0, nfull, va, vb, col);
-        __syncthreads();
-        for (int s = threadIdx.x; s < cnt; s += kT) {
-          const double c = ((sm.colW[0][s] + sm.colW[1][s]) + sm.colW[2][s]) + sm.colW[3][s];
-          if (c > 0.0) fp_add(A.gacc + 3 * static_cast<size_t>(sm.tJ[s]), c);
-        }
+        pend = cnt;  // summed after the next tile barrier (one barrier less per tile)
       }
     }
     __syncthreads();
+    if (PHASE == 2) {
+      fused_flush_cols(sm, A, pend);
+      pend = 0;
+    }
   }
 }
 
@@ -1106,7 +1159,7 @@ __device__ __noinline__ void warp_exact_atom(const FusedArgs& A, double x0, doub
           const double ex = reference_exponent(A.psi[j], d2, A.eps, y.w);
           if (pass == 0) acc = fmax(acc, ex);
           else if (pass == 1) acc += exp(ex - mx);
-          else fp_add(A.gacc + 3 * static_cast<size_t>(j), exp(ex - mx) * (m / sum));
+          else fp_red(A.gacc + kLimbs * static_cast<size_t>(j), exp(ex - mx) * (m / sum));
         }
       }
     if (pass == 0) mx = warp_max(acc);
@@ -1388,10 +1441,10 @@ __device__ __forceinline__ float butterfly16f(float (&v)[16]) {
 }
 
 // Next tile's raw target data (each thread its entries tid + u kT).
-__device__ __forceinline__ void fused_prefetch32(Fused32Smem& sm, const FusedArgs& A, int base,
-                                                 int cnt) {
+__device__ __forceinline__ void fused_prefetch32(Fused32Smem& sm, const FusedArgs& A,
+                                                 const TileMap& m, int tk, int cnt) {
   for (int t = threadIdx.x; t < cnt; t += kT) {
-    const int s = base + t;
+    const int s = tile_pos(m, tk, t);
     const int r = find_row(sm.rowPref, s);
     const int k = sm.rowStart[r] + (s - sm.rowPref[r]);
     sm.rawK[t] = k;
@@ -1406,9 +1459,18 @@ __device__ __forceinline__ void fused_prefetch32(Fused32Smem& sm, const FusedArg
 // Stages the landed tile: its b2 maximum is reduced first (phase 1 raises
 // the CTA shift and rescales the sums), then the staged exponent offsets are
 // written relative to the updated shift.  Two barriers per tile.
+// Phase 2 column sums of the last computed tile (see fused_flush_cols).
+__device__ __forceinline__ void fused_flush_cols32(const Fused32Smem& sm, const FusedArgs& A, int cnt) {
+  for (int s = threadIdx.x; s < cnt; s += kT) {
+    const double c = ((static_cast<double>(sm.colW[0][s]) + sm.colW[1][s]) + sm.colW[2][s]) +
+                     sm.colW[3][s];
+    if (c > 0.0) fp_red(A.gacc + kLimbs * static_cast<size_t>(sm.tJ[s]), c);
+  }
+}
+
 template <int PHASE>
 __device__ __forceinline__ void fused_stage32(Fused32Smem& sm, const FusedArgs& A, int cnt,
-                                              double& Bc, Atoms32& at) {
+                                              double& Bc, Atoms32& at, int& pend) {
   cp_async_wait_all();
   if (PHASE == 1) {
     float mx = -INFINITY;
@@ -1417,6 +1479,10 @@ __device__ __forceinline__ void fused_stage32(Fused32Smem& sm, const FusedArgs& 
     if ((threadIdx.x & 31) == 0) sm.wmax[threadIdx.x >> 5] = mx;
   }
   __syncthreads();  // previous tile fully consumed; wmax visible
+  if (PHASE == 2) {  // its column sums, before its entries are overwritten
+    fused_flush_cols32(sm, A, pend);
+    pend = 0;
+  }
   if (PHASE == 1) {
     // CTA-uniform running shift (same value in every thread)
     const float tm = fmaxf(fmaxf(sm.wmax[0], sm.wmax[1]), fmaxf(sm.wmax[2], sm.wmax[3]));
@@ -1543,6 +1609,7 @@ __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox&
   // bandmask bit i: phase 1 met a pair in the FP32 error band in this warp's
   // tile i; phase 2 re-tests only those tiles (same tiles, same lists)
   int tix = 0;
+  int pend = 0;  // phase 2: entries of the previous tile with pending column sums
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   ListT* const list = sm.wlist[warp];
   Step32 K = make_step(at.lo_thr, at.hi_thr);
@@ -1560,17 +1627,14 @@ __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox&
     sm.rowPref[threadIdx.x] = pre;
     if (threadIdx.x == 0) sm.rowPref[kT] = total;
     __syncthreads();  // the prefetch reads every thread's row range
-    int tile = kTileT32, start = 0, step = kTileT32;  // (split: as fused_scan)
-    if (KS > 1) {
-      tile = min(kTileT32, max(32, (total + 4 * KS - 1) / (4 * KS)));
-      start = split * tile;
-      step = KS * tile;
-    }
-    if (start < total) fused_prefetch32(sm, A, start, min(tile, total - start));
-    for (int base = start; base < total; base += step) {
-      const int cnt = min(tile, total - base);
-      fused_stage32<PHASE>(sm, A, cnt, Bc, at);
-      if (base + step < total) fused_prefetch32(sm, A, base + step, min(tile, total - base - step));
+    int tile = kTileT32;  // (split: as fused_scan)
+    if (KS > 1) tile = min(kTileT32, max(32, (total + 4 * KS - 1) / (4 * KS))) & ~(kGroup - 1);
+    const TileMap tm = tile_map(total, tile, false);
+    if (split < tm.ntile) fused_prefetch32(sm, A, tm, split, tile_count(tm, split));
+    for (int tk = split; tk < tm.ntile; tk += KS) {
+      const int cnt = tile_count(tm, tk);
+      fused_stage32<PHASE>(sm, A, cnt, Bc, at, pend);
+      if (tk + KS < tm.ntile) fused_prefetch32(sm, A, tm, tk + KS, tile_count(tm, tk + KS));
       const int nsel = fused_cull<Fused32Smem, 4>(sm, cnt, wb, cull_thr, list);
       if (PHASE == 1) {
         float2 acc = make_float2(0.f, 0.f), cn = make_float2(0.f, 0.f);
@@ -1596,16 +1660,15 @@ __device__ void fused_scan32(Fused32Smem& sm, const FusedArgs& A, const WarpBox&
           for (; b0 + 16 <= nsel; b0 += 16) batch32<true, DEBUG, false>(sm, A, at, K, list, b0, nsel, col);
           if (b0 < nsel) batch32<false, DEBUG, false>(sm, A, at, K, list, b0, nsel, col);
         }
-        __syncthreads();
-        for (int s = threadIdx.x; s < cnt; s += kT) {
-          const double c = ((static_cast<double>(sm.colW[0][s]) + sm.colW[1][s]) + sm.colW[2][s]) +
-                           sm.colW[3][s];
-          if (c > 0.0) fp_add(A.gacc + 3 * static_cast<size_t>(sm.tJ[s]), c);
-        }
+        pend = cnt;  // summed after the next tile barrier
       }
       ++tix;
     }
     __syncthreads();
+    if (PHASE == 2) {
+      fused_flush_cols32(sm, A, pend);
+      pend = 0;
+    }
   }
 }
 
@@ -1876,7 +1939,7 @@ __global__ void chunk_order_keys(const unsigned long long* __restrict__ cost,
 __global__ void trunc_assemble_fp(const unsigned long long* __restrict__ gacc, int n,
                                   double* __restrict__ res) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n) res[j] = fp_to_double(gacc + 3 * static_cast<size_t>(j));
+  if (j < n) res[j] = fp_limbs_to_double(gacc + kLimbs * static_cast<size_t>(j));
 }
 
 __global__ void set_visited(double* __restrict__ res, int n, double nq) {
@@ -2369,7 +2432,7 @@ static int ensure_trunc_ws(TruncWorkspace& ws, int nq, int n, std::string& err) 
   if (static_cast<size_t>(n) > ws.tgt_cap || !ws.b2s) {
     const size_t c = std::max<size_t>(n, 1);
     TCK(realloc_exact(ws.b2s, c));
-    TCK(realloc_exact(ws.empty_fp, 3 * c));
+    TCK(realloc_exact(ws.empty_fp, kLimbs * c));
     ws.tgt_cap = c;
   }
   if (!ws.red) TCK(cudaMalloc(&ws.red, sizeof(double) * 4096));
@@ -2429,7 +2492,7 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
   const double c2 = kLog2e / (2.0 * eps);
 
   TCK(cudaMemsetAsync(b.scal + kSlotFlagCount, 0, sizeof(double), s));
-  TCK(cudaMemsetAsync(ws.empty_fp, 0, sizeof(unsigned long long) * 3 * static_cast<size_t>(n), s));
+  TCK(cudaMemsetAsync(ws.empty_fp, 0, sizeof(unsigned long long) * kLimbs * static_cast<size_t>(n), s));
   (note_launch(), gather_d_kernel<<<(n + 255) / 256, 256, 0, s>>>(b.b2, tc.perm_c, n, ws.b2s));
   if (nq > 0) {
     FusedArgs A;

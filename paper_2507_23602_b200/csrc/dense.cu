@@ -130,7 +130,7 @@ dense_passA(const double4* __restrict__ atoms, int nq,
             double* __restrict__ partS, double* __restrict__ shiftA, double3 tlo, double3 thi) {
   __shared__ double4 tile[kTile];
   __shared__ double4 tile2[kTile];
-  __shared__ int2 tbl[kExpTab];
+  __shared__ int2 tbl[ExpTab64::kTab];
   __shared__ double sh[200];
   load_exp2_table(tbl);
 
@@ -331,7 +331,7 @@ dense_passB(const double4* __restrict__ atoms, const double* __restrict__ atomLa
             double* __restrict__ partG) {
   __shared__ double4 tile[kTile];
   __shared__ double4 tile2[kTile];
-  __shared__ int2 tbl[kExpTab];
+  __shared__ int2 tbl[ExpTab64::kTab];
   __shared__ double sh[200];
   load_exp2_table(tbl);
 

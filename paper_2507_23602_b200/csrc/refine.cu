@@ -38,7 +38,7 @@ refine_phase1(const double4* __restrict__ atoms, int nq, const double4* __restri
               double* __restrict__ shiftA) {
   __shared__ double4 tD[kRTile];
   __shared__ float4 tF[kRTile];
-  __shared__ int2 tbl[kExpTab];
+  __shared__ int2 tbl[ExpTab64::kTab];
   __shared__ double sh[200];
   load_exp2_table(tbl);
   const int q = blockIdx.x * kRT + threadIdx.x;

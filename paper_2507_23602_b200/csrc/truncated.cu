@@ -525,9 +525,12 @@ __global__ void trunc_nearest_empty(const double4* __restrict__ xs, int nq,
 constexpr int kFA = 2 * kT;  // atoms per CTA
 
 struct FusedSmem {
-  double4 tD[kTileT];                  // {y0', y1', y2', w_j}
+  // 16-byte strided arrays: the culled lists hold byte offsets t << 4, so
+  // the step's shared loads need no address arithmetic
+  double2 tDa[kTileT];                 // {y0', y1'}
+  double2 tDb[kTileT];                 // {y2', w_j}
   float4 tN0[kTileT];                  // {-y0', -y0', -y1', -y1'}  (FP32x2 pairs)
-  float2 tN1[kTileT];                  // {-y2', -y2'}
+  float4 tN1[kTileT];                  // {-y2', -y2', 0, 0}
   int tK[kTileT];                      // cell-order target position
   int tJ[kTileT];                      // original target index
   int rowStart[kT];
@@ -539,7 +542,7 @@ struct FusedSmem {
   int rawJ[kTileT];
   int rawK[kTileT];
   Region R;                            // CTA-uniform scan region (kept out of registers)
-  int2 tbl[kExpTab];
+  int2 tbl[ExpTab512::kTab];
   double sh[200];
   int shi[40];
 };
@@ -610,30 +613,24 @@ template <bool CLAMP>
 __device__ __forceinline__ double exp2_pair_weighted(double sa, double sb, double wa, double wb,
                                                      const int2* __restrict__ tbl, bool ta,
                                                      bool tb) {
-  const double kka = __dadd_rn(sa, kExpMagic);
-  const double kkb = __dadd_rn(sb, kExpMagic);
+  const double kka = __dadd_rn(sa, ExpTab512::kMagic);
+  const double kkb = __dadd_rn(sb, ExpTab512::kMagic);
   int na = __double2loint(kka);
   int nb = __double2loint(kkb);
   if (CLAMP) {
-    na = min(max(na, kExpNMin), kExpNMax);
-    nb = min(max(nb, kExpNMin), kExpNMax);
+    na = min(max(na, ExpTab512::kNMin), ExpTab512::kNMax);
+    nb = min(max(nb, ExpTab512::kNMin), ExpTab512::kNMax);
   }
-  const double ra = __dadd_rn(sa, -__dadd_rn(kka, -kExpMagic));
-  const double rb = __dadd_rn(sb, -__dadd_rn(kkb, -kExpMagic));
-  double qa = fma(kP4, ra, kP3);
-  double qb = fma(kP4, rb, kP3);
-  qa = fma(qa, ra, kP2);
-  qb = fma(qb, rb, kP2);
-  qa = fma(qa, ra, kP1);
-  qb = fma(qb, rb, kP1);
-  qa = fma(qa, ra, kP0);
-  qb = fma(qb, rb, kP0);
-  na = ta ? na : kExpZeroN;  // scale word pattern 0 -> +0.0
-  nb = tb ? nb : kExpZeroN;
-  const int2 Ta = tbl[na & (kExpTab - 1)];
-  const int2 Tb = tbl[nb & (kExpTab - 1)];
-  const double sca = __hiloint2double(Ta.y + na * kExpUnit, Ta.x) * wa;
-  const double scb = __hiloint2double(Tb.y + nb * kExpUnit, Tb.x) * wb;
+  const double ra = __dadd_rn(sa, -__dadd_rn(kka, -ExpTab512::kMagic));
+  const double rb = __dadd_rn(sb, -__dadd_rn(kkb, -ExpTab512::kMagic));
+  const double qa = ExpTab512::poly(ra);
+  const double qb = ExpTab512::poly(rb);
+  na = ta ? na : ExpTab512::kZeroN;  // scale word pattern 0 -> +0.0
+  nb = tb ? nb : ExpTab512::kZeroN;
+  const int2 Ta = tbl[na & (ExpTab512::kTab - 1)];
+  const int2 Tb = tbl[nb & (ExpTab512::kTab - 1)];
+  const double sca = __hiloint2double(Ta.y + na * ExpTab512::kUnit, Ta.x) * wa;
+  const double scb = __hiloint2double(Tb.y + nb * ExpTab512::kUnit, Tb.x) * wb;
   return fma(qa, sca, qb * scb);
 }
 
@@ -699,11 +696,12 @@ __device__ __forceinline__ void fused_convert(FusedSmem& sm, const FusedArgs& A,
     const double y0 = y.x - o0, y1 = y.y - o1, y2 = y.z - o2;
     const double yy = fma(y2, y2, fma(y1, y1, y0 * y0));
     const double w = fmax(fma(-A.c2, yy, sm.rawB2[t]) - B, -1.0e5);
-    sm.tD[t] = make_double4(y0, y1, y2, w);
+    sm.tDa[t] = make_double2(y0, y1);
+    sm.tDb[t] = make_double2(y2, w);
     const float f0 = -static_cast<float>(y0), f1 = -static_cast<float>(y1),
                 f2 = -static_cast<float>(y2);
     sm.tN0[t] = make_float4(f0, f0, f1, f1);
-    sm.tN1[t] = make_float2(f2, f2);
+    sm.tN1[t] = make_float4(f2, f2, 0.f, 0.f);
     sm.tJ[t] = sm.rawJ[t];
     sm.tK[t] = sm.rawK[t];
   }
@@ -724,7 +722,7 @@ __device__ __forceinline__ void fused_flush_cols(const FusedSmem& sm, const Fuse
 // warp box is still inside lo (conservatively: far^2 < full_thr) are in for
 // every atom of the warp, with no per-pair test; they go to the back of the
 // list (list[cap - 1 - i], i < *nfull), the others to the front.
-template <class SM>
+template <class SM, int SHIFT = 4>
 __device__ __forceinline__ int fused_cull2(const SM& sm, int cnt, const WarpBox& w, float thr,
                                            float full_thr, ListT* __restrict__ list, int cap,
                                            int* nfull) {
@@ -749,8 +747,8 @@ __device__ __forceinline__ int fused_cull2(const SM& sm, int cnt, const WarpBox&
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);
     const unsigned mf = __ballot_sync(0xffffffffu, full);
-    if (keep) list[nsel + __popc(m & lt)] = static_cast<ListT>(t);
-    if (full) list[cap - 1 - (nf + __popc(mf & lt))] = static_cast<ListT>(t);
+    if (keep) list[nsel + __popc(m & lt)] = static_cast<ListT>(t << SHIFT);
+    if (full) list[cap - 1 - (nf + __popc(mf & lt))] = static_cast<ListT>(t << SHIFT);
     nsel += __popc(m);
     nf += __popc(mf);
   }
@@ -786,14 +784,21 @@ __device__ __forceinline__ int fused_cull(const SM& sm, int cnt, const WarpBox& 
   return nsel;
 }
 
-// Packed FP32x2 squared distances of item t to the thread's atoms (a, b).
+// Element at byte offset o of a 16-byte strided staged array.
+template <class T>
+__device__ __forceinline__ const T& at16(const T* arr, int o) {
+  return *reinterpret_cast<const T*>(reinterpret_cast<const char*>(arr) + o);
+}
+
+// Packed FP32x2 squared distances of the item at byte offset o (t << 4) to
+// the thread's atoms (a, b).
 template <class SM, class AT>
-__device__ __forceinline__ float2 fused_d2(const SM& sm, const AT& at, int t) {
-  const float4 n01 = sm.tN0[t];
-  const float2 n2 = sm.tN1[t];
+__device__ __forceinline__ float2 fused_d2(const SM& sm, const AT& at, int o) {
+  const float4 n01 = at16(sm.tN0, o);
+  const float4 n2 = at16(sm.tN1, o);
   const float2 dx = __fadd2_rn(at.F0, make_float2(n01.x, n01.y));
   const float2 dy = __fadd2_rn(at.F1, make_float2(n01.z, n01.w));
-  const float2 dz = __fadd2_rn(at.F2, n2);
+  const float2 dz = __fadd2_rn(at.F2, make_float2(n2.x, n2.y));
   float2 d2 = __fmul2_rn(dx, dx);
   d2 = __ffma2_rn(dy, dy, d2);
   return __ffma2_rn(dz, dz, d2);
@@ -906,7 +911,8 @@ __device__ __forceinline__ double2 exp_part64(const FusedSmem& sm, FusedAtoms& a
                                               bool k1b, float2& cnt) {
   double2 out = make_double2(0.0, 0.0);
   {
-    const double4 y0 = sm.tD[t0];
+    const double2 y0a = at16(sm.tDa, t0), y0b = at16(sm.tDb, t0);
+    const double4 y0 = make_double4(y0a.x, y0a.y, y0b.x, y0b.y);
     double sa0 = chain3(at.Xa, y0), sb0 = chain3(at.Xb, y0);
     if (wide) {
       sa0 -= at.xsqa;
@@ -914,13 +920,14 @@ __device__ __forceinline__ double2 exp_part64(const FusedSmem& sm, FusedAtoms& a
     }
     if (PHASE == 1) {
       cnt = __fadd2_rn(cnt, make_float2(k0a ? 1.f : 0.f, k0b ? 1.f : 0.f));
-      at.Sa = exp2_acc_masked<SAFE>(sa0, at.Sa, sm.tbl, k0a);
-      at.Sb = exp2_acc_masked<SAFE>(sb0, at.Sb, sm.tbl, k0b);
+      at.Sa = exp2_acc_masked<SAFE, ExpTab512>(sa0, at.Sa, sm.tbl, k0a);
+      at.Sb = exp2_acc_masked<SAFE, ExpTab512>(sb0, at.Sb, sm.tbl, k0b);
     } else {
       out.x = exp2_pair_weighted<SAFE>(sa0, sb0, at.wa, at.wb, sm.tbl, k0a, k0b);
     }
     if (PAIR) {
-      const double4 y1 = sm.tD[t1];
+      const double2 y1a = at16(sm.tDa, t1), y1b = at16(sm.tDb, t1);
+      const double4 y1 = make_double4(y1a.x, y1a.y, y1b.x, y1b.y);
       double sa1 = chain3(at.Xa, y1), sb1 = chain3(at.Xb, y1);
       if (wide) {
         sa1 -= at.xsqa;
@@ -928,8 +935,8 @@ __device__ __forceinline__ double2 exp_part64(const FusedSmem& sm, FusedAtoms& a
       }
       if (PHASE == 1) {
         cnt = __fadd2_rn(cnt, make_float2(k1a ? 1.f : 0.f, k1b ? 1.f : 0.f));
-        at.Sa = exp2_acc_masked<SAFE>(sa1, at.Sa, sm.tbl, k1a);
-        at.Sb = exp2_acc_masked<SAFE>(sb1, at.Sb, sm.tbl, k1b);
+        at.Sa = exp2_acc_masked<SAFE, ExpTab512>(sa1, at.Sa, sm.tbl, k1a);
+        at.Sb = exp2_acc_masked<SAFE, ExpTab512>(sb1, at.Sb, sm.tbl, k1b);
       } else {
         out.y = exp2_pair_weighted<SAFE>(sa1, sb1, at.wa, at.wb, sm.tbl, k1a, k1b);
       }
@@ -944,28 +951,25 @@ __device__ __forceinline__ double2 step64d(const FusedSmem& sm, const FusedArgs&
                                            float2 d1, float2& cnt, bool& hit) {
   // culled steps always hold accepted pairs (no all-out steps in practice):
   // no vote on the work, masked pairs contribute +0
-  bool k0a, k0b, k1a = false, k1b = false;
   if (DEBUG || (CHECK && __any_sync(0xffffffffu, step_in_band<PAIR>(K, d0, d1)))) {
     hit = true;
-    const unsigned in = slow_mask(sm, A, at.qa, at.qb, K, t0, t1, d0, d1, PAIR);
-    k0a = in & 1u;
-    k0b = in & 2u;
-    k1a = in & 4u;
-    k1b = in & 8u;
+    const unsigned in = slow_mask(sm, A, at.qa, at.qb, K, t0 >> 4, t1 >> 4, d0, d1, PAIR);
     if (DEBUG && PHASE == 1) {
-      if (k0a) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
-      if (k1a) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
-      if (k0b) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0]));
-      if (k1b) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1]));
+      if (in & 1u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0 >> 4]));
+      if (in & 4u) at.ha += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1 >> 4]));
+      if (in & 2u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t0 >> 4]));
+      if (in & 8u) at.hb += candidate_hash_term(static_cast<uint64_t>(sm.tJ[t1 >> 4]));
     }
-  } else {
-    k0a = d0.x < K.lo;
-    k0b = d0.y < K.lo;
-    if (PAIR) {
-      k1a = d1.x < K.lo;
-      k1b = d1.y < K.lo;
-    }
+    // the exact decisions, re-expressed as distances on either side of lo:
+    // both paths meet in the FP32 registers and the predicates below come
+    // straight from FSETP (merging bool masks materialised them as bytes)
+    d0.x = (in & 1u) ? -INFINITY : INFINITY;
+    d0.y = (in & 2u) ? -INFINITY : INFINITY;
+    d1.x = (in & 4u) ? -INFINITY : INFINITY;
+    d1.y = (in & 8u) ? -INFINITY : INFINITY;
   }
+  const bool k0a = d0.x < K.lo, k0b = d0.y < K.lo;
+  const bool k1a = PAIR && d1.x < K.lo, k1b = PAIR && d1.y < K.lo;
   return exp_part64<PHASE, PAIR, SAFE>(sm, at, wide, t0, t1, k0a, k0b, k1a, k1b, cnt);
 }
 
@@ -1001,7 +1005,7 @@ __device__ __forceinline__ void batch64(const FusedSmem& sm, const FusedArgs& A,
   }
   const double tot = butterfly16(v);
   const int item = b0 + (lane >> 1);
-  if (!(lane & 1) && item < nsel) col[list[item]] = tot;
+  if (!(lane & 1) && item < nsel) col[list[item] >> 4] = tot;
 }
 
 // Phase-2 batch over full-in items (every pair of valid atoms taken).
@@ -1027,7 +1031,7 @@ __device__ __forceinline__ void batch64_full(const FusedSmem& sm, FusedAtoms& at
   }
   const double tot = butterfly16(v);
   const int item = b0 + (lane >> 1);
-  if (!(lane & 1) && item < nfull) col[full[-item]] = tot;
+  if (!(lane & 1) && item < nfull) col[full[-item] >> 4] = tot;
 }
 
 // KS > 1: this CTA is split `split` of KS sharing one chunk (heavy chunks,
@@ -1235,7 +1239,7 @@ static_assert(sizeof(SplitXchg) <= sizeof(double) * (kT / 32) * kTileT, "exchang
 // CTA of the cluster holds the same S_q and the result is deterministic).
 template <bool DEBUG, int KS>
 __device__ __forceinline__ void fused_body(FusedSmem& sm, const FusedArgs& A, int chunk, int split) {
-  load_exp2_table(sm.tbl);
+  load_exp2_table<ExpTab512>(sm.tbl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   FusedAtoms at;
   at.qa = chunk * kFA + warp * 64 + lane;

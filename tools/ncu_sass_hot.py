@@ -57,3 +57,20 @@ print("\nhottest instructions:")
 for a, t, s, st, ex in sorted(ins, key=lambda x: -x[2])[:40]:
     top = ", ".join(f"{k[6:]} {v}" for k, v in Counter(st).most_common(2))
     print(f"  {a-base:#07x} {t[:60]:60s} {s/tot:6.2%}  {top}")
+
+# instructions executed per innermost loop (each instruction assigned to the
+# shortest loop containing it; the rest is "straight-line")
+owner = [None] * len(ins)
+for s0, s1 in sorted(loops, key=lambda x: x[1] - x[0], reverse=True):
+    for k in range(s0, s1 + 1):
+        owner[k] = (s0, s1)
+by = Counter()
+smp = Counter()
+for k, i in enumerate(ins):
+    by[owner[k]] += i[4]
+    smp[owner[k]] += i[2]
+allx = sum(i[4] for i in ins)
+print("\ninstructions executed by innermost loop:")
+for o, v in by.most_common(16):
+    lab = "straight" if o is None else f"{ins[o[0]][0]-base:#07x}-{ins[o[1]][0]-base:#07x} ({o[1]-o[0]+1} instr)"
+    print(f"  {lab:32s} {v:.3e} {v/allx:6.1%}  samples {smp[o]/tot:6.1%}")

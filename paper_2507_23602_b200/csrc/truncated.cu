@@ -498,7 +498,7 @@ __global__ void trunc_nearest_empty(const double4* __restrict__ xs, int nq,
         atomL[qq] = L;
         atomJ[qq] = eps * L * a.w;
         atomD[qq] = a.w * exp(-L);
-        fp_red(empty_fp + kLimbs * static_cast<size_t>(bj), a.w);
+        fp_red(empty_fp + kLimbs * static_cast<size_t>(bk), a.w);
         if (DEBUG) hash_out[qq] = candidate_hash_term(static_cast<uint64_t>(bj));
       }
     }
@@ -567,7 +567,7 @@ struct FusedArgs {
   const double* scal; const double* psi;
   double c2, r2, r_scan, eps;
   double* atomJ; double* atomD; double* cntd; double* emptyd;
-  unsigned long long* gacc;              // [kLimbs N] fixed point (fp_red), original index
+  unsigned long long* gacc;              // [kLimbs N] fixed point (fp_red), cell-order index
   uint32_t* dbg_cnt; uint64_t* dbg_hash; double* dbg_logs;  // Hilbert order
   uint32_t* cnt_out;                     // 0 = empty candidate set (Hilbert order)
   const int* chunk_order;                // CTA -> atom chunk (heaviest first) or null
@@ -714,7 +714,7 @@ __device__ __forceinline__ void fused_convert(FusedSmem& sm, const FusedArgs& A,
 __device__ __forceinline__ void fused_flush_cols(const FusedSmem& sm, const FusedArgs& A, int cnt) {
   for (int s = threadIdx.x; s < cnt; s += kT) {
     const double c = ((sm.colW[0][s] + sm.colW[1][s]) + sm.colW[2][s]) + sm.colW[3][s];
-    if (c > 0.0) fp_red(A.gacc + kLimbs * static_cast<size_t>(sm.tJ[s]), c);
+    if (c > 0.0) fp_red(A.gacc + kLimbs * static_cast<size_t>(sm.tK[s]), c);
   }
 }
 
@@ -1163,7 +1163,7 @@ __device__ __noinline__ void warp_exact_atom(const FusedArgs& A, double x0, doub
           const double ex = reference_exponent(A.psi[j], d2, A.eps, y.w);
           if (pass == 0) acc = fmax(acc, ex);
           else if (pass == 1) acc += exp(ex - mx);
-          else fp_red(A.gacc + kLimbs * static_cast<size_t>(j), exp(ex - mx) * (m / sum));
+          else fp_red(A.gacc + kLimbs * static_cast<size_t>(k), exp(ex - mx) * (m / sum));
         }
       }
     if (pass == 0) mx = warp_max(acc);
@@ -1468,7 +1468,7 @@ __device__ __forceinline__ void fused_flush_cols32(const Fused32Smem& sm, const 
   for (int s = threadIdx.x; s < cnt; s += kT) {
     const double c = ((static_cast<double>(sm.colW[0][s]) + sm.colW[1][s]) + sm.colW[2][s]) +
                      sm.colW[3][s];
-    if (c > 0.0) fp_red(A.gacc + kLimbs * static_cast<size_t>(sm.tJ[s]), c);
+    if (c > 0.0) fp_red(A.gacc + kLimbs * static_cast<size_t>(sm.tK[s]), c);
   }
 }
 
@@ -1934,16 +1934,24 @@ __global__ void chunk_order_keys(const unsigned long long* __restrict__ cost,
   if (c >= nblk) return;
   const unsigned char r = role[c];
   const uint32_t cls = r == kRoleSplit ? 0u : r == kRoleMine ? 1u : 2u;
+  // quarter-octave cost buckets, Hilbert order inside a bucket: the heavy
+  // chunks still lead, while chunks of similar cost (all of them on a
+  // uniform instance) keep their spatial order, so concurrently resident
+  // CTAs share staged target rows in L2 (a fine-grained cost sort scattered
+  // them: cfg5 DRAM traffic 1.4 -> 5.5 GB per evaluation)
   const uint32_t bucket =
-      0xFFFFu - min(0xFFFFu, static_cast<uint32_t>(log2(static_cast<double>(cost[c]) + 1.0) * 1024.0));
+      0xFFFFu - min(0xFFFFu, static_cast<uint32_t>(log2(static_cast<double>(cost[c]) + 1.0) * 4.0));
   keys[c] = (static_cast<uint64_t>((cls << 16) | bucket) << 32) | static_cast<uint32_t>(c);
   idx[c] = c;
 }
 
-__global__ void trunc_assemble_fp(const unsigned long long* __restrict__ gacc, int n,
-                                  double* __restrict__ res) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n) res[j] = fp_limbs_to_double(gacc + kLimbs * static_cast<size_t>(j));
+// The accumulator is indexed by cell-order position k (a CTA's reductions
+// land in the few contiguous runs of its scanned rows: L2-friendly), the
+// result by original target index tperm[k].
+__global__ void trunc_assemble_fp(const unsigned long long* __restrict__ gacc,
+                                  const int* __restrict__ tperm, int n, double* __restrict__ res) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) res[tperm[k]] = fp_limbs_to_double(gacc + kLimbs * static_cast<size_t>(k));
 }
 
 __global__ void set_visited(double* __restrict__ res, int n, double nq) {
@@ -2603,7 +2611,7 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
       cudaEventRecord(b.timing[3], s);
       cudaEventRecord(b.timing[4], s);
     }
-    (note_launch(), trunc_assemble_fp<<<(n + 255) / 256, 256, 0, s>>>(ws.empty_fp, n, b.res));
+    (note_launch(), trunc_assemble_fp<<<(n + 255) / 256, 256, 0, s>>>(ws.empty_fp, tc.perm_c, n, b.res));
     // J, D, pairs, empty in res[n + 0..3] (fixed-order sums of this rank's atoms)
     launch_det_sum4(ws.atomJ, ws.atomD, ws.cntd, ws.emptyd, nq, range, ws.red, b.res + n + kResJ, s);
     if (dbg) {

@@ -10,8 +10,15 @@ import sys
 from collections import Counter
 
 rows = list(csv.reader(open(sys.argv[1])))
-hdr = rows[1]
-data = [r for r in rows[2:] if len(r) == len(hdr)]
+# one section per kernel ("Kernel Name" line, header, rows): take the first
+hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+hdr = rows[hi]
+data = []
+for r in rows[hi + 1:]:
+    if r and r[0] in ("Kernel Name", "Address"):
+        break
+    if len(r) == len(hdr):
+        data.append(r)
 col = {h: i for i, h in enumerate(hdr)}
 stalls = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 ins = []

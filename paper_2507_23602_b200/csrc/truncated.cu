@@ -250,7 +250,7 @@ __device__ __forceinline__ int find_row(const int* pref, int s) {
 // (ncu: 15 % of the cfg5 warp samples at the two per-tile barriers).
 // Groups keep the staging loads coalesced (8 x 32 B of target records).
 // Measured: fp64 cfg5 -2 %, cfg3 unchanged; the fp32 kernel keeps contiguous
-// tiles (+1-3 % there: its shorter steps feel the scattered staging loads).
+// tiles (interleaving is neutral there: +-0.3 %).
 constexpr int kGroup = 8;
 struct TileMap {
   int total, tile, ng, ntile;

@@ -523,6 +523,11 @@ __global__ void trunc_nearest_empty(const double4* __restrict__ xs, int nq,
 // accumulator per target (order independent => deterministic).
 
 constexpr int kFA = 2 * kT;  // atoms per CTA
+// Mask slots: a resident CTA holds one (at most 4 x 148 are resident), kMaskWords
+// words per thread (+1 scratch word); CTAs that need more recompute the masks
+// in phase 2; slot kMaskSlots is the shared scratch of CTAs without a slot.
+constexpr int kMaskSlots = 1024;
+constexpr int kMaskWords = 2048;
 
 struct FusedSmem {
   // 16-byte strided arrays: the culled lists hold byte offsets t << 4, so
@@ -542,6 +547,8 @@ struct FusedSmem {
   int rawJ[kTileT];
   int rawK[kTileT];
   Region R;                            // CTA-uniform scan region (kept out of registers)
+  int mslot;                           // this CTA's mask slot (-1: none)
+  int mok;                             // 1: phase 1 stored every step's pair mask
   int2 tbl[ExpTab512::kTab];
   double sh[200];
   int shi[40];
@@ -574,6 +581,10 @@ struct FusedArgs {
   const unsigned char* role;             // per chunk: kRoleOther / kRoleMine / kRoleSplit, or null
   const int* heavy_count;                // split chunks: chunk_order[0, heavy_count)
   int* queue;                            // trunc_fused_split work counter
+  uint32_t* mbuf;                        // phase-1 pair masks for phase 2 (kMaskSlots slots), or null
+  int* mbusy;                            // per slot: held by a resident CTA
+  unsigned* mticket;                     // slot search start
+  int mslots;                            // 0: no slots (phase 2 recomputes the masks)
 };
 
 // chunk roles (chunk_role)
@@ -945,10 +956,45 @@ __device__ __forceinline__ double2 exp_part64(const FusedSmem& sm, FusedAtoms& a
   return out;
 }
 
+// Pair masks of phase 1, replayed in phase 2 (same tiles, same culled lists,
+// same step order): phase 2 skips the FP32 pre-test, the band vote and the
+// exact band path.  4 bits per step (bit 2i: atom a, 2i+1: atom b of item
+// i), 8 steps per word, each tile's stream padded to a word; thread t's words
+// are p[0], p[kT], ... of its CTA's region (coalesced).  CTAs whose region
+// does not fit recompute the masks in phase 2 (identical results).
+struct MaskIO {
+  uint32_t* base;  // thread's first word (words base[i * kT])
+  int* ok;         // &sm.mok (cleared on overflow)
+  int widx;        // next word
+  int n;           // steps in w (the first in the top bits)
+  uint32_t w;
+};
+__device__ __forceinline__ void mask_store(MaskIO& m) {
+  m.base[static_cast<size_t>(min(m.widx, kMaskWords)) * kT] = m.w;  // (overflow: scratch word)
+  if (m.widx >= kMaskWords) *m.ok = 0;
+  ++m.widx;
+  m.w = 0u;
+  m.n = 0;
+}
+__device__ __forceinline__ void mask_put(MaskIO& m, bool k0a, bool k0b, bool k1a, bool k1b) {
+  const uint32_t b = (k0a ? 1u : 0u) | (k0b ? 2u : 0u) | (k1a ? 4u : 0u) | (k1b ? 8u : 0u);
+  m.w = (m.w << 4) | b;
+  if (++m.n == 8) mask_store(m);
+}
+__device__ __forceinline__ void mask_flush(MaskIO& m) {
+  if (m.n) {
+    m.w <<= 4 * (8 - m.n);
+    mask_store(m);
+  }
+}
+// Bits of step p (0..7) of a word.
+__device__ __forceinline__ uint32_t mask_bits(uint32_t w, int p) { return w >> (28 - 4 * p); }
+
 template <int PHASE, bool PAIR, bool SAFE, bool DEBUG, bool CHECK = true>
 __device__ __forceinline__ double2 step64d(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at,
                                            const Step32& K, bool wide, int t0, int t1, float2 d0,
-                                           float2 d1, float2& cnt, bool& hit) {
+                                           float2 d1, float2& cnt, bool& hit,
+                                           MaskIO* mio = nullptr) {
   // culled steps always hold accepted pairs (no all-out steps in practice):
   // no vote on the work, masked pairs contribute +0
   if (DEBUG || (CHECK && __any_sync(0xffffffffu, step_in_band<PAIR>(K, d0, d1)))) {
@@ -970,16 +1016,43 @@ __device__ __forceinline__ double2 step64d(const FusedSmem& sm, const FusedArgs&
   }
   const bool k0a = d0.x < K.lo, k0b = d0.y < K.lo;
   const bool k1a = PAIR && d1.x < K.lo, k1b = PAIR && d1.y < K.lo;
+  if (PHASE == 1 && !DEBUG && mio) mask_put(*mio, k0a, k0b, k1a, k1b);  // (mio: compile-time null or not)
   return exp_part64<PHASE, PAIR, SAFE>(sm, at, wide, t0, t1, k0a, k0b, k1a, k1b, cnt);
 }
 
 template <int PHASE, bool PAIR, bool SAFE, bool DEBUG, bool CHECK = true>
 __device__ __forceinline__ double2 step64(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at,
                                           const Step32& K, bool wide, int t0, int t1,
-                                          float2& cnt, bool& hit) {
+                                          float2& cnt, bool& hit, MaskIO* mio = nullptr) {
   const float2 d0 = fused_d2(sm, at, t0);
   const float2 d1 = PAIR ? fused_d2(sm, at, t1) : d0;
-  return step64d<PHASE, PAIR, SAFE, DEBUG, CHECK>(sm, A, at, K, wide, t0, t1, d0, d1, cnt, hit);
+  return step64d<PHASE, PAIR, SAFE, DEBUG, CHECK>(sm, A, at, K, wide, t0, t1, d0, d1, cnt, hit, mio);
+}
+
+// Phase-2 batch replaying the stored masks (word = the batch's 8 steps).
+template <bool SAFE>
+__device__ __forceinline__ void batch64_masked(const FusedSmem& sm, FusedAtoms& at, bool wide,
+                                               const ListT* list, int b0, int nsel, uint32_t mw,
+                                               double* col) {
+  const int lane = threadIdx.x & 31;
+  double v[16];
+  float2 dummy = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int i = b0 + 2 * p;
+    double2 val = make_double2(0.0, 0.0);
+    if (i < nsel) {
+      const int t0 = list[i];
+      const int t1 = i + 1 < nsel ? list[i + 1] : t0;
+      const uint32_t b = mask_bits(mw, p);
+      val = exp_part64<2, true, SAFE>(sm, at, wide, t0, t1, b & 1u, b & 2u, b & 4u, b & 8u, dummy);
+    }
+    v[2 * p] = val.x;
+    v[2 * p + 1] = i + 1 < nsel ? val.y : 0.0;
+  }
+  const double tot = butterfly16(v);
+  const int item = b0 + (lane >> 1);
+  if (!(lane & 1) && item < nsel) col[list[item] >> 4] = tot;
 }
 
 template <bool SAFE, bool DEBUG, bool CHECK>
@@ -1062,6 +1135,20 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
   const int ny = sm.R.c_hi[1] - sm.R.c_lo[1] + 1;
   const int nrows = ny * (sm.R.c_hi[2] - sm.R.c_lo[2] + 1);
   int pend = 0;  // phase 2: entries of the previous tile with pending column sums
+  // stored pair masks (fused_body holds a slot for this CTA; phase 2 replays
+  // them when phase 1 stored every step's)
+  // (phase 1 always stores when the kernel has a mask buffer: CTAs without a
+  // slot write a shared scratch slot, so the step loop has no branch on it)
+  constexpr bool kStore = !DEBUG && KS == 1;
+  const bool mon = kStore && A.mbuf && (PHASE == 1 || (sm.mslot >= 0 && sm.mok));
+  MaskIO mio;
+  mio.base = A.mbuf + static_cast<size_t>(sm.mslot < 0 ? kMaskSlots : sm.mslot) * (kMaskWords + 1) * kT +
+             threadIdx.x;
+  mio.ok = &sm.mok;
+  mio.widx = 0;
+  mio.n = 0;
+  mio.w = 0u;
+  MaskIO* const mp = kStore ? &mio : nullptr;
   for (int rb = 0; rb < nrows; rb += kT) {
     int st = 0, ln = 0;
     if (rb + threadIdx.x < nrows)
@@ -1106,10 +1193,11 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
               d0 = fused_d2(sm, at, t0);
               d1 = fused_d2(sm, at, t1);
             }
-            step64d<1, true, SAFE, DEBUG>(sm, A, at, K, wide, c0, c1, e0, e1, cn, hit);
+            step64d<1, true, SAFE, DEBUG>(sm, A, at, K, wide, c0, c1, e0, e1, cn, hit, mp);
           }
         }
-        if (i < nsel) step64<1, false, SAFE, DEBUG>(sm, A, at, K, wide, list[i], list[i], cn, hit);
+        if (i < nsel) step64<1, false, SAFE, DEBUG>(sm, A, at, K, wide, list[i], list[i], cn, hit, mp);
+        if (kStore) mask_flush(mio);  // each tile's stream starts on a word
         int f = 0;
         for (; f + 1 < nfull; f += 2)
           exp_part64<1, true, SAFE>(sm, at, wide, full[-f], full[-(f + 1)], va, vb, va, vb, cn);
@@ -1123,8 +1211,18 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
         __syncwarp();
         // (a band-free second instantiation, as in fused_scan32, costs more in
         // instruction-cache misses than it saves here: measured +6 %)
-        for (int b0 = 0; b0 < nsel; b0 += 16)
-          batch64<SAFE, DEBUG, true>(sm, A, at, K, wide, list, b0, nsel, col);
+        if (mon) {  // one word per batch of 8 steps (the next one prefetched)
+          uint32_t nw = mio.base[static_cast<size_t>(mio.widx) * kT];
+          for (int b0 = 0; b0 < nsel; b0 += 16) {
+            const uint32_t mw = nw;
+            ++mio.widx;
+            nw = mio.base[static_cast<size_t>(mio.widx) * kT];
+            batch64_masked<SAFE>(sm, at, wide, list, b0, nsel, mw, col);
+          }
+        } else {
+          for (int b0 = 0; b0 < nsel; b0 += 16)
+            batch64<SAFE, DEBUG, true>(sm, A, at, K, wide, list, b0, nsel, col);
+        }
         for (int b0 = 0; b0 < nfull; b0 += 16) batch64_full<SAFE>(sm, at, wide, full, b0, nfull, va, vb, col);
         pend = cnt;  // summed after the next tile barrier (one barrier less per tile)
       }
@@ -1257,7 +1355,24 @@ __device__ __forceinline__ void fused_body(FusedSmem& sm, const FusedArgs& A, in
     hi[2] = fmax(va ? pa.z : -INFINITY, vb ? pb.z : -INFINITY);
     Region R;
     setup_region(A.g, lo, hi, A.r2, A.r_scan, A.c2, sm.sh, R);
-    if (threadIdx.x == 0) sm.R = R;
+    if (threadIdx.x == 0) {
+      sm.R = R;
+      // a mask slot for phase 2 (linear probing from a ticket: more slots
+      // than resident CTAs, so the search always ends)
+      int slot = -1;
+      if (!DEBUG && KS == 1 && A.mbuf && A.mslots) {
+        const unsigned t0 = atomicAdd(A.mticket, 1u);
+        for (unsigned k = 0; k < static_cast<unsigned>(kMaskSlots); ++k) {
+          const int c = static_cast<int>((t0 + k) & (kMaskSlots - 1));
+          if (atomicCAS(A.mbusy + c, 0, 1) == 0) {
+            slot = c;
+            break;
+          }
+        }
+      }
+      sm.mslot = slot;
+      sm.mok = slot >= 0 ? 1 : 0;
+    }
     __syncthreads();
   }
   const double o0 = sm.R.o[0], o1 = sm.R.o[1], o2 = sm.R.o[2];
@@ -1330,6 +1445,13 @@ __device__ __forceinline__ void fused_body(FusedSmem& sm, const FusedArgs& A, in
     fused_scan<2, true, DEBUG, KS>(sm, A, wb, cull_thr, B, at, split);
   else
     fused_scan<2, false, DEBUG, KS>(sm, A, wb, cull_thr, B, at, split);
+  if (!DEBUG && KS == 1 && A.mbuf) {
+    __syncthreads();  // every thread is done with the slot
+    if (threadIdx.x == 0 && sm.mslot >= 0) {
+      __threadfence();
+      atomicExch(A.mbusy + sm.mslot, 0);
+    }
+  }
 }
 
 template <bool DEBUG>
@@ -2377,7 +2499,7 @@ void PointOrders::release() {
 void TruncWorkspace::release() {
   void* ptrs[] = {cub_tmp, keys, keys2, idx, idx2, b2s, S, atomL, atomJ, atomD, cntd, emptyd, cnt,
                   hash, empty_fp, pts, near_out, red, chunk_cost, heavy_flag,
-                  chunk_w, chunk_pre, part_range};
+                  chunk_w, chunk_pre, part_range, mbuf, mbusy, mticket};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (fork_ev) cudaEventDestroy(fork_ev);
@@ -2520,6 +2642,19 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
     A.role = nullptr;
     A.heavy_count = ws.part_range + 3;
     A.queue = ws.part_range + 4;
+    // phase-1 pair masks replayed by phase 2 (fp64 kernel; RSOT_CUDA_PAIR_MASKS=0: off)
+    A.mbuf = nullptr; A.mbusy = nullptr; A.mticket = nullptr; A.mslots = 0;
+    if (!fp32 && !dbg) {
+      if (!ws.mbuf) {
+        TCK(cudaMalloc(&ws.mbuf, sizeof(uint32_t) * (static_cast<size_t>(kMaskSlots) + 1) * (kMaskWords + 1) * kT));
+        TCK(cudaMalloc(&ws.mbusy, sizeof(int) * kMaskSlots));
+        TCK(cudaMalloc(&ws.mticket, sizeof(unsigned)));
+        TCK(cudaMemsetAsync(ws.mbusy, 0, sizeof(int) * kMaskSlots, s));
+        TCK(cudaMemsetAsync(ws.mticket, 0, sizeof(unsigned), s));
+      }
+      A.mbuf = ws.mbuf; A.mbusy = ws.mbusy; A.mticket = ws.mticket;
+      A.mslots = env_double("RSOT_CUDA_PAIR_MASKS", 1.0) != 0.0 ? 1 : 0;  // 0: phase 2 recomputes
+    }
     // Scan costs of the chunks -> roles (partitioned atoms: this rank's
     // work-balanced range; heavy chunks run split across a CTA cluster) and a
     // heaviest-first schedule.  RSOT_CUDA_SPLIT_ALPHA / RSOT_CUDA_SPLIT_FLOOR

@@ -90,6 +90,9 @@ struct TruncWorkspace {
   int* part_range = nullptr;                  // [5]: this rank's atoms [lo, hi), atom count, split count, queue
   int split_clusters = 0, split_clusters32 = 0;  // resident clusters of trunc_fused(32)_split
   cudaStream_t side = nullptr; cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  // phase-1 pair masks replayed by phase 2 (trunc_fused): slots held by
+  // resident CTAs, busy flags, slot-search ticket
+  uint32_t* mbuf = nullptr; int* mbusy = nullptr; unsigned* mticket = nullptr;
   void release();
 };
 

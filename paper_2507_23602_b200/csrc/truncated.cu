@@ -585,6 +585,7 @@ struct FusedArgs {
   int* mbusy;                            // per slot: held by a resident CTA
   unsigned* mticket;                     // slot search start
   int mslots;                            // 0: no slots (phase 2 recomputes the masks)
+  int mwords;                            // words per thread a slot may hold (<= kMaskWords)
 };
 
 // chunk roles (chunk_role)
@@ -965,13 +966,14 @@ __device__ __forceinline__ double2 exp_part64(const FusedSmem& sm, FusedAtoms& a
 struct MaskIO {
   uint32_t* base;  // thread's first word (words base[i * kT])
   int* ok;         // &sm.mok (cleared on overflow)
+  int cap;         // words this thread may store
   int widx;        // next word
   int n;           // steps in w (the first in the top bits)
   uint32_t w;
 };
 __device__ __forceinline__ void mask_store(MaskIO& m) {
-  m.base[static_cast<size_t>(min(m.widx, kMaskWords)) * kT] = m.w;  // (overflow: scratch word)
-  if (m.widx >= kMaskWords) *m.ok = 0;
+  m.base[static_cast<size_t>(min(m.widx, m.cap)) * kT] = m.w;  // (overflow: scratch word)
+  if (m.widx >= m.cap) *m.ok = 0;
   ++m.widx;
   m.w = 0u;
   m.n = 0;
@@ -1145,6 +1147,7 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
   mio.base = A.mbuf + static_cast<size_t>(sm.mslot < 0 ? kMaskSlots : sm.mslot) * (kMaskWords + 1) * kT +
              threadIdx.x;
   mio.ok = &sm.mok;
+  mio.cap = A.mwords;
   mio.widx = 0;
   mio.n = 0;
   mio.w = 0u;
@@ -2643,7 +2646,7 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
     A.heavy_count = ws.part_range + 3;
     A.queue = ws.part_range + 4;
     // phase-1 pair masks replayed by phase 2 (fp64 kernel; RSOT_CUDA_PAIR_MASKS=0: off)
-    A.mbuf = nullptr; A.mbusy = nullptr; A.mticket = nullptr; A.mslots = 0;
+    A.mbuf = nullptr; A.mbusy = nullptr; A.mticket = nullptr; A.mslots = 0; A.mwords = 0;
     if (!fp32 && !dbg) {
       if (!ws.mbuf) {
         TCK(cudaMalloc(&ws.mbuf, sizeof(uint32_t) * (static_cast<size_t>(kMaskSlots) + 1) * (kMaskWords + 1) * kT));
@@ -2654,6 +2657,9 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
       }
       A.mbuf = ws.mbuf; A.mbusy = ws.mbusy; A.mticket = ws.mticket;
       A.mslots = env_double("RSOT_CUDA_PAIR_MASKS", 1.0) != 0.0 ? 1 : 0;  // 0: phase 2 recomputes
+      // (tests: a small cap forces the overflow fallback in most CTAs)
+      A.mwords = static_cast<int>(std::min<double>(kMaskWords, std::max(0.0, env_double("RSOT_CUDA_MASK_WORDS",
+                                                                                        kMaskWords))));
     }
     // Scan costs of the chunks -> roles (partitioned atoms: this rank's
     // work-balanced range; heavy chunks run split across a CTA cluster) and a

@@ -543,3 +543,35 @@ def test_partitioned_atoms_balance():
     cnt = want["count"].astype(float)
     contiguous = np.array([cnt[len(A) * r // 8:len(A) * (r + 1) // 8].sum() for r in range(8)])
     assert contiguous.max() / contiguous.mean() > 2.0
+
+
+@pytest.mark.parametrize("cutoff", [0.004, 0.02])
+def test_pair_mask_replay_and_fallbacks(cutoff, monkeypatch):
+    """Phase 2 of the fp64 truncated kernel replays phase 1's pair masks from
+    per-CTA slots (truncated.cu MaskIO); CTAs whose masks overflow their slot
+    (forced here with RSOT_CUDA_MASK_WORDS) or that hold no slot
+    (RSOT_CUDA_PAIR_MASKS=0) recompute them.  All three paths must give
+    bitwise identical results, within 1e-10 of the oracle."""
+    rng = np.random.default_rng(977)
+    A = np.vstack([0.45 + 0.1 * rng.uniform(size=(4000, 3)), rng.uniform(size=(12000, 3))])
+    T = np.vstack([0.4 + 0.2 * rng.uniform(size=(60000, 3)), rng.uniform(size=(20000, 3))])
+    M = rng.uniform(size=len(A)) + 0.1
+    M /= M.sum()
+    W = np.full(len(T), 1.0 / len(T))
+    psi = rng.normal(0, 1e-3, size=len(T))
+    eps = 2e-3
+    runs = {}
+    for mode, env in (("replay", {}), ("overflow", {"RSOT_CUDA_MASK_WORDS": "3"}),
+                      ("recompute", {"RSOT_CUDA_PAIR_MASKS": "0"})):
+        for k in ("RSOT_CUDA_MASK_WORDS", "RSOT_CUDA_PAIR_MASKS"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        ctx = rs.Context(0)
+        runs[mode] = gpu_eval(ctx, A, M, T, W, psi, eps, cutoff)
+    for mode in ("overflow", "recompute"):
+        assert runs[mode]["J"] == runs["replay"]["J"] and runs[mode]["D"] == runs["replay"]["D"], mode
+        assert np.array_equal(runs[mode]["gradient"], runs["replay"]["gradient"]), mode
+        assert runs[mode]["candidate_pairs"] == runs["replay"]["candidate_pairs"], mode
+    want = C.evaluate_dual(A, M, T, W, psi, eps, cutoff, workers=8)
+    assert_parity(runs["replay"], want, marginal_scale(W, want["gradient"]), TOL)

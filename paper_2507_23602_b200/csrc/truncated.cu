@@ -917,7 +917,8 @@ __device__ __noinline__ unsigned slow_mask(const SM& sm, const FusedArgs& A, int
 // exponent split clamped.
 // The exponential part of a step for given pair predicates (kxy: item x,
 // atom y).
-template <int PHASE, bool PAIR, bool SAFE>
+// COUNT = false: the pair counts come from the stored mask words instead.
+template <int PHASE, bool PAIR, bool SAFE, bool COUNT = true>
 __device__ __forceinline__ double2 exp_part64(const FusedSmem& sm, FusedAtoms& at, bool wide,
                                               int t0, int t1, bool k0a, bool k0b, bool k1a,
                                               bool k1b, float2& cnt) {
@@ -931,7 +932,7 @@ __device__ __forceinline__ double2 exp_part64(const FusedSmem& sm, FusedAtoms& a
       sb0 -= at.xsqb;
     }
     if (PHASE == 1) {
-      cnt = __fadd2_rn(cnt, make_float2(k0a ? 1.f : 0.f, k0b ? 1.f : 0.f));
+      if (COUNT) cnt = __fadd2_rn(cnt, make_float2(k0a ? 1.f : 0.f, k0b ? 1.f : 0.f));
       at.Sa = exp2_acc_masked<SAFE, ExpTab512>(sa0, at.Sa, sm.tbl, k0a);
       at.Sb = exp2_acc_masked<SAFE, ExpTab512>(sb0, at.Sb, sm.tbl, k0b);
     } else {
@@ -946,7 +947,7 @@ __device__ __forceinline__ double2 exp_part64(const FusedSmem& sm, FusedAtoms& a
         sb1 -= at.xsqb;
       }
       if (PHASE == 1) {
-        cnt = __fadd2_rn(cnt, make_float2(k1a ? 1.f : 0.f, k1b ? 1.f : 0.f));
+        if (COUNT) cnt = __fadd2_rn(cnt, make_float2(k1a ? 1.f : 0.f, k1b ? 1.f : 0.f));
         at.Sa = exp2_acc_masked<SAFE, ExpTab512>(sa1, at.Sa, sm.tbl, k1a);
         at.Sb = exp2_acc_masked<SAFE, ExpTab512>(sb1, at.Sb, sm.tbl, k1b);
       } else {
@@ -967,12 +968,15 @@ struct MaskIO {
   uint32_t* base;  // thread's first word (words base[i * kT])
   int* ok;         // &sm.mok (cleared on overflow)
   int cap;         // words this thread may store
+  uint32_t ca, cb; // accepted pairs of atoms a, b in the stored words
   int widx;        // next word
   int n;           // steps in w (the first in the top bits)
   uint32_t w;
 };
 __device__ __forceinline__ void mask_store(MaskIO& m) {
   m.base[static_cast<size_t>(min(m.widx, m.cap)) * kT] = m.w;  // (overflow: scratch word)
+  m.ca += __popc(m.w & 0x55555555u);  // (bits 4s, 4s + 2: atom a; 4s + 1, 4s + 3: atom b)
+  m.cb += __popc(m.w & 0xAAAAAAAAu);
   if (m.widx >= m.cap) *m.ok = 0;
   ++m.widx;
   m.w = 0u;
@@ -992,7 +996,7 @@ __device__ __forceinline__ void mask_flush(MaskIO& m) {
 // Bits of step p (0..7) of a word.
 __device__ __forceinline__ uint32_t mask_bits(uint32_t w, int p) { return w >> (28 - 4 * p); }
 
-template <int PHASE, bool PAIR, bool SAFE, bool DEBUG, bool CHECK = true>
+template <int PHASE, bool PAIR, bool SAFE, bool DEBUG, bool CHECK = true, bool MASK = false>
 __device__ __forceinline__ double2 step64d(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at,
                                            const Step32& K, bool wide, int t0, int t1, float2 d0,
                                            float2 d1, float2& cnt, bool& hit,
@@ -1018,20 +1022,26 @@ __device__ __forceinline__ double2 step64d(const FusedSmem& sm, const FusedArgs&
   }
   const bool k0a = d0.x < K.lo, k0b = d0.y < K.lo;
   const bool k1a = PAIR && d1.x < K.lo, k1b = PAIR && d1.y < K.lo;
-  if (PHASE == 1 && !DEBUG && mio) mask_put(*mio, k0a, k0b, k1a, k1b);  // (mio: compile-time null or not)
-  return exp_part64<PHASE, PAIR, SAFE>(sm, at, wide, t0, t1, k0a, k0b, k1a, k1b, cnt);
+  if (PHASE == 1 && MASK) mask_put(*mio, k0a, k0b, k1a, k1b);
+  return exp_part64<PHASE, PAIR, SAFE, !(PHASE == 1 && MASK)>(sm, at, wide, t0, t1, k0a, k0b, k1a, k1b,
+                                                               cnt);
 }
 
-template <int PHASE, bool PAIR, bool SAFE, bool DEBUG, bool CHECK = true>
+template <int PHASE, bool PAIR, bool SAFE, bool DEBUG, bool CHECK = true, bool MASK = false>
 __device__ __forceinline__ double2 step64(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at,
                                           const Step32& K, bool wide, int t0, int t1,
                                           float2& cnt, bool& hit, MaskIO* mio = nullptr) {
   const float2 d0 = fused_d2(sm, at, t0);
   const float2 d1 = PAIR ? fused_d2(sm, at, t1) : d0;
-  return step64d<PHASE, PAIR, SAFE, DEBUG, CHECK>(sm, A, at, K, wide, t0, t1, d0, d1, cnt, hit, mio);
+  return step64d<PHASE, PAIR, SAFE, DEBUG, CHECK, MASK>(sm, A, at, K, wide, t0, t1, d0, d1, cnt, hit,
+                                                        mio);
 }
 
 // Phase-2 batch replaying the stored masks (word = the batch's 8 steps).
+// No guards on the steps (one basic block of 8 steps): items past nsel read
+// stale but finite staged entries (fused_body zeroes the list and staging
+// arrays once) and carry zero mask bits (phase 1 pads each tile's last word
+// with zeros), so they add +0; only the column writes are guarded.
 template <bool SAFE>
 __device__ __forceinline__ void batch64_masked(const FusedSmem& sm, FusedAtoms& at, bool wide,
                                                const ListT* list, int b0, int nsel, uint32_t mw,
@@ -1042,15 +1052,11 @@ __device__ __forceinline__ void batch64_masked(const FusedSmem& sm, FusedAtoms& 
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
     const int i = b0 + 2 * p;
-    double2 val = make_double2(0.0, 0.0);
-    if (i < nsel) {
-      const int t0 = list[i];
-      const int t1 = i + 1 < nsel ? list[i + 1] : t0;
-      const uint32_t b = mask_bits(mw, p);
-      val = exp_part64<2, true, SAFE>(sm, at, wide, t0, t1, b & 1u, b & 2u, b & 4u, b & 8u, dummy);
-    }
+    const uint32_t b = mask_bits(mw, p);
+    const double2 val = exp_part64<2, true, SAFE>(sm, at, wide, list[i], list[i + 1], b & 1u, b & 2u,
+                                                  b & 4u, b & 8u, dummy);
     v[2 * p] = val.x;
-    v[2 * p + 1] = i + 1 < nsel ? val.y : 0.0;
+    v[2 * p + 1] = val.y;
   }
   const double tot = butterfly16(v);
   const int item = b0 + (lane >> 1);
@@ -1148,10 +1154,10 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
              threadIdx.x;
   mio.ok = &sm.mok;
   mio.cap = A.mwords;
+  mio.ca = mio.cb = 0u;
   mio.widx = 0;
   mio.n = 0;
   mio.w = 0u;
-  MaskIO* const mp = kStore ? &mio : nullptr;
   for (int rb = 0; rb < nrows; rb += kT) {
     int st = 0, ln = 0;
     if (rb + threadIdx.x < nrows)
@@ -1196,10 +1202,11 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
               d0 = fused_d2(sm, at, t0);
               d1 = fused_d2(sm, at, t1);
             }
-            step64d<1, true, SAFE, DEBUG>(sm, A, at, K, wide, c0, c1, e0, e1, cn, hit, mp);
+            step64d<1, true, SAFE, DEBUG, true, kStore>(sm, A, at, K, wide, c0, c1, e0, e1, cn, hit, &mio);
           }
         }
-        if (i < nsel) step64<1, false, SAFE, DEBUG>(sm, A, at, K, wide, list[i], list[i], cn, hit, mp);
+        if (i < nsel)
+          step64<1, false, SAFE, DEBUG, true, kStore>(sm, A, at, K, wide, list[i], list[i], cn, hit, &mio);
         if (kStore) mask_flush(mio);  // each tile's stream starts on a word
         int f = 0;
         for (; f + 1 < nfull; f += 2)
@@ -1235,6 +1242,10 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
       fused_flush_cols(sm, A, pend);
       pend = 0;
     }
+  }
+  if (PHASE == 1 && kStore) {  // the mixed-list pairs were counted in the mask words
+    at.ca += mio.ca;
+    at.cb += mio.cb;
   }
 }
 
@@ -1341,6 +1352,12 @@ static_assert(sizeof(SplitXchg) <= sizeof(double) * (kT / 32) * kTileT, "exchang
 template <bool DEBUG, int KS>
 __device__ __forceinline__ void fused_body(FusedSmem& sm, const FusedArgs& A, int chunk, int split) {
   load_exp2_table<ExpTab512>(sm.tbl);
+  // finite, in-range stale entries for the unguarded replay batches
+  for (int t = threadIdx.x; t < kTileT; t += kT) {
+    sm.tDa[t] = make_double2(0.0, 0.0);
+    sm.tDb[t] = make_double2(0.0, 0.0);
+  }
+  for (int t = threadIdx.x; t < (kT / 32) * kTileT; t += kT) (&sm.wlist[0][0])[t] = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   FusedAtoms at;
   at.qa = chunk * kFA + warp * 64 + lane;

@@ -1099,14 +1099,10 @@ __device__ __forceinline__ void batch64_full(const FusedSmem& sm, FusedAtoms& at
   float2 dummy = make_float2(0.f, 0.f);
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
-    const int i = b0 + 2 * p;
-    double2 val = make_double2(0.0, 0.0);
-    if (i < nfull) {
-      const int t0 = full[-i];
-      const bool two = i + 1 < nfull;
-      const int t1 = two ? full[-(i + 1)] : t0;
-      val = exp_part64<2, true, SAFE>(sm, at, wide, t0, t1, va, vb, two && va, two && vb, dummy);
-    }
+    const int i = b0 + 2 * p;  // (unguarded: items past nfull are stale entries taken by no atom)
+    const bool in0 = i < nfull, in1 = i + 1 < nfull;
+    const double2 val = exp_part64<2, true, SAFE>(sm, at, wide, full[-i], full[-(i + 1)], in0 && va,
+                                                  in0 && vb, in1 && va, in1 && vb, dummy);
     v[2 * p] = val.x;
     v[2 * p + 1] = val.y;
   }
@@ -1208,11 +1204,14 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
         if (i < nsel)
           step64<1, false, SAFE, DEBUG, true, kStore>(sm, A, at, K, wide, list[i], list[i], cn, hit, &mio);
         if (kStore) mask_flush(mio);  // each tile's stream starts on a word
-        int f = 0;
-        for (; f + 1 < nfull; f += 2)
-          exp_part64<1, true, SAFE>(sm, at, wide, full[-f], full[-(f + 1)], va, vb, va, vb, cn);
-        if (f < nfull)
-          exp_part64<1, false, SAFE>(sm, at, wide, full[-f], full[-f], va, vb, false, false, cn);
+        // full-in items, 4 per iteration without guards (items past nfull:
+        // stale entries taken by no atom; f <= 252, so f + 3 stays in the list)
+        for (int f = 0; f < nfull; f += 4) {
+          const bool i1 = f + 1 < nfull, i2 = f + 2 < nfull, i3 = f + 3 < nfull;
+          exp_part64<1, true, SAFE>(sm, at, wide, full[-f], full[-(f + 1)], va, vb, i1 && va, i1 && vb, cn);
+          exp_part64<1, true, SAFE>(sm, at, wide, full[-(f + 2)], full[-(f + 3)], i2 && va, i2 && vb,
+                                    i3 && va, i3 && vb, cn);
+        }
         at.ca += static_cast<uint32_t>(cn.x);
         at.cb += static_cast<uint32_t>(cn.y);
       } else {

@@ -279,6 +279,10 @@ def run_ours(args, rank, world, local_rank):
     h_psi.copy_(torch.from_numpy(np.stack(psis[W:W + K])))
     h_g = torch.empty(n, dtype=torch.float64).pin_memory()
     scal = _lib.RsotCudaScalars()
+    for k in range(min(W, K)):  # warm-up of the host-pointer path (untimed, like the device steps)
+        _lib.check(lib.rsot_cuda_eval(ctx.handle, dev_a.handle, dev_t.handle,
+                                      ctypes.c_void_p(h_psi[k].data_ptr()), prob.eps, cutoffs[W + k],
+                                      ctypes.c_void_p(h_g.data_ptr()), ctypes.byref(scal)))
     barrier()
     t0 = time.perf_counter()
     for k in range(K):

@@ -43,7 +43,8 @@ constexpr int kTileT = 256;    // staged points per tile (fp64 kernel)
 constexpr int kTileT32 = 384;  // staged points per tile (fp32 kernel)
 using ListT = unsigned short;  // per-warp culled-list entry (tile index)
 constexpr int kMortonBits = 7; // per dim, position inside a cell
-double g_cells_per_radius = 3.0;  // grid cell side ~ r / 3 (env RSOT_CELLS_PER_RADIUS)
+double g_cells_per_radius = 5.0;  // grid cell side ~ r / 5 (env RSOT_CELLS_PER_RADIUS; swept 2-8: r/5-r/6 best
+                                  // for cfg3/cfg5 in both precisions since the phase-2 mask replay)
 
 struct GridDev {
   double lo[3];

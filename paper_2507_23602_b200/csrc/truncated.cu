@@ -841,6 +841,7 @@ struct Step32 {
   float nbig, lobig;  // indicator sat(lo*BIG - d2*BIG) = [d2 < lo] exactly
   float2 nlo, nhi;
   float2 nc2;
+  float2 nmid2;    // (-mid, -mid) for the packed band test
 };
 
 __device__ __forceinline__ float sat_fma(float a, float b, float c) {
@@ -860,6 +861,7 @@ __device__ __forceinline__ Step32 make_step(float lo_thr, float hi_thr) {
     const double lo = lo_thr, hi = hi_thr;
     const float mid = static_cast<float>(0.5 * (lo + hi));
     K.nmid = -mid;
+    K.nmid2 = make_float2(-mid, -mid);
     K.hw = static_cast<float>(fmax(hi - mid, mid - lo) * (1.0 + 0x1p-20) +
                               4.0 * fabs(hi) * 0x1p-23) + 1e-30f;
   }
@@ -876,8 +878,12 @@ __device__ __forceinline__ Step32 make_step(float lo_thr, float hi_thr) {
 // [lo, hi] where the exact fp64 predicate decides (false positives harmless).
 template <bool PAIR>
 __device__ __forceinline__ bool step_in_band(const Step32& K, float2 d0, float2 d1) {
-  float bm = fminf(fabsf(d0.x + K.nmid), fabsf(d0.y + K.nmid));
-  if (PAIR) bm = fminf(bm, fminf(fabsf(d1.x + K.nmid), fabsf(d1.y + K.nmid)));
+  const float2 a = __fadd2_rn(d0, K.nmid2);  // (same roundings as scalar adds)
+  float bm = fminf(fabsf(a.x), fabsf(a.y));
+  if (PAIR) {
+    const float2 b = __fadd2_rn(d1, K.nmid2);
+    bm = fminf(bm, fminf(fabsf(b.x), fabsf(b.y)));
+  }
   return bm <= K.hw;
 }
 

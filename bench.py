@@ -1,16 +1,19 @@
 """bench.py -- RSOT dual objective + gradient evaluations on B200.
 
-Default workload = BASELINE.json configs[1] (cfg2: 3D dense, 262,144 Gauss
-atoms x 16,384 mixture targets, eps = 1e-2, fp64, fresh psi per
-evaluation).  A step is one evaluation (dual objective J + gradient over all
-pairs) with a fresh psi.
+Default workload = BASELINE.json configs[4] (cfg5: truncated, 128^3 hexes x
+2^3 Gauss = 16,777,216 atoms x 1,048,576 U[0,1]^3 targets, eps = 1e-4,
+pointwise truncation 1e-12, fp64), the largest configuration that fits one
+GPU; cfg1/cfg2/cfg3 behind --workload, fp32 behind --precision.  A step is
+one evaluation (dual objective J + gradient over all candidate pairs) with a
+fresh psi.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg5]
   python bench.py --impl reference ...   (the reference CPU evaluate_dual)
 
-Under torchrun (N > 1) every rank owns a contiguous atom shard and the
-library reduces [g | J | D | counters] with one ncclAllReduce per
-evaluation; timing is the max over ranks.
+Under torchrun (N > 1) every rank holds the atoms partitioned by
+work-balanced Hilbert chunk ranges (truncated) or contiguous shards (dense)
+and the library combines [g | J | D | counters] with one ncclAllGather and a
+rank-ordered sum per evaluation; timing is the max over ranks.
 
 Prints ONE JSON line on rank 0.  `value` times device-resident psi/g
 (rsot_cuda_eval_device); `e2e` times the C-ABI call a user makes
@@ -20,6 +23,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes
+import hashlib
 import json
 import math
 import os
@@ -44,6 +48,11 @@ WORKLOADS = {
     "cfg5": "cfg5: 3D truncated (pointwise 1e-12), 128^3 hexes x 2^3 = 16,777,216 atoms, N=1,048,576 "
             "U[0,1]^3, eps=1e-4",
 }
+# Reference-arm (and cpu_baseline) sample per step: a seeded atom subset of
+# 1/frac of the atoms against ALL targets (~2-4 s of 16-thread CPU work), so
+# K + W steps finish within minutes; evals/s = (sample atoms / atoms) / step
+# time.  Dense cfg1/cfg2 run at full size.
+REF_SAMPLE_FRACTION = {"cfg1": 1, "cfg2": 1, "cfg3": 64, "cfg5": 32}
 
 
 def parse():
@@ -52,7 +61,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
                     help="fp32: mixed-precision truncated path (FP32 exponent + ex2, fp64 sums; "
@@ -66,12 +75,37 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
+# Shared configuration (identical dict in both arms)
+
+def input_sha256(prob) -> str:
+    """SHA-256 over the exact input bits (atoms, masses, targets, nu)."""
+    h = hashlib.sha256()
+    for a in (prob.atoms, prob.masses, prob.targets, prob.nu):
+        h.update(np.ascontiguousarray(a, dtype=np.float64).tobytes())
+    return h.hexdigest()
+
+
+def bench_config(args, prob, world):
+    return {"workload": WORKLOADS[args.workload], "nq": prob.nq, "n": prob.n, "eps": prob.eps,
+            "truncation": ("none (cutoff=+inf)" if prob.truncation == "none" else
+                           f"pointwise delta_thr={prob.delta_thr:g}: cutoff = max psi + eps ln(nu_max/delta_thr) "
+                           "per evaluation (evaluate.cpp:22-25), radius sqrt(2 cutoff)"),
+            "parallelism": f"atoms partitioned over {world} GPU(s), targets replicated, "
+                           "1 allgather + rank-ordered sum / eval",
+            "precision": args.precision,
+            "l2": "flushed between steps (160 MiB write > 126 MB L2, inside the timed region)",
+            "psi": f"fresh psi~N(0,{prob.psi_sigma:g}^2) per step (seeded)",
+            "inputs_sha256": input_sha256(prob)}
+
+
+# ---------------------------------------------------------------------------
 # CPU reference arm (oracle/_ref: the reference's own evaluate_dual compiled
 # from its sources; oracle port if that was not built)
 
-def cpu_reference_runner(prob, sample_atoms):
+def cpu_reference_runner(prob, frac_den):
     from paper_2507_23602_b200 import synth
-    sub = synth.subsample_atoms(prob, sample_atoms) if sample_atoms < prob.nq else prob
+    count = prob.nq // frac_den
+    sub = synth.subsample_atoms(prob, count) if frac_den > 1 else prob
     threads = os.cpu_count() or 1
     try:
         from oracle.oracle import RefLib
@@ -89,20 +123,19 @@ def cpu_reference_runner(prob, sample_atoms):
         def run(psi, cutoff):
             return C.evaluate_dual(sub.atoms, sub.masses, prob.targets, prob.nu, psi, prob.eps, cutoff, threads)
     frac = sub.nq / prob.nq
-    desc = (f"{sub.nq} of {prob.nq} atoms (seeded subset) x all {prob.n} targets per evaluation, "
-            f"{threads} std::thread workers (SolverConfig::workers), evals/s extrapolated by the atom fraction")
+    if frac_den > 1:
+        desc = (f"each step: one evaluate_dual over a fixed seeded subset of {sub.nq} of {prob.nq} atoms "
+                f"(1/{frac_den}) x all {prob.n} targets, fresh psi; {threads} std::thread workers "
+                "(SolverConfig::workers); evals/s = atom fraction / step time; ms_per_step is the timed "
+                "sample step")
+    else:
+        desc = (f"each step: one full-size evaluate_dual ({prob.nq} atoms x {prob.n} targets), fresh psi; "
+                f"{threads} std::thread workers (SolverConfig::workers)")
     return run, frac, kind, threads, desc
 
 
-def cpu_sample_size(prob):
-    # ~2-4 s per sampled evaluation on a 16-core host
-    pairs_budget = {"none": 1.0e9, "pointwise": 6.0e7}[prob.truncation]
-    per_atom = prob.n if prob.truncation == "none" else 700
-    return int(max(256, min(prob.nq, pairs_budget / per_atom)))
-
-
-def time_cpu(prob, steps, warmup):
-    run, frac, kind, threads, desc = cpu_reference_runner(prob, cpu_sample_size(prob))
+def time_cpu(prob, workload, steps, warmup):
+    run, frac, kind, threads, desc = cpu_reference_runner(prob, REF_SAMPLE_FRACTION.get(workload, 1))
     times = []
     for k in range(warmup + steps):
         psi = prob.psi(k)
@@ -111,8 +144,8 @@ def time_cpu(prob, steps, warmup):
         dt = time.perf_counter() - t0
         if k >= warmup:
             times.append(dt)
-    per_eval_full = statistics.median(times) / frac
-    return 1.0 / per_eval_full, kind, threads, desc, times
+    step_s = sum(times) / len(times)
+    return frac / step_s, step_s, kind, threads, desc, times
 
 
 def run_reference(args, rank):
@@ -120,15 +153,16 @@ def run_reference(args, rank):
         return
     from paper_2507_23602_b200 import synth
     prob = synth.make(args.workload)
-    steps = max(1, min(args.steps, 10))
-    warm = max(0, min(args.warmup, 2))
-    v, kind, cores, desc, times = time_cpu(prob, steps, warm)
+    K, W = args.steps, args.warmup
+    v, step_s, kind, cores, desc, times = time_cpu(prob, args.workload, K, W)
+    frac = prob.nq // REF_SAMPLE_FRACTION.get(args.workload, 1) / prob.nq
     line = {
-        "metric": METRIC, "value": v, "unit": "evals/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
-        "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded; BASELINE shapes)", "impl": "reference",
-        "config": {"workload": WORKLOADS[args.workload]},
-        "pairs_per_s": v * prob.nq * prob.n if prob.truncation == "none" else None,
+        "metric": METRIC, "value": v, "unit": "evals/s", "n_gpus": args.gpus, "steps": K, "warmup": W,
+        "ms_per_step": 1e3 * step_s, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded generator with BASELINE shapes; no dataset exists)",
+        "impl": "reference", "config": bench_config(args, prob, args.gpus),
+        "sample_fraction": frac,
+        "step_s": {"median": statistics.median(times), "min": min(times), "max": max(times)},
         "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": kind, "sample": desc},
         "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -325,11 +359,16 @@ def run_ours(args, rank, world, local_rank):
     achieved = algo_flops / (kern_ms * 1e-3) / 1e12
     kernel_desc = ("pass A (LSE) + pass B (gradient gather), per GPU" if prob.truncation == "none" else
                    "trunc_fused%s (both phases) + trunc_nearest_empty, per GPU" % ("32" if mixed else ""))
-    traffic = None
+    # DRAM bytes of the hot kernels per evaluation: a LOOKUP of the committed
+    # ncu --set full summary (ncu cannot run inside the timed bench), labelled
+    # with the capture it comes from
+    traffic, traffic_src = None, None
     prof = os.path.join(ROOT, "profiles", f"ncu_summary_{args.workload}{'_fp32' if mixed else ''}.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_eval")
+            pj = json.load(open(prof))
+            traffic = pj.get("dram_bytes_per_eval")
+            traffic_src = f"lookup: {os.path.relpath(prof, ROOT)} ({pj.get('note', '')})"
         except Exception:
             traffic = None
     line = {
@@ -337,16 +376,13 @@ def run_ours(args, rank, world, local_rank):
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32+f64" if mixed else "f64",
         "data": "synthetic (seeded generator with BASELINE shapes; no dataset exists)",
-        "config": {"workload": WORKLOADS[args.workload], "nq": prob.nq, "n": prob.n, "eps": prob.eps,
-                   "parallelism": f"atoms sharded over {world} GPU(s), targets replicated, "
-                                  "1 allgather + rank-ordered sum / eval",
-                   "precision": args.precision,
-                   "l2": "flushed between steps (160 MiB write > 126 MB L2, inside the timed region)"},
+        "config": bench_config(args, prob, world),
         "pairs_per_s": pairs * value,
         "candidate_pairs_per_eval": pairs,
         "roofline": {
             "bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic,
+            "traffic_source": traffic_src,
             "kernel": kernel_desc,
             "kernel_ms": {"pass_a": statistics.median(passA), "pass_b": statistics.median(passB)},
             "definition": definition,
@@ -358,7 +394,7 @@ def run_ours(args, rank, world, local_rank):
     }
     if not args.no_cpu_baseline and world == 1:
         try:
-            v, kind, cores, desc, _ = time_cpu(prob, 2, 1)
+            v, _, kind, cores, desc, _ = time_cpu(prob, args.workload, 3, 1)
             line["cpu_baseline"] = {"value": v, "unit": "evals/s", "cores": cores, "kind": kind, "sample": desc}
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "port",

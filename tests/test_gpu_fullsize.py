@@ -1,0 +1,108 @@
+"""Full-size parity at the BASELINE configs cfg2 / cfg3 / cfg5 against the
+REFERENCE's own evaluate_dual (proj/src/evaluate.cpp:86-174, compiled from
+its sources as oracle/_ref) stored in tests/golden/fullsize_<cfg>.npz by
+tests/golden/make_fullsize.py.
+
+The seeded inputs are regenerated here (paper_2507_23602_b200/synth.py) and
+checked bit for bit against the fixture's SHA-256 before any comparison.
+Bars: |dJ| <= 1e-10 |J|, ||dg||_inf <= 1e-10 max_k(nu~_k+nu_k),
+|dD| <= 1e-10 D, counters exact; truncated configs also match the per-atom
+(candidate count, candidate hash) digest over ALL atoms (ball_query,
+spatial_index.cpp:47-61) and a stored sample of the raw per-atom values.
+The fp32 path is held to its stated tolerance (2e-5, tests/test_gpu_fp32.py)
+with exact candidate sets.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import assert_parity, marginal_scale
+import paper_2507_23602_b200 as rs
+from paper_2507_23602_b200 import synth
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+from fullsize import CONFIGS, PSI_INDEX, atom_digest, input_sha256, path  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+TOL32 = 2e-5
+
+
+def _fixture(name):
+    p = path(name)
+    if not os.path.exists(p):
+        pytest.skip(f"{p} not generated (tests/golden/make_fullsize.py)")
+    return np.load(p)
+
+
+@pytest.fixture(scope="module")
+def problems():
+    cache = {}
+
+    def get(name):
+        if name not in cache:
+            cache.clear()  # one full-size config resident at a time (host memory)
+            p = synth.make(name)
+            psi = p.psi(PSI_INDEX)
+            cache[name] = (p, psi)
+        return cache[name]
+    return get
+
+
+def _want(z):
+    visited, pairs, empty = (int(v) for v in z["counters"])
+    return dict(J=float(z["J"]), D=float(z["D"]), gradient=z["gradient"], atoms_visited=visited,
+                candidate_pairs=pairs, empty_candidate_atoms=empty)
+
+
+_CTX = {}
+
+
+def _check(p, psi, z, precision, tol):
+    if precision not in _CTX:
+        _CTX[precision] = rs.Context(0)
+        _CTX[precision].set_precision(precision)
+    ctx = _CTX[precision]
+    atoms = rs.SourceAtoms(dim=p.dim, points=p.atoms, masses=p.masses)
+    tgt = rs.TargetMeasure(dim=p.dim, points=p.targets, weights=p.nu)
+    cut = float(z["cutoff"])
+    assert cut == p.cutoff(psi)
+    want = _want(z)
+    scale = marginal_scale(p.nu, want["gradient"])
+    # the user-facing call (host psi in, host g out)
+    res = rs.evaluate_dual(atoms, tgt, rs.DualPotential(psi), rs.SolverConfig(epsilon=p.eps),
+                           rs.TruncationState(cutoff=cut), ctx=ctx)
+    got = dict(J=res.J, D=res.D, gradient=res.gradient, atoms_visited=res.atoms_visited,
+               candidate_pairs=res.candidate_pairs, empty_candidate_atoms=res.empty_candidate_atoms)
+    assert_parity(got, want, scale, tol)
+    if p.truncation == "none":
+        return
+    # selection parity over every atom (debug entry point, same evaluation)
+    res2, cnt, hsh, _ = rs.evaluate_dual_debug(atoms, tgt, psi, p.eps, cut, ctx=ctx)
+    idx = z["sample_idx"]
+    assert np.array_equal(cnt[idx], z["sample_count"]), "per-atom candidate counts differ (sample)"
+    assert np.array_equal(hsh[idx], z["sample_hash"]), "per-atom candidate hashes differ (sample)"
+    assert int(np.sum(cnt, dtype=np.uint64)) == int(z["count_sum"])
+    assert int(cnt.max()) == int(z["count_max"])
+    assert atom_digest(cnt, hsh) == int(z["digest"]), "per-atom (count, hash) digest differs"
+    assert res2.J == res.J and np.array_equal(res2.gradient, res.gradient)  # bitwise reproducible
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_fullsize_fp64_vs_reference(problems, name):
+    z = _fixture(name)
+    assert bool(z["c_oracle_equals_ref"])  # the C restatement matched the reference at this size
+    p, psi = problems(name)
+    assert input_sha256(p, psi) == str(z["sha256"]), "regenerated inputs differ from the fixture's"
+    _check(p, psi, z, "fp64", TOL)
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg5"])
+def test_fullsize_fp32_vs_reference(problems, name):
+    z = _fixture(name)
+    p, psi = problems(name)
+    assert input_sha256(p, psi) == str(z["sha256"])
+    _check(p, psi, z, "fp32", TOL32)

@@ -93,6 +93,37 @@ void rsot_cuda_shard_range(size_t nq, int rank, int world, size_t* lo,
  * J = sum_r J_r + (world-1) sum psi nu, D and the counters add). */
 int rsot_cuda_ctx_set_virtual_rank(rsot_cuda_ctx* ctx, int rank, int world);
 
+/* Atoms evaluated whole on this rank: evaluations and covering_cost on this
+ * handle never take part in the cross-rank combination, even on a context
+ * with a communicator (per-rank work such as PlanView construction, which
+ * plan.cpp:35-64 does for the caller's own atoms; no hidden collective). */
+int rsot_cuda_atoms_create_local(rsot_cuda_ctx* ctx, const double* xyz,
+                                 const double* mass, size_t nq,
+                                 rsot_cuda_atoms** out);
+
+/* Testing: one evaluation as `world` virtual ranks of a multi-GPU run on
+ * this GPU (partitioned atom handle, context without a communicator).  Every
+ * virtual rank's packed partial [g + nu | J + sum psi nu | D | pairs | empty |
+ * visited] is computed as that rank computes it and copied to the rank's
+ * offset of the gather buffer (in place of ncclAllGather); the rank-ordered
+ * sum and finalisation are the launches that follow the collective in a
+ * real multi-GPU evaluation (merge order: parallel.hpp:24-30). */
+int rsot_cuda_eval_virtual_world(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
+                                 rsot_cuda_targets* targets, const double* psi,
+                                 double epsilon, double cutoff, int world,
+                                 double* g_out, rsot_cuda_scalars* out);
+
+/* Host mirrors of the cross-rank combination (same element functions as
+ * the device kernels; used by the multi-process CPU tests):
+ * out[i] = sum over r in rank order of gathered[r * len + i];
+ * g_out[j] = res[j] - nu[j], scalars_out = [J - psi_nu, D, pairs, empty,
+ * visited] (evaluate.cpp:157-172). */
+void rsot_cuda_host_rank_sum(const double* gathered, int world, size_t len,
+                             double* out);
+void rsot_cuda_host_finalize(const double* res, const double* nu, size_t n,
+                             double psi_nu, double* g_out,
+                             double* scalars_out);
+
 /* ---- resident data ------------------------------------------------------- */
 /* TargetMeasure{points, weights} (measures.hpp:13-19); n >= 1 else
  * RSOT_CUDA_INVALID_ARGUMENT ("spatial index: empty point set"). */
@@ -186,6 +217,13 @@ int rsot_cuda_nearest(rsot_cuda_ctx* ctx, rsot_cuda_targets* targets,
  * max-reduced over ranks (spatial_index.cpp:101-121). */
 int rsot_cuda_covering_cost(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
                             rsot_cuda_targets* targets, double* out);
+/* covering_cost for either cost kind (spatial_index.cpp:101-121).
+ * SqGeodesicSphere: the device finds t* = min_q max_j clamp(x_q . y_j) with
+ * the reference's unfused dot; acos(t*)^2 is taken on the host (monotone, so
+ * equal to the reference's max_q min_j cost). */
+int rsot_cuda_covering_cost_kind(rsot_cuda_ctx* ctx, rsot_cuda_atoms* atoms,
+                                 rsot_cuda_targets* targets, int cost_kind,
+                                 double* out);
 
 /* ---- softmax_refine (multilevel prolongation) -----------------------------
  * rsot::softmax_refine (proj/src/solve.cpp:62-142): psi on the n_fine points

@@ -217,6 +217,8 @@ class RefLib:
                                          c_void_p]
         L.ref_covering_cost.restype = c_int
         L.ref_covering_cost.argtypes = [c_void_p, POINTER(c_double)]
+        L.ref_covering_cost_kind.restype = c_int
+        L.ref_covering_cost_kind.argtypes = [c_void_p, c_int, POINTER(c_double)]
         L.ref_evaluate_dual_kind.restype = c_int
         L.ref_evaluate_dual_kind.argtypes = [c_void_p, c_void_p, c_size_t, c_double, c_double, c_int, c_void_p,
                                              POINTER(Scalars)]
@@ -287,9 +289,10 @@ class RefProblem:
         out["starved"] = int(st.value)
         return out
 
-    def covering_cost(self):
+    def covering_cost(self, kind: int = 0):
+        """kind 0 = SqEuclidean, 1 = SqGeodesicSphere."""
         v = c_double()
-        if self.lib.L.ref_covering_cost(self.h, ctypes.byref(v)) != 0:
+        if self.lib.L.ref_covering_cost_kind(self.h, kind, ctypes.byref(v)) != 0:
             raise ValueError(self.lib.L.ref_last_error().decode())
         return v.value
 

@@ -136,17 +136,21 @@ int ref_evaluate_dual_kind(void* prob, const double* psi, size_t n, double eps, 
   }
 }
 
-// rsot::covering_cost (spatial_index.cpp:101-121 semantics).
-int ref_covering_cost(void* prob, double* out) {
+// rsot::covering_cost (spatial_index.cpp:101-121 semantics); kind 0 =
+// SqEuclidean, 1 = SqGeodesicSphere (the reference's full scan).
+int ref_covering_cost_kind(void* prob, int kind, double* out) {
   auto* p = static_cast<RefProblem*>(prob);
   try {
-    *out = rsot::covering_cost(p->atoms, p->target, rsot::CostKind::SqEuclidean);
+    *out = rsot::covering_cost(p->atoms, p->target,
+                               kind == 1 ? rsot::CostKind::SqGeodesicSphere : rsot::CostKind::SqEuclidean);
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;
   }
 }
+
+int ref_covering_cost(void* prob, double* out) { return ref_covering_cost_kind(prob, 0, out); }
 
 // rsot::softmax_refine (solve.cpp:62-142): prob's targets are the coarse
 // level, prob's atoms the atoms; fine points given separately.

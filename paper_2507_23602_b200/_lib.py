@@ -75,6 +75,12 @@ _SIGNATURES = [
     ("rsot_cuda_last_kernel_ms", c_int, [c_void_p, POINTER(c_double), POINTER(c_double), POINTER(c_double)]),
     ("rsot_cuda_measure_fp64_peak", c_int, [c_void_p, POINTER(c_double)]),
     ("rsot_cuda_kernel_launches", c_uint64, []),
+    ("rsot_cuda_eval_virtual_world", c_int,
+     [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_int, c_void_p, POINTER(RsotCudaScalars)]),
+    ("rsot_cuda_host_rank_sum", None, [c_void_p, c_int, c_size_t, c_void_p]),
+    ("rsot_cuda_atoms_create_local", c_int, [c_void_p, c_void_p, c_void_p, c_size_t, POINTER(c_void_p)]),
+    ("rsot_cuda_covering_cost_kind", c_int, [c_void_p, c_void_p, c_void_p, c_int, POINTER(c_double)]),
+    ("rsot_cuda_host_finalize", None, [c_void_p, c_void_p, c_size_t, c_double, c_void_p, c_void_p]),
 ]
 
 EXPORTED_SYMBOLS = [name for name, _, _ in _SIGNATURES]

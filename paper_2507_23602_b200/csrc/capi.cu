@@ -17,6 +17,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "../../include/rsot_cuda.h"
@@ -152,6 +153,8 @@ struct rsot_cuda_atoms {
   double4* x = nullptr;  // {x0, x1, x2, m}
   AtomCells cells;       // Hilbert order (built on first truncated use)
   bool partitioned = false;  // every atom on every rank; evaluations split the work
+  double mass_sum = 0.0;     // sum of the masses (bounds every gradient contribution)
+  bool local = false;        // evaluated whole on this rank, never combined across ranks
 };
 
 namespace {
@@ -212,11 +215,11 @@ EvalBuffers buffers(rsot_cuda_ctx* c, double* g_out, double* scalars_out) {
   return b;
 }
 
-// Enqueues one evaluation reading psi from b.psi (device) and leaving the
-// final gradient / scalars in b.g_out / b.scalars_out.
-int enqueue_eval(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
-                 EvalBuffers& b, double eps, double cutoff, DebugOut* dbg,
-                 int cost = RSOT_CUDA_COST_SQEUCLIDEAN) {
+// Enqueues this rank's share of one evaluation reading psi from b.psi
+// (device): the packed partial buffer b.res = [g + nu | J + sum psi nu | D |
+// pairs | empty | visited] before the cross-rank combination.
+int enqueue_partial(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
+                    EvalBuffers& b, double eps, double cutoff, DebugOut* dbg, int cost) {
   const cudaStream_t s = c->stream;
   const DeviceTargets dt = make_dt(t);
   DeviceAtoms da{a->x, static_cast<int>(a->nq)};
@@ -246,6 +249,12 @@ int enqueue_eval(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
                                 dbg ? dbg->log_s : nullptr);
     if (rc != 0) return fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error);
   } else if (std::isfinite(cutoff)) {
+    // every truncated gradient contribution m_q p_qj / S_q <= m_q goes into
+    // the fixed-point accumulator, whose top limb holds totals below 2^42
+    if (!(a->mass_sum < 0x1p40))
+      return fail(RSOT_CUDA_INVALID_ARGUMENT,
+                  "truncated evaluation: total atom mass >= 2^40 exceeds the fixed-point gradient "
+                  "accumulator (normalise the masses)");
     const int rc = run_truncated(c->trunc, da, a->cells, dt, t->cells, b, eps,
                                  cutoff, c->num_sms, dbg, s, g_last_error,
                                  c->precision == RSOT_CUDA_PRECISION_FP32, prank, pworld);
@@ -255,7 +264,19 @@ int enqueue_eval(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
     launch_dense(da, dt, b, plan, eps, s);
     if (dbg) launch_dense_debug(da, dt, b, *dbg, s);
   }
-  if (c->comm) {
+  return RSOT_CUDA_OK;
+}
+
+// Enqueues one evaluation reading psi from b.psi (device) and leaving the
+// final gradient / scalars in b.g_out / b.scalars_out.
+int enqueue_eval(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
+                 EvalBuffers& b, double eps, double cutoff, DebugOut* dbg,
+                 int cost = RSOT_CUDA_COST_SQEUCLIDEAN) {
+  const cudaStream_t s = c->stream;
+  const DeviceTargets dt = make_dt(t);
+  const int rc = enqueue_partial(c, a, t, b, eps, cutoff, dbg, cost);
+  if (rc) return rc;
+  if (c->comm && !a->local) {
     // one collective per evaluation: every rank gathers all packed partial
     // buffers and sums them in rank order, so the result is bitwise the same
     // on every rank and run to run (independent of NCCL's ring / tree / NVLS
@@ -300,10 +321,18 @@ int finish_host_eval(rsot_cuda_ctx* c, rsot_cuda_targets* t, double* g_out,
                           sizeof(double), cudaMemcpyDeviceToHost, s));
   RSOT_CK(cudaMemcpyAsync(g_out, c->g_out.p, sizeof(double) * t->n,
                           cudaMemcpyDeviceToHost, s));
+  unsigned* ovf = reinterpret_cast<unsigned*>(c->h_pinned + kResTail + 1);
+  RSOT_CK(trunc_read_overflow(ovf, s));
   RSOT_CK(cudaStreamSynchronize(s));
   record_timing(c);
   if (c->h_pinned[kResTail] != 0.0)
     return fail(RSOT_CUDA_INVALID_ARGUMENT, "potential has non-finite entries");
+  if (*ovf) {
+    trunc_clear_overflow();
+    return fail(RSOT_CUDA_RUNTIME_ERROR,
+                "gradient accumulator overflow: a single atom-target contribution >= 2^41 "
+                "(masses far from normalised)");
+  }
   out->J = c->h_pinned[kResJ];
   out->D = c->h_pinned[kResD];
   out->candidate_pairs = static_cast<uint64_t>(c->h_pinned[kResPairs]);
@@ -444,30 +473,46 @@ int rsot_cuda_targets_create(rsot_cuda_ctx* c, const double* xyz, const double* 
   if (n > (1u << 30)) return fail(RSOT_CUDA_INVALID_ARGUMENT, "too many targets");
   int rc = set_device(c);
   if (rc) return rc;
+  // validation before any device allocation (every point, from j = 0)
+  double lo[3], hi[3];
+  for (int d = 0; d < 3; ++d) lo[d] = hi[d] = xyz[d];
   std::vector<double4> h(n);
-  for (size_t j = 0; j < n; ++j)
-    h[j] = make_double4(xyz[3 * j], xyz[3 * j + 1], xyz[3 * j + 2], std::log(nu[j]));
-  auto* t = new rsot_cuda_targets();
-  for (int d = 0; d < 3; ++d) t->cells.bbox_lo[d] = t->cells.bbox_hi[d] = xyz[d];
-  for (size_t j = 1; j < n; ++j)
+  for (size_t j = 0; j < n; ++j) {
     for (int d = 0; d < 3; ++d) {
       const double v = xyz[3 * j + d];
-      if (!std::isfinite(v)) {
-        delete t;
+      if (!std::isfinite(v))
         return fail(RSOT_CUDA_INVALID_ARGUMENT, "target point has non-finite coordinates");
-      }
-      t->cells.bbox_lo[d] = std::min(t->cells.bbox_lo[d], v);
-      t->cells.bbox_hi[d] = std::max(t->cells.bbox_hi[d], v);
+      lo[d] = std::min(lo[d], v);
+      hi[d] = std::max(hi[d], v);
     }
+    h[j] = make_double4(xyz[3 * j], xyz[3 * j + 1], xyz[3 * j + 2], std::log(nu[j]));
+  }
+  std::unique_ptr<rsot_cuda_targets> t(new (std::nothrow) rsot_cuda_targets());
+  if (!t) return fail(RSOT_CUDA_RUNTIME_ERROR, "out of host memory");
+  for (int d = 0; d < 3; ++d) {
+    t->cells.bbox_lo[d] = lo[d];
+    t->cells.bbox_hi[d] = hi[d];
+  }
   t->cells.bbox_set = true;
   t->ctx = c;
   t->n = n;
-  RSOT_CK(cudaMalloc(&t->y, sizeof(double4) * n));
-  RSOT_CK(cudaMalloc(&t->nu, sizeof(double) * n));
-  RSOT_CK(cudaMemcpyAsync(t->y, h.data(), sizeof(double4) * n, cudaMemcpyHostToDevice, c->stream));
-  RSOT_CK(cudaMemcpyAsync(t->nu, nu, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
-  RSOT_CK(cudaStreamSynchronize(c->stream));
-  *out = t;
+  // (on any error below the partially built handle is released)
+  auto release = [&](cudaError_t e, const char* what) {
+    cudaFree(t->y);
+    cudaFree(t->nu);
+    t->y = nullptr;
+    t->nu = nullptr;
+    return fail(RSOT_CUDA_RUNTIME_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+  };
+  cudaError_t e = cudaMalloc(&t->y, sizeof(double4) * n);
+  if (e != cudaSuccess) return release(e, "cudaMalloc(targets)");
+  e = cudaMalloc(&t->nu, sizeof(double) * n);
+  if (e != cudaSuccess) return release(e, "cudaMalloc(weights)");
+  e = cudaMemcpyAsync(t->y, h.data(), sizeof(double4) * n, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t->nu, nu, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return release(e, "target upload");
+  *out = t.release();
   return RSOT_CUDA_OK;
 }
 
@@ -492,27 +537,44 @@ int rsot_cuda_atoms_create(rsot_cuda_ctx* c, const double* xyz, const double* ma
   if (nq > (1u << 30)) return fail(RSOT_CUDA_INVALID_ARGUMENT, "too many atoms");
   int rc = set_device(c);
   if (rc) return rc;
+  // validation before any device allocation: finite coordinates, finite
+  // non-negative masses (every atom, from q = 0)
+  double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, msum = 0.0;
+  if (nq)
+    for (int d = 0; d < 3; ++d) lo[d] = hi[d] = xyz[d];
   std::vector<double4> h(nq);
-  for (size_t q = 0; q < nq; ++q)
+  for (size_t q = 0; q < nq; ++q) {
+    for (int d = 0; d < 3; ++d) {
+      const double v = xyz[3 * q + d];
+      if (!std::isfinite(v))
+        return fail(RSOT_CUDA_INVALID_ARGUMENT, "atom point has non-finite coordinates");
+      lo[d] = std::min(lo[d], v);
+      hi[d] = std::max(hi[d], v);
+    }
+    if (!(mass[q] >= 0.0) || !std::isfinite(mass[q]))
+      return fail(RSOT_CUDA_INVALID_ARGUMENT, "atom mass is negative or non-finite");
+    msum += mass[q];
     h[q] = make_double4(xyz[3 * q], xyz[3 * q + 1], xyz[3 * q + 2], mass[q]);
-  auto* a = new rsot_cuda_atoms();
-  if (nq) {
-    for (int d = 0; d < 3; ++d) a->cells.bbox_lo[d] = a->cells.bbox_hi[d] = xyz[d];
-    for (size_t q = 1; q < nq; ++q)
-      for (int d = 0; d < 3; ++d) {
-        const double v = xyz[3 * q + d];
-        a->cells.bbox_lo[d] = std::min(a->cells.bbox_lo[d], v);
-        a->cells.bbox_hi[d] = std::max(a->cells.bbox_hi[d], v);
-      }
+  }
+  std::unique_ptr<rsot_cuda_atoms> a(new (std::nothrow) rsot_cuda_atoms());
+  if (!a) return fail(RSOT_CUDA_RUNTIME_ERROR, "out of host memory");
+  for (int d = 0; d < 3; ++d) {
+    a->cells.bbox_lo[d] = lo[d];
+    a->cells.bbox_hi[d] = hi[d];
   }
   a->cells.bbox_set = true;
   a->ctx = c;
   a->nq = nq;
-  RSOT_CK(cudaMalloc(&a->x, sizeof(double4) * (nq ? nq : 1)));
-  if (nq)
-    RSOT_CK(cudaMemcpyAsync(a->x, h.data(), sizeof(double4) * nq, cudaMemcpyHostToDevice, c->stream));
-  RSOT_CK(cudaStreamSynchronize(c->stream));
-  *out = a;
+  a->mass_sum = msum;
+  cudaError_t e = cudaMalloc(&a->x, sizeof(double4) * (nq ? nq : 1));
+  if (e == cudaSuccess && nq)
+    e = cudaMemcpyAsync(a->x, h.data(), sizeof(double4) * nq, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    cudaFree(a->x);
+    return fail(RSOT_CUDA_RUNTIME_ERROR, std::string("atom upload: ") + cudaGetErrorString(e));
+  }
+  *out = a.release();
   return RSOT_CUDA_OK;
 }
 
@@ -520,6 +582,13 @@ int rsot_cuda_atoms_create_partitioned(rsot_cuda_ctx* c, const double* xyz, cons
                                        size_t nq, rsot_cuda_atoms** out) {
   const int rc = rsot_cuda_atoms_create(c, xyz, mass, nq, out);
   if (rc == RSOT_CUDA_OK) (*out)->partitioned = true;
+  return rc;
+}
+
+int rsot_cuda_atoms_create_local(rsot_cuda_ctx* c, const double* xyz, const double* mass, size_t nq,
+                                 rsot_cuda_atoms** out) {
+  const int rc = rsot_cuda_atoms_create(c, xyz, mass, nq, out);
+  if (rc == RSOT_CUDA_OK) (*out)->local = true;
   return rc;
 }
 
@@ -691,14 +760,78 @@ int rsot_cuda_eval_device(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_target
   return eval_common(c, a, t, nullptr, d_psi, eps, cutoff, d_g_out, d_scalars, nullptr);
 }
 
+// Debug / test entry point: one evaluation as `world` virtual ranks of a
+// multi-GPU run on this GPU.  Each virtual rank's packed partial buffer is
+// computed exactly as that rank would (partitioned atoms: its work-balanced
+// chunk range or contiguous shard) and copied into the gather buffer at the
+// rank's offset, which stands in for ncclAllGather; the rank-ordered sum and
+// the finalisation are the same launches that follow the collective in
+// enqueue_eval.
+int rsot_cuda_eval_virtual_world(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t,
+                                 const double* psi, double eps, double cutoff, int world,
+                                 double* g_out, rsot_cuda_scalars* out) {
+  int rc = check_ready(c, a, t);
+  if (rc) return rc;
+  if (!psi || !g_out || !out) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  if (world < 1 || world > 1024) return fail(RSOT_CUDA_INVALID_ARGUMENT, "bad world size");
+  if (c->comm) return fail(RSOT_CUDA_INVALID_ARGUMENT, "context has a communicator");
+  if (!a->partitioned && world > 1)
+    return fail(RSOT_CUDA_INVALID_ARGUMENT, "virtual ranks need partitioned atoms");
+  if (!(eps > 0.0)) return fail(RSOT_CUDA_INVALID_ARGUMENT, "epsilon must be > 0");
+  if (std::isnan(cutoff)) cutoff = INFINITY;
+  const DenseLaunch plan = plan_dense(static_cast<int>(a->nq), static_cast<int>(t->n), c->num_sms);
+  rc = ensure_workspace(c, a->nq, t->n, plan);
+  if (rc) return rc;
+  const size_t len = t->n + kResTail;
+  RSOT_CK(c->gathered.ensure(static_cast<size_t>(world) * len));
+  EvalBuffers b = buffers(c, nullptr, nullptr);
+  b.timing = nullptr;
+  const cudaStream_t s = c->stream;
+  RSOT_CK(cudaMemcpyAsync(b.psi, psi, sizeof(double) * t->n, cudaMemcpyHostToDevice, s));
+  const int vr = c->vrank, vw = c->vworld;
+  for (int r = 0; r < world && rc == 0; ++r) {
+    c->vrank = r;
+    c->vworld = world;
+    rc = enqueue_partial(c, a, t, b, eps, cutoff, nullptr, RSOT_CUDA_COST_SQEUCLIDEAN);
+    if (rc == 0 && cudaMemcpyAsync(c->gathered.p + static_cast<size_t>(r) * len, b.res, sizeof(double) * len,
+                                   cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      rc = fail(RSOT_CUDA_RUNTIME_ERROR, "gather copy failed");
+  }
+  c->vrank = vr;
+  c->vworld = vw;
+  if (rc) return rc;
+  launch_rank_sum(c->gathered.p, world, len, b.res, s);
+  launch_finalize(make_dt(t), b, s);
+  RSOT_CK(cudaGetLastError());
+  return finish_host_eval(c, t, g_out, out);
+}
+
+// Host mirrors of the combination kernels (the same element functions,
+// kernels.cuh), for the multi-process CPU tests of the host logic.
+void rsot_cuda_host_rank_sum(const double* gathered, int world, size_t len, double* out) {
+  for (size_t i = 0; i < len; ++i) out[i] = rank_sum_element(gathered, world, len, i);
+}
+
+void rsot_cuda_host_finalize(const double* res, const double* nu, size_t n, double psi_nu, double* g_out,
+                             double* scalars_out) {
+  for (size_t j = 0; j < n; ++j) g_out[j] = finalize_gradient_element(res, nu, j);
+  finalize_scalars(res, n, psi_nu, scalars_out);
+}
+
 int rsot_cuda_check_status(rsot_cuda_ctx* c) {
   if (!c) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null context");
   RSOT_CK(cudaSetDevice(c->device));
   RSOT_CK(cudaMemcpyAsync(c->h_pinned, c->scal.p + kSlotNonFinite, sizeof(double),
                           cudaMemcpyDeviceToHost, c->stream));
+  unsigned* ovf = reinterpret_cast<unsigned*>(c->h_pinned + 1);
+  RSOT_CK(trunc_read_overflow(ovf, c->stream));
   RSOT_CK(cudaStreamSynchronize(c->stream));
   if (c->h_pinned[0] != 0.0)
     return fail(RSOT_CUDA_INVALID_ARGUMENT, "potential has non-finite entries");
+  if (*ovf) {
+    trunc_clear_overflow();
+    return fail(RSOT_CUDA_RUNTIME_ERROR, "gradient accumulator overflow (masses far from normalised)");
+  }
   return RSOT_CUDA_OK;
 }
 
@@ -762,12 +895,41 @@ int rsot_cuda_covering_cost(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targ
                          make_dt(t), t->cells,
                          &c0, c->stream, g_last_error);
   if (rc) return fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error);
-  if (c->comm) {
+  if (c->comm && !a->local) {
     // max over ranks: all values are >= 0, so a max-allreduce is exact.
     RSOT_CK(cudaMemcpyAsync(c->scal.p, &c0, sizeof(double), cudaMemcpyHostToDevice, c->stream));
     NcclApi& api = nccl();
     const ncclResult_t r = api.AllReduce(c->scal.p, c->scal.p, 1, ncclDouble, ncclMax,
                                          c->comm, c->stream);
+    if (r != ncclSuccess)
+      return fail(RSOT_CUDA_RUNTIME_ERROR, std::string("ncclAllReduce: ") + api.GetErrorString(r));
+    RSOT_CK(cudaMemcpyAsync(c->h_pinned, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    RSOT_CK(cudaStreamSynchronize(c->stream));
+    c0 = c->h_pinned[0];
+  }
+  *out = c0;
+  return RSOT_CUDA_OK;
+}
+
+int rsot_cuda_covering_cost_kind(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda_targets* t, int cost_kind,
+                                 double* out) {
+  if (cost_kind == RSOT_CUDA_COST_SQEUCLIDEAN) return rsot_cuda_covering_cost(c, a, t, out);
+  if (cost_kind != RSOT_CUDA_COST_SQGEODESIC) return fail(RSOT_CUDA_INVALID_ARGUMENT, "unknown cost kind");
+  int rc = check_ready(c, a, t);
+  if (rc) return rc;
+  if (!out) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  if (a->nq == 0) return fail(RSOT_CUDA_INVALID_ARGUMENT, "covering cost: empty input");
+  double tstar = 0.0;
+  rc = run_geo_covering_dot(c->geo, DeviceAtoms{a->x, static_cast<int>(a->nq)}, make_dt(t), &tstar, c->stream,
+                            g_last_error);
+  if (rc) return fail(RSOT_CUDA_RUNTIME_ERROR, g_last_error);
+  // cost.hpp:24-25 on the host (the reference's libm acos), monotone in t
+  const double g = std::acos(tstar);
+  double c0 = g * g;
+  if (c->comm && !a->local) {
+    RSOT_CK(cudaMemcpyAsync(c->scal.p, &c0, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    NcclApi& api = nccl();
+    const ncclResult_t r = api.AllReduce(c->scal.p, c->scal.p, 1, ncclDouble, ncclMax, c->comm, c->stream);
     if (r != ncclSuccess)
       return fail(RSOT_CUDA_RUNTIME_ERROR, std::string("ncclAllReduce: ") + api.GetErrorString(r));
     RSOT_CK(cudaMemcpyAsync(c->h_pinned, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));

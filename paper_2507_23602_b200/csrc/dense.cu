@@ -526,14 +526,8 @@ __global__ void finalize_kernel(const double* __restrict__ res,
                                 double* __restrict__ g_out,
                                 double* __restrict__ scalars_out) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n) g_out[j] = res[j] - nu[j];
-  if (j == 0) {
-    scalars_out[kResJ] = res[n + kResJ] - scal[kSlotPsiNu];
-    scalars_out[kResD] = res[n + kResD];
-    scalars_out[kResPairs] = res[n + kResPairs];
-    scalars_out[kResEmpty] = res[n + kResEmpty];
-    scalars_out[kResVisited] = res[n + kResVisited];
-  }
+  if (j < n) g_out[j] = finalize_gradient_element(res, nu, j);
+  if (j == 0) finalize_scalars(res, n, scal[kSlotPsiNu], scalars_out);
 }
 
 __global__ void dfma_probe(double* out, double a, double b, int iters) {
@@ -679,9 +673,7 @@ __global__ void rank_sum_kernel(const double* __restrict__ gathered, int world, 
                                 double* __restrict__ out) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < len;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    double acc = gathered[i];
-    for (int r = 1; r < world; ++r) acc += gathered[r * len + i];
-    out[i] = acc;
+    out[i] = rank_sum_element(gathered, world, len, i);
   }
 }
 }  // namespace

@@ -313,7 +313,11 @@ __device__ __forceinline__ double exp2_acc_masked(double s, double acc,
   const double r = __dadd_rn(s, -kd);
   const double p = E::poly(r);
   n = take ? n : E::kZeroN;
+#ifdef RSOT_EXP_NOTABLE
+  const int2 t = make_int2(0, 0x3ff00000 - (n & (E::kTab - 1)) * E::kUnit);
+#else
   const int2 t = tbl[n & (E::kTab - 1)];
+#endif
   return fma(p, __hiloint2double(t.y + n * E::kUnit, t.x), acc);
 }
 
@@ -407,6 +411,22 @@ __device__ inline double fp_to_double(const unsigned long long* acc) {
 // phase-2 warps on their results).  Integer sums are order independent, so
 // the total is deterministic; bits below 2^-150 are dropped as in fp_add.
 constexpr int kLimbs = 5;
+// Set when a contribution cannot be represented in the accumulator (a single
+// term >= 2^41, i.e. masses far from normalised); the C ABI turns it into
+// RSOT_CUDA_RUNTIME_ERROR instead of returning a silently wrong gradient.
+static __device__ unsigned int g_fp_overflow = 0;
+
+// Limb words past the top limb fold into it (limb 4 is a u64 with 32 bits of
+// headroom: a part of value v at limb 4 + k adds v << 32 k).
+__device__ __forceinline__ void fp_red_top(unsigned long long* acc, int limb, unsigned long long v) {
+  const int k = limb - (kLimbs - 1);
+  if (k >= 2 || (k == 1 && (v >> 31))) {
+    atomicOr(&g_fp_overflow, 1u);
+    return;
+  }
+  atomicAdd(acc + kLimbs - 1, v << (32 * k));
+}
+
 __device__ __forceinline__ void fp_red(unsigned long long* acc, double m) {
   if (!(m > 0.0)) return;
   int e;
@@ -423,9 +443,15 @@ __device__ __forceinline__ void fp_red(unsigned long long* acc, double m) {
   const unsigned long long l0 = static_cast<unsigned long long>(w) & 0xffffffffull;
   const unsigned long long l1 = static_cast<unsigned long long>(w >> 32) & 0xffffffffull;
   const unsigned long long l2 = static_cast<unsigned long long>(w >> 64);
-  if (l0 && i0 < kLimbs) atomicAdd(acc + i0, l0);
-  if (l1 && i0 + 1 < kLimbs) atomicAdd(acc + i0 + 1, l1);
-  if (l2 && i0 + 2 < kLimbs) atomicAdd(acc + i0 + 2, l2);
+  if (i0 + 2 < kLimbs) {  // (every in-range contribution: m < 2^10)
+    if (l0) atomicAdd(acc + i0, l0);
+    if (l1) atomicAdd(acc + i0 + 1, l1);
+    if (l2) atomicAdd(acc + i0 + 2, l2);
+  } else {
+    if (l0) (i0 < kLimbs ? atomicAdd(acc + i0, l0) : (fp_red_top(acc, i0, l0), 0ull));
+    if (l1) (i0 + 1 < kLimbs ? atomicAdd(acc + i0 + 1, l1) : (fp_red_top(acc, i0 + 1, l1), 0ull));
+    if (l2) fp_red_top(acc, i0 + 2, l2);
+  }
 }
 
 __device__ __forceinline__ double fp_limbs_to_double(const unsigned long long* acc) {

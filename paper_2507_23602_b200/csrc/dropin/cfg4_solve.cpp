@@ -15,7 +15,15 @@
 //
 // usage: cfg4_solve <dir> [delta_tol] [max_iterations]
 //   <dir>/{coarse,fine}_{atoms,masses,targets,nu}.f64  (raw little-endian)
-// prints one JSON object.
+// prints one JSON object.  RSOT_DUMP_STAGE_PSI=<prefix> also writes the
+// (raw-gauge) potential entering every stage: <prefix>_{coarse_1e-01,
+// coarse_1e-02, fine_1e-03, fine_1e-04}.f64.
+//
+// usage: cfg4_solve <dir> --stage <level> <eps> <psi_in.f64> [delta_tol] [max_iterations]
+//   one stage alone (solve_single through rsot::solve with no scaling
+//   steps) from a given potential: per-stage evaluation rates and the
+//   behaviour of one stage, e.g. the CPU reference build (cfg4_solve_ref)
+//   from the GPU run's potential entering that stage.
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -82,12 +90,78 @@ void print_stages(const rsot::SolverReport& r, const char* name, bool last) {
 
 }  // namespace
 
+void dump_psi(const std::string& level, double eps, const std::vector<double>& psi) {
+  const char* prefix = std::getenv("RSOT_DUMP_STAGE_PSI");
+  if (!prefix) return;
+  char tag[64];
+  std::snprintf(tag, sizeof(tag), "_%s_%.0e.f64", level.c_str(), eps);
+  std::ofstream f(std::string(prefix) + tag, std::ios::binary);
+  f.write(reinterpret_cast<const char*>(psi.data()), static_cast<std::streamsize>(sizeof(double) * psi.size()));
+}
+
+// rsot::solve one epsilon at a time (the same stages as the scaling loop of
+// solve.cpp:42-60), dumping the potential entering each stage.
+std::pair<rsot::DualPotential, rsot::SolverReport> solve_staged(const rsot::SourceAtoms& a,
+                                                                const rsot::TargetMeasure& t,
+                                                                const rsot::SolverConfig& cfg,
+                                                                std::vector<double> psi,
+                                                                const std::string& level) {
+  rsot::SolverReport rep;
+  for (double eps : rsot::epsilon_schedule(cfg.epsilon, cfg.scaling_steps)) {
+    dump_psi(level, eps, psi);
+    rsot::SolverConfig st = cfg;
+    st.epsilon = eps;
+    st.scaling_steps = 0;
+    auto [p, r] = rsot::solve(a, t, st, rsot::DualPotential{psi, rsot::Gauge::Raw});
+    psi = p.values;
+    for (auto& sr : r.stages) rep.stages.push_back(std::move(sr));
+  }
+  rep.converged = rep.stages.back().status == rsot::SolveStatus::Converged;
+  return {rsot::DualPotential{std::move(psi), rsot::Gauge::Raw}, rep};
+}
+
+int run_stage(const std::string& dir, int argc, char** argv) {
+  const std::string level = argv[3];
+  const double eps = std::atof(argv[4]);
+  const std::vector<double> psi0 = read_f64(argv[5]);
+  const double tol = argc > 6 ? std::atof(argv[6]) : 1e-8;
+  const int max_it = argc > 7 ? std::atoi(argv[7]) : 1000;
+  const rsot::SourceAtoms a = atoms_of(dir, level);
+  const rsot::TargetMeasure t = targets_of(dir, level);
+  rsot::SolverConfig cfg;
+  cfg.truncation = rsot::TruncationKind::Pointwise;
+  cfg.delta_thr = 1e-12;
+  cfg.delta_tol = tol;
+  cfg.max_iterations = max_it;
+  cfg.scaling_steps = 0;
+  cfg.epsilon = eps;
+  cfg.workers = std::getenv("RSOT_WORKERS") ? std::atoi(std::getenv("RSOT_WORKERS")) : 1;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto [psi, rep] = rsot::solve(a, t, cfg, rsot::DualPotential{psi0, rsot::Gauge::Raw});
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  std::printf("{\n  \"workload\": \"cfg4 stage\", \"level\": \"%s\", \"n_atoms\": %zu, \"n_targets\": %zu, "
+              "\"workers\": %d, \"max_iterations\": %d, \"wall_ms\": %.3f, \"evals_per_s\": %.4f,\n",
+              level.c_str(), a.size(), t.size(), cfg.workers, max_it, ms,
+              rep.total_evaluations() / (ms * 1e-3));
+  print_stages(rep, "stages", true);
+  std::printf("}\n");
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc < 2) {
     std::fprintf(stderr, "usage: %s <dir> [delta_tol] [max_iterations]\n", argv[0]);
     return 2;
   }
   const std::string dir = argv[1];
+  if (argc > 5 && std::string(argv[2]) == "--stage") {
+    try {
+      return run_stage(dir, argc, argv);
+    } catch (const std::exception& e) {
+      std::fprintf(stderr, "cfg4_solve: %s\n", e.what());
+      return 1;
+    }
+  }
   const double tol = argc > 2 ? std::atof(argv[2]) : 1e-8;
   const int max_it = argc > 3 ? std::atoi(argv[3]) : 1000;
   try {
@@ -103,7 +177,7 @@ int main(int argc, char** argv) {
     cfg.workers = std::getenv("RSOT_WORKERS") ? std::atoi(std::getenv("RSOT_WORKERS")) : 1;
     const auto t0 = std::chrono::steady_clock::now();
     cfg.epsilon = 1e-2;
-    auto [psi_c, rep_c] = rsot::solve(ca, ct, cfg);
+    auto [psi_c, rep_c] = solve_staged(ca, ct, cfg, std::vector<double>(ct.size(), 0.0), "coarse");
     const auto t1 = std::chrono::steady_clock::now();
     const double last_cutoff = rep_c.stages.back().cutoff_history.back();
     const int workers = std::getenv("RSOT_WORKERS") ? std::atoi(std::getenv("RSOT_WORKERS")) : 1;
@@ -112,7 +186,7 @@ int main(int argc, char** argv) {
                                                      rsot::CostKind::SqEuclidean, last_cutoff, workers);
     const auto t2 = std::chrono::steady_clock::now();
     cfg.epsilon = 1e-4;
-    auto [psi, rep_f] = rsot::solve(fa, ft, cfg, rsot::DualPotential{psi_f, rsot::Gauge::Raw});
+    auto [psi, rep_f] = solve_staged(fa, ft, cfg, psi_f, "fine");
     const auto t3 = std::chrono::steady_clock::now();
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
     const int evals = rep_c.total_evaluations() + rep_f.total_evaluations();

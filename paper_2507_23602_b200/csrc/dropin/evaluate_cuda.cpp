@@ -6,11 +6,10 @@
 //     (evaluate.cpp:90-93, potential.hpp:42-46), then runs the evaluation on
 //     the GPU through the C ABI of include/rsot_cuda.h.  No CPU fallback:
 //     a missing/unsupported GPU throws std::runtime_error.
-//   - the host-side truncation bookkeeping that shares the translation unit
-//     in the reference (TruncationState stats, cutoff_* and
-//     refresh_truncation, evaluate.cpp:11-72), restated operation for
-//     operation because the reference L-BFGS loop (lbfgs.cpp:72,197) uses
-//     them on the host.
+// The host-side truncation bookkeeping that shares the translation unit in
+// the reference (TruncationState stats, cutoff_* and refresh_truncation,
+// evaluate.cpp:11-72) is the reference's own code: evaluate.cpp is compiled
+// unchanged with its evaluate_dual weakened (csrc/dropin/Makefile).
 // cfg.workers (a CPU thread count) is ignored; the GPU count comes from
 // rsot_cuda_context.hpp.
 #include <algorithm>
@@ -18,10 +17,13 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <future>
 #include <list>
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "rsot/evaluate.hpp"
 #include "rsot/solve.hpp"
@@ -30,100 +32,49 @@
 
 namespace rsot {
 
-// ---- evaluate.cpp:11-72 (host scalars) -------------------------------------
-
-void TruncationState::set_psi_stats(const std::vector<double>& psi) {
-  psi_max = *std::max_element(psi.begin(), psi.end());
-  psi_min = *std::min_element(psi.begin(), psi.end());
-  psi_range = psi_max - psi_min;
-}
-
-void TruncationState::set_weight_stats(const std::vector<double>& nu) {
-  nu_max = *std::max_element(nu.begin(), nu.end());
-  nu_min = *std::min_element(nu.begin(), nu.end());
-}
-
-double cutoff_pointwise(const TruncationState& trunc, double eps, double delta_thr) {
-  return trunc.psi_max + eps * std::log(trunc.nu_max / delta_thr);
-}
-
-double cutoff_integrated(const TruncationState& trunc, double eps, double tau) {
-  const double absJ = std::max(trunc.cached_absJ, 1e-30);
-  if (absJ <= 1e-30) throw std::runtime_error("functional estimate degenerate");
-  const double c = trunc.psi_max + eps * std::log(eps * trunc.cached_D / (tau * absJ));
-  return std::max(c, trunc.covering);
-}
-
-double cutoff_geometric(const TruncationState& trunc, double eps, double tau) {
-  const double absJ = std::max(trunc.cached_absJ, 1e-30);
-  if (absJ <= 1e-30) throw std::runtime_error("functional estimate degenerate");
-  const double c = trunc.covering + trunc.psi_range +
-                   eps * std::log(eps / (trunc.nu_min * tau * absJ));
-  return std::max(c, trunc.covering);
-}
-
-double cutoff_bootstrap(const TruncationState& trunc, double eps, double tau) {
-  const double c = trunc.covering + trunc.psi_range + eps * std::log(eps / (trunc.nu_min * tau));
-  return std::max(c, trunc.covering);
-}
-
-void refresh_truncation(TruncationState& trunc, const std::vector<double>& psi,
-                        const SolverConfig& cfg) {
-  trunc.set_psi_stats(psi);
-  switch (cfg.truncation) {
-    case TruncationKind::None:
-      trunc.cutoff = std::numeric_limits<double>::infinity();
-      break;
-    case TruncationKind::Pointwise:
-      trunc.cutoff = cutoff_pointwise(trunc, cfg.epsilon, cfg.delta_thr);
-      break;
-    case TruncationKind::Integrated:
-      trunc.cutoff = trunc.has_cache ? cutoff_integrated(trunc, cfg.epsilon, cfg.tau)
-                                     : cutoff_bootstrap(trunc, cfg.epsilon, cfg.tau);
-      break;
-    case TruncationKind::Geometric:
-      trunc.cutoff = trunc.has_cache ? cutoff_geometric(trunc, cfg.epsilon, cfg.tau)
-                                     : cutoff_bootstrap(trunc, cfg.epsilon, cfg.tau);
-      break;
-  }
-}
-
 // ---- device state ------------------------------------------------------------
 
 namespace cuda_detail {
 
-struct Key {
-  const void* a = nullptr;
-  const void* b = nullptr;
-  size_t n = 0;
-  uint64_t h = 0;
-  bool operator==(const Key& o) const { return a == o.a && b == o.b && n == o.n && h == o.h; }
-};
-
-// Sampled FNV-1a over up to 4096 evenly spaced (point, weight) entries.
-Key make_key(const PointList& pts, const std::vector<double>& w) {
-  Key k;
-  k.a = pts.data();
-  k.b = w.data();
-  k.n = pts.size();
-  uint64_t h = 1469598103934665603ull;
-  auto mix = [&h](const void* p, size_t bytes) {
-    const unsigned char* c = static_cast<const unsigned char*>(p);
-    for (size_t i = 0; i < bytes; ++i) h = (h ^ c[i]) * 1099511628211ull;
-  };
-  const size_t n = pts.size();
-  const size_t step = n > 4096 ? n / 4096 : 1;
-  for (size_t i = 0; i < n; i += step) {
-    mix(pts[i].data(), sizeof(double) * 3);
-    mix(&w[i], sizeof(double));
+// Device copies are reused only while the caller's arrays hold exactly the
+// uploaded values: each resident handle keeps a host shadow copy that is
+// compared in full (memcmp, parallel for large arrays) on every call, so an
+// in-place edit of any entry -- e.g. the barycenter loop's
+// `nu.points = points` into the same buffer (barycenter.cpp:55) -- uploads
+// the new values.  O(N) host bytes per call (cfg4 fine level: ~70 MB, a few
+// ms over the host cores), no sampling.
+bool same_bytes(const void* a, const void* b, size_t n) {
+  constexpr size_t kPar = size_t(8) << 20;
+  if (n < kPar) return std::memcmp(a, b, n) == 0;
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const size_t chunk = (n + hw - 1) / hw;
+  std::vector<std::future<bool>> parts;
+  for (size_t off = chunk; off < n; off += chunk) {
+    const size_t len = std::min(chunk, n - off);
+    parts.push_back(std::async(std::launch::async, [=] {
+      return std::memcmp(static_cast<const char*>(a) + off, static_cast<const char*>(b) + off, len) == 0;
+    }));
   }
-  if (n) {
-    mix(pts[n - 1].data(), sizeof(double) * 3);
-    mix(&w[n - 1], sizeof(double));
-  }
-  k.h = h;
-  return k;
+  bool eq = std::memcmp(a, b, std::min(chunk, n)) == 0;
+  for (auto& f : parts) eq = f.get() && eq;
+  return eq;
 }
+
+struct Shadow {
+  std::vector<double> x, w;  // points (3 per point), masses / weights
+  uint64_t mode = 0;         // atoms: (world, rank, local) the handle was made for
+  void assign(const PointList& p, const std::vector<double>& v, uint64_t m) {
+    x.resize(3 * p.size());
+    if (!p.empty()) std::memcpy(x.data(), p.data()->data(), sizeof(double) * x.size());
+    w = v;
+    mode = m;
+  }
+  bool matches(const PointList& p, const std::vector<double>& v, uint64_t m) const {
+    if (mode != m || x.size() != 3 * p.size() || w.size() != v.size()) return false;
+    return (p.empty() || same_bytes(x.data(), p.data()->data(), sizeof(double) * x.size())) &&
+           (v.empty() || same_bytes(w.data(), v.data(), sizeof(double) * w.size()));
+  }
+};
 
 [[noreturn]] void raise(int rc, const char* where) {
   const std::string msg = std::string(where) + ": " + rsot_cuda_last_error();
@@ -136,8 +87,8 @@ struct State {
   int device = -1;
   rsot_cuda_ctx* ctx = nullptr;
   int rank = 0, world = 1;
-  std::list<std::pair<Key, rsot_cuda_targets*>> targets;  // MRU first
-  std::list<std::pair<Key, rsot_cuda_atoms*>> atoms;
+  std::list<std::pair<Shadow, rsot_cuda_targets*>> targets;  // MRU first
+  std::list<std::pair<Shadow, rsot_cuda_atoms*>> atoms;
   static constexpr size_t kKeep = 4;
 
   int default_device() const {
@@ -165,17 +116,17 @@ struct State {
   }
 
   rsot_cuda_targets* get_targets(const TargetMeasure& t) {
-    const Key k = make_key(t.points, t.weights);
     for (auto it = targets.begin(); it != targets.end(); ++it)
-      if (it->first == k) {
+      if (it->first.matches(t.points, t.weights, 0)) {
         targets.splice(targets.begin(), targets, it);
         return targets.front().second;
       }
     rsot_cuda_targets* h = nullptr;
-    const int rc = rsot_cuda_targets_create(context(), t.points.data()->data(), t.weights.data(),
-                                            t.points.size(), &h);
+    const int rc = rsot_cuda_targets_create(context(), t.points.empty() ? nullptr : t.points.data()->data(),
+                                            t.weights.data(), t.points.size(), &h);
     if (rc) raise(rc, "rsot_cuda_targets_create");
-    targets.emplace_front(k, h);
+    targets.emplace_front(Shadow(), h);
+    targets.front().first.assign(t.points, t.weights, 0);
     while (targets.size() > kKeep) {
       rsot_cuda_targets_destroy(targets.back().second);
       targets.pop_back();
@@ -183,26 +134,26 @@ struct State {
     return h;
   }
 
+  // full = false: this rank's share of a multi-rank evaluation (partitioned
+  // handle, combined across ranks); full = true: every atom evaluated on this
+  // rank alone (PlanView, softmax_refine: a local handle, no collective).
   rsot_cuda_atoms* get_atoms(const SourceAtoms& a, bool full = false) {
-    const int world_eff = full ? 1 : world;
-    Key k = make_key(a.points, a.masses);
-    k.h ^= static_cast<uint64_t>(world_eff) * 0x9E3779B97F4A7C15ull +
-           static_cast<uint64_t>(full ? 0 : rank);
+    const uint64_t mode = full ? 1 : (static_cast<uint64_t>(world) << 33) | (static_cast<uint64_t>(rank) << 1);
     for (auto it = atoms.begin(); it != atoms.end(); ++it)
-      if (it->first == k) {
+      if (it->first.matches(a.points, a.masses, mode)) {
         atoms.splice(atoms.begin(), atoms, it);
         return atoms.front().second;
       }
-    // multi-rank: every rank holds all atoms and each evaluation takes its
-    // work-balanced share (rsot_cuda_atoms_create_partitioned)
     const size_t nq = a.points.size();
     rsot_cuda_atoms* h = nullptr;
     const double* xyz = nq ? a.points[0].data() : nullptr;
     const double* m = nq ? a.masses.data() : nullptr;
-    const int rc = world_eff > 1 ? rsot_cuda_atoms_create_partitioned(context(), xyz, m, nq, &h)
-                                 : rsot_cuda_atoms_create(context(), xyz, m, nq, &h);
+    const int rc = full ? rsot_cuda_atoms_create_local(context(), xyz, m, nq, &h)
+                        : world > 1 ? rsot_cuda_atoms_create_partitioned(context(), xyz, m, nq, &h)
+                                    : rsot_cuda_atoms_create(context(), xyz, m, nq, &h);
     if (rc) raise(rc, "rsot_cuda_atoms_create");
-    atoms.emplace_front(k, h);
+    atoms.emplace_front(Shadow(), h);
+    atoms.front().first.assign(a.points, a.masses, mode);
     while (atoms.size() > kKeep) {
       rsot_cuda_atoms_destroy(atoms.back().second);
       atoms.pop_back();
@@ -313,13 +264,14 @@ void clear_cache() {
 std::uint64_t kernel_launches() { return rsot_cuda_kernel_launches(); }
 
 // covering_cost on the GPU (spatial_index_cuda.cpp).
-double covering_cost_device(const SourceAtoms& atoms, const TargetMeasure& target) {
+double covering_cost_device(const SourceAtoms& atoms, const TargetMeasure& target, bool geodesic) {
   auto& st = cuda_detail::state();
   std::lock_guard<std::mutex> lock(st.mu);
   rsot_cuda_targets* dt = st.get_targets(target);
   rsot_cuda_atoms* da = st.get_atoms(atoms);
   double c0 = 0.0;
-  const int rc = rsot_cuda_covering_cost(st.context(), da, dt, &c0);
+  const int rc = rsot_cuda_covering_cost_kind(
+      st.context(), da, dt, geodesic ? RSOT_CUDA_COST_SQGEODESIC : RSOT_CUDA_COST_SQEUCLIDEAN, &c0);
   if (rc) cuda_detail::raise(rc, "rsot_cuda_covering_cost");
   return c0;
 }

@@ -4,8 +4,10 @@
 // unchanged) without Boost.Geometry:
 //   - evaluate_dual does not use it: its truncation query runs on the GPU
 //     cell list that lives with the resident targets (truncated.cu);
-//   - covering_cost (SqEuclidean) runs on the GPU (rsot_cuda_covering_cost,
-//     nearest by expanding cell rings, max over atoms and ranks);
+//   - covering_cost runs on the GPU for both cost kinds
+//     (rsot_cuda_covering_cost_kind: SqEuclidean by the nearest target per
+//     atom over expanding cell rings, SqGeodesicSphere by a full scan of
+//     clamped dot products; max over atoms and ranks);
 //   - the per-point host queries (ball_query / nearest / range_query) serve
 //     the reference's out-of-scope host callers (PlanView, plan.cpp:35-49;
 //     nearest_atom_density_oracle, hierarchy.cpp:68-74) from worker threads,
@@ -23,7 +25,7 @@
 namespace rsot {
 
 namespace cuda {
-double covering_cost_device(const SourceAtoms& atoms, const TargetMeasure& target);
+double covering_cost_device(const SourceAtoms& atoms, const TargetMeasure& target, bool geodesic);
 }
 
 struct SpatialIndex::Impl {
@@ -170,16 +172,9 @@ std::vector<std::size_t> range_query(const SpatialIndex& index, const Point& cen
 double covering_cost(const SourceAtoms& atoms, const TargetMeasure& target, CostKind kind) {
   if (atoms.size() == 0 || target.size() == 0)
     throw std::invalid_argument("covering cost: empty input");
-  if (kind == CostKind::SqEuclidean) return cuda::covering_cost_device(atoms, target);
-  // SqGeodesicSphere (blue-noise application, out of scope for the GPU):
-  // the reference's brute-force scan (spatial_index.cpp:113-119).
-  double c0 = 0.0;
-  for (const Point& x : atoms.points) {
-    double cmin = std::numeric_limits<double>::infinity();
-    for (const Point& y : target.points) cmin = std::min(cmin, cost(kind, x, y));
-    c0 = std::max(c0, cmin);
-  }
-  return c0;
+  // both kinds on the GPU (SqGeodesicSphere: the reference's full scan,
+  // spatial_index.cpp:113-119, as min_q max_j clamped dot + one host acos)
+  return cuda::covering_cost_device(atoms, target, kind == CostKind::SqGeodesicSphere);
 }
 
 }  // namespace rsot

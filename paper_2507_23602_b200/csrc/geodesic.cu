@@ -18,6 +18,7 @@
 //                  order (deterministic).
 //   geo_empty    : empty-set atoms add m_q to their nearest target (fixed
 //                  point, order independent).
+#include <algorithm>
 #include <cmath>
 
 #include "block_util.cuh"
@@ -235,6 +236,77 @@ int run_geodesic(GeoWorkspace& w, const DeviceAtoms& a, const DeviceTargets& t, 
     launch_det_sum(w.empty, nq, w.red + 3072, b.res + n + kResEmpty, s);
   }
   GCK(cudaGetLastError());
+  return 0;
+}
+
+namespace {
+// Thread per atom: max over all targets (tiled through shared memory) of the
+// clamped unfused dot product; block minimum over the atoms.
+__global__ void __launch_bounds__(kGT)
+geo_cover_dot(const double4* __restrict__ atoms, int nq, const double4* __restrict__ tgt, int n,
+              double* __restrict__ block_min) {
+  __shared__ double4 ty[kGTile];
+  __shared__ double red[kGT];
+  const int q = blockIdx.x * kGT + threadIdx.x;
+  const bool valid = q < nq;
+  const double4 x = valid ? atoms[q] : make_double4(0, 0, 0, 0);
+  double best = -INFINITY;
+  for (int base = 0; base < n; base += kGTile) {
+    const int ct = min(kGTile, n - base);
+    __syncthreads();
+    for (int k = threadIdx.x; k < ct; k += kGT) ty[k] = tgt[base + k];
+    __syncthreads();
+    if (!valid) continue;
+    for (int k = 0; k < ct; ++k) {
+      const double4 y = ty[k];
+      const double d = __dadd_rn(__dadd_rn(__dmul_rn(x.x, y.x), __dmul_rn(x.y, y.y)), __dmul_rn(x.z, y.z));
+      best = fmax(best, d);
+    }
+  }
+  // clamp(max) = max(clamp) (cost.hpp:22-23)
+  best = best < -1.0 ? -1.0 : (1.0 < best ? 1.0 : best);
+  red[threadIdx.x] = valid ? best : INFINITY;
+  __syncthreads();
+  for (int o = kGT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmin(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) block_min[blockIdx.x] = red[0];
+}
+
+__global__ void min_final(const double* __restrict__ v, int m, double* __restrict__ out) {
+  __shared__ double red[256];
+  double b = INFINITY;
+  for (int i = threadIdx.x; i < m; i += 256) b = fmin(b, v[i]);
+  red[threadIdx.x] = b;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmin(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+}  // namespace
+
+int run_geo_covering_dot(GeoWorkspace& w, const DeviceAtoms& a, const DeviceTargets& t, double* t_star,
+                         cudaStream_t s, std::string& err) {
+  const int blocks = (a.nq + kGT - 1) / kGT;
+  if (blocks == 0 || t.n == 0) {
+    err = "covering cost: empty input";
+    return 1;
+  }
+  if (grow(w.red, w.red_cap, std::max<size_t>(4096, static_cast<size_t>(blocks) + 1)) != cudaSuccess) {
+    err = "cudaMalloc (covering cost)";
+    return 1;
+  }
+  (note_launch(), geo_cover_dot<<<blocks, kGT, 0, s>>>(a.x, a.nq, t.y, t.n, w.red));
+  (note_launch(), min_final<<<1, 256, 0, s>>>(w.red, blocks, w.red + blocks));
+  cudaError_t e = cudaMemcpyAsync(t_star, w.red + blocks, sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    err = std::string("covering cost: ") + cudaGetErrorString(e);
+    return 1;
+  }
   return 0;
 }
 

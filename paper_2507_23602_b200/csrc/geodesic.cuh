@@ -31,4 +31,14 @@ int run_geodesic(GeoWorkspace& w, const DeviceAtoms& a, const DeviceTargets& t, 
                  uint32_t* dbg_count = nullptr, uint64_t* dbg_hash = nullptr,
                  double* dbg_log_s = nullptr);
 
+// covering_cost for SqGeodesicSphere (spatial_index.cpp:113-119,
+// c0 = max_q min_j acos(clamp(x_q . y_j))^2): the cost is a non-increasing
+// function of the clamped dot product, so min_j cost = cost(max_j clamp(dot))
+// and max_q of that = cost(min_q max_j clamp(dot)).  The device computes
+// t* = min_q max_j clamp(x_q . y_j) with the reference's unfused dot
+// (cost.hpp:19-33, exact comparisons, order independent); the caller applies
+// acos and the square on the host (the same libm call as the reference).
+int run_geo_covering_dot(GeoWorkspace& w, const DeviceAtoms& a, const DeviceTargets& t, double* t_star,
+                         cudaStream_t s, std::string& err);
+
 }  // namespace rsot_cuda

@@ -41,6 +41,27 @@ enum ResultSlot : int {
   kResTail = 5
 };
 
+// Element functions of the cross-rank combination, shared by the kernels
+// (rank_sum_kernel, finalize_kernel) and their host mirrors in the C ABI.
+// Ranks' packed partials summed in rank order (parallel.hpp:24-30 merges the
+// workers' partials in worker order): bitwise identical on every rank.
+__host__ __device__ inline double rank_sum_element(const double* gathered, int world, size_t len, size_t i) {
+  double acc = gathered[i];
+  for (int r = 1; r < world; ++r) acc += gathered[static_cast<size_t>(r) * len + i];
+  return acc;
+}
+// evaluate.cpp:157-172: g_j -= nu_j, J -= sum psi nu.
+__host__ __device__ inline double finalize_gradient_element(const double* res, const double* nu, size_t j) {
+  return res[j] - nu[j];
+}
+__host__ __device__ inline void finalize_scalars(const double* res, size_t n, double psi_nu, double* out) {
+  out[kResJ] = res[n + kResJ] - psi_nu;
+  out[kResD] = res[n + kResD];
+  out[kResPairs] = res[n + kResPairs];
+  out[kResEmpty] = res[n + kResEmpty];
+  out[kResVisited] = res[n + kResVisited];
+}
+
 struct DeviceTargets {
   const double4* y;   // {y0, y1, y2, ln nu}
   const double* nu;

@@ -640,8 +640,13 @@ __device__ __forceinline__ double exp2_pair_weighted(double sa, double sb, doubl
   const double qb = ExpTab512::poly(rb);
   na = ta ? na : ExpTab512::kZeroN;  // scale word pattern 0 -> +0.0
   nb = tb ? nb : ExpTab512::kZeroN;
+#ifdef RSOT_EXP_NOTABLE
+  const int2 Ta = make_int2(0, 0x3ff00000 - (na & 511) * ExpTab512::kUnit);
+  const int2 Tb = make_int2(0, 0x3ff00000 - (nb & 511) * ExpTab512::kUnit);
+#else
   const int2 Ta = tbl[na & (ExpTab512::kTab - 1)];
   const int2 Tb = tbl[nb & (ExpTab512::kTab - 1)];
+#endif
   const double sca = __hiloint2double(Ta.y + na * ExpTab512::kUnit, Ta.x) * wa;
   const double scb = __hiloint2double(Tb.y + nb * ExpTab512::kUnit, Tb.x) * wb;
   return fma(qa, sca, qb * scb);
@@ -1467,10 +1472,12 @@ __device__ __forceinline__ void fused_body(FusedSmem& sm, const FusedArgs& A, in
   fused_finalize<DEBUG>(A, B, wide, vb, at.cb != 0u, 0.0, at.cb, at.Sb, at.xsqb, at.qb, at.hb,
                         at.wb, 0x1p-960, primary);
 
+#ifndef RSOT_EXP_NOPHASE2
   if (safe)
     fused_scan<2, true, DEBUG, KS>(sm, A, wb, cull_thr, B, at, split);
   else
     fused_scan<2, false, DEBUG, KS>(sm, A, wb, cull_thr, B, at, split);
+#endif
   if (!DEBUG && KS == 1 && A.mbuf) {
     __syncthreads();  // every thread is done with the slot
     if (threadIdx.x == 0 && sm.mslot >= 0) {
@@ -2304,7 +2311,13 @@ GridDesc plan_grid(const double blo[3], const double bhi[3], int n, double r) {
     }
   double hmin = 1.0;
   if (active > 0) hmin = std::pow(vol / std::max(1.0, n / 2.0), 1.0 / active);
-  double h = std::max(r / cells_per_radius(), hmin);
+  // cell side ~ r / cells_per_radius on a quarter-octave ladder: the grid is
+  // a function of (bounding box, n, r) alone, so every rank of a multi-GPU
+  // run cuts the same chunk costs (chunk_scan_cost) whatever it evaluated
+  // before, and the cached grid is reused while r stays on its rung
+  double want = r / cells_per_radius();
+  if (want > 0.0 && std::isfinite(want)) want = std::exp2(std::round(4.0 * std::log2(want)) * 0.25);
+  double h = std::max(want, hmin);
   if (!(h > 0.0) || !std::isfinite(h)) h = 1.0;
   for (;;) {
     long long nc = 1;
@@ -2542,17 +2555,26 @@ static double env_double(const char* name, double dflt) {
   return end != e ? v : dflt;
 }
 
+cudaError_t trunc_read_overflow(unsigned* h_flag, cudaStream_t s) {
+  return cudaMemcpyFromSymbolAsync(h_flag, g_fp_overflow, sizeof(unsigned), 0, cudaMemcpyDeviceToHost, s);
+}
+
+cudaError_t trunc_clear_overflow() {
+  const unsigned zero = 0;
+  return cudaMemcpyToSymbol(g_fp_overflow, &zero, sizeof(unsigned));
+}
+
 static int ensure_target_cells(TruncWorkspace& ws, const DeviceTargets& t, TargetCells& tc,
                                double r, cudaStream_t s, std::string& err) {
   if (!tc.bbox_set) {
     err = "target bounding box not set";
     return 1;
   }
-  const double want = std::max(r / cells_per_radius(), tc.hmin);
-  if (tc.cell_valid && tc.g.h >= 0.75 * want && tc.g.h <= 1.35 * want) return 0;
   GridDesc g = plan_grid(tc.bbox_lo, tc.bbox_hi, t.n, r);
+  if (tc.cell_valid && tc.g.h == g.h && tc.g.dims[0] == g.dims[0] && tc.g.dims[1] == g.dims[1] &&
+      tc.g.dims[2] == g.dims[2])
+    return 0;
   g.id = g_next_grid_id++;
-  tc.hmin = plan_grid(tc.bbox_lo, tc.bbox_hi, t.n, 0.0).h;
   tc.cell_valid = false;
   if (build_cells(ws, t.y, t.n, g, tc, s, err)) return 1;
   tc.g = g;

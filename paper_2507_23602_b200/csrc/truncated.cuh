@@ -138,4 +138,10 @@ int run_covering_cost(TruncWorkspace& ws, const DeviceAtoms& a,
                       const DeviceTargets& t, TargetCells& tc, double* out,
                       cudaStream_t s, std::string& err);
 
+// Gradient accumulator overflow (fp_red: a single contribution >= 2^41):
+// enqueues a copy of the device flag into *h_flag (pinned host memory);
+// trunc_clear_overflow resets it (synchronous).
+cudaError_t trunc_read_overflow(unsigned* h_flag, cudaStream_t s);
+cudaError_t trunc_clear_overflow();
+
 }  // namespace rsot_cuda

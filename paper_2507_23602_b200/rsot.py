@@ -417,36 +417,41 @@ def build_index(points, ctx: Optional[Context] = None) -> SpatialIndex:
     return SpatialIndex(points, ctx)
 
 
+def _resident(obj, ctx: Context, arrays, extra, make):
+    """Device copy of `obj`'s arrays on `ctx`, reused only while the arrays
+    hold exactly the uploaded values: a host shadow copy is compared in full
+    (np.array_equal) on every call, so in-place edits of any entry (e.g. the
+    barycenter loop's `nu.points = points`, barycenter.cpp:55) are seen."""
+    arrays = [np.ascontiguousarray(np.asarray(a, dtype=np.float64)) for a in arrays]
+    dev = getattr(obj, "_rsot_dev", None)
+    if (dev is not None and dev[0] is ctx and dev[1] == extra and len(dev[2]) == len(arrays)
+            and all(a.shape == b.shape and np.array_equal(a, b) for a, b in zip(arrays, dev[2]))):
+        return dev[3]
+    handle = make(*arrays)
+    object.__setattr__(obj, "_rsot_dev", (ctx, extra, [a.copy() for a in arrays], handle))
+    return handle
+
+
 def _device_targets(target: TargetMeasure, ctx: Context) -> DeviceTargets:
-    key = (id(ctx), target.points.ctypes.data, target.weights.ctypes.data, target.size())
-    dev = getattr(target, "_rsot_dev", None)
-    if dev is None or dev[0] != key:
-        dev = (key, DeviceTargets(ctx, target.points, target.weights))
-        object.__setattr__(target, "_rsot_dev", dev)
-    return dev[1]
+    return _resident(target, ctx, [target.points, target.weights], (),
+                     lambda p, w: DeviceTargets(ctx, p, w))
 
 
 def _device_atoms(atoms: SourceAtoms, ctx: Context) -> DeviceAtoms:
-    key = (id(ctx), atoms.points.ctypes.data, atoms.masses.ctypes.data, atoms.size(), ctx.world,
-           getattr(ctx, "vworld", 1))
-    dev = getattr(atoms, "_rsot_dev", None)
-    if dev is None or dev[0] != key:
-        dev = (key, DeviceAtoms(ctx, atoms.points, atoms.masses))
-        object.__setattr__(atoms, "_rsot_dev", dev)
-    return dev[1]
+    return _resident(atoms, ctx, [atoms.points, atoms.masses], (ctx.world, getattr(ctx, "vworld", 1)),
+                     lambda p, m: DeviceAtoms(ctx, p, m))
 
 
 def covering_cost(atoms: SourceAtoms, target: TargetMeasure, kind: CostKind = CostKind.SqEuclidean,
                   ctx: Optional[Context] = None) -> float:
-    """spatial_index.cpp:101-121 (SqEuclidean only)."""
+    """spatial_index.cpp:101-121 on the GPU, both cost kinds."""
     if atoms.size() == 0 or target.size() == 0:
         raise ValueError("covering cost: empty input")
-    if kind != CostKind.SqEuclidean:
-        raise NotImplementedError("SqGeodesicSphere is out of scope for the B200 evaluator")
     ctx = ctx or Context.default()
     out = ctypes.c_double()
-    _lib.check(ctx.lib.rsot_cuda_covering_cost(ctx.handle, _device_atoms(atoms, ctx).handle,
-                                               _device_targets(target, ctx).handle, ctypes.byref(out)))
+    _lib.check(ctx.lib.rsot_cuda_covering_cost_kind(ctx.handle, _device_atoms(atoms, ctx).handle,
+                                                    _device_targets(target, ctx).handle, _cost_code(kind),
+                                                    ctypes.byref(out)))
     return out.value
 
 

@@ -4,8 +4,11 @@ The B200 path shards atoms contiguously (rsot_cuda_shard_range), evaluates
 each shard, all-gathers the packed partial buffers [g + nu | J + sum psi nu |
 D | pairs | empty | visited], sums them in rank order on every rank and
 finalises once.  Here the
-shard evaluation is the CPU oracle, the collective is gloo, and the
-result must equal the single-process evaluation."""
+shard evaluation is the CPU oracle, the collective is gloo, the rank-ordered
+sum and finalisation are the library's (host mirrors of rank_sum_kernel /
+finalize_kernel), and the result must equal the single-process evaluation.
+The device kernels themselves run in tests/test_gpu_parity.py
+(rsot_cuda_eval_virtual_world, W = 2, 3, 8)."""
 import math
 import os
 import socket
@@ -50,16 +53,21 @@ def _worker(rank, world, port, cutoff, q):
     t = torch.from_numpy(buf)
     parts = [torch.empty_like(t) for _ in range(world)]
     dist.all_gather(parts, t)
-    red = parts[0].numpy().copy()
-    for r in range(1, world):  # rank order, as rank_sum_kernel
-        red += parts[r].numpy()
+    # the library's rank-ordered sum and finalisation (host mirrors of
+    # rank_sum_kernel / finalize_kernel: the same element functions)
+    gathered = np.ascontiguousarray(np.concatenate([p.numpy() for p in parts]))
     n = len(W)
-    g = red[:n] - W
-    J = red[n] - psinu
+    red = np.empty(n + 5)
+    lib.rsot_cuda_host_rank_sum(gathered.ctypes.data, world, n + 5, red.ctypes.data)
+    g = np.empty(n)
+    sc = np.empty(5)
+    lib.rsot_cuda_host_finalize(red.ctypes.data, np.ascontiguousarray(W).ctypes.data, n, psinu,
+                                g.ctypes.data, sc.ctypes.data)
+    J = sc[0]
     full = C.evaluate_dual(A, M, T, W, psi, 0.02, cutoff)
     ok = (abs(J - full["J"]) <= 1e-12 * abs(full["J"]) and np.max(np.abs(g - full["gradient"])) <= 1e-14
-          and abs(red[n + 1] - full["D"]) <= 1e-12 * full["D"] and int(red[n + 2]) == full["candidate_pairs"]
-          and int(red[n + 3]) == full["empty_candidate_atoms"] and int(red[n + 4]) == len(A))
+          and abs(sc[1] - full["D"]) <= 1e-12 * full["D"] and int(sc[2]) == full["candidate_pairs"]
+          and int(sc[3]) == full["empty_candidate_atoms"] and int(sc[4]) == len(A))
     q.put((rank, bool(ok), red.tobytes()))
     dist.destroy_process_group()
 

@@ -88,7 +88,15 @@ def _check(p, psi, z, precision, tol):
     assert int(np.sum(cnt, dtype=np.uint64)) == int(z["count_sum"])
     assert int(cnt.max()) == int(z["count_max"])
     assert atom_digest(cnt, hsh) == int(z["digest"]), "per-atom (count, hash) digest differs"
-    assert res2.J == res.J and np.array_equal(res2.gradient, res.gradient)  # bitwise reproducible
+    # the debug build of the kernel (no full-in lists, no stored masks: the
+    # per-atom sums run in another order) is held to the same bar
+    got2 = dict(J=res2.J, D=res2.D, gradient=res2.gradient, atoms_visited=res2.atoms_visited,
+                candidate_pairs=res2.candidate_pairs, empty_candidate_atoms=res2.empty_candidate_atoms)
+    assert_parity(got2, want, scale, tol)
+    # bitwise reproducible run to run
+    res3 = rs.evaluate_dual(atoms, tgt, rs.DualPotential(psi), rs.SolverConfig(epsilon=p.eps),
+                            rs.TruncationState(cutoff=cut), ctx=ctx)
+    assert res3.J == res.J and np.array_equal(res3.gradient, res.gradient)
 
 
 @pytest.mark.parametrize("name", CONFIGS)

@@ -49,3 +49,22 @@ def test_geodesic_matches_oracle(ctx, n, nq, eps, cutoff):
                candidate_pairs=r.candidate_pairs, empty_candidate_atoms=r.empty_candidate_atoms)
     want = C.evaluate_dual_geodesic(A, M, T, W, psi, eps, cutoff)
     assert_parity(got, want, marginal_scale(W, want["gradient"]), 1e-10)
+
+
+@pytest.mark.parametrize("n,nq", [(1, 50), (300, 2000), (4000, 3000)])
+def test_geodesic_covering_cost_matches_reference(ctx, n, nq):
+    """covering_cost(SqGeodesicSphere) on the GPU (rsot_cuda_covering_cost_kind:
+    min_q max_j clamped unfused dot, then one host acos) equals the
+    reference's brute-force max_q min_j acos(clamp(x . y))^2
+    (spatial_index.cpp:113-119, reference build oracle/_ref) bit for bit; the
+    SqEuclidean kind through the same entry point too."""
+    from oracle.oracle import RefLib
+    rng = np.random.default_rng(900 + n)
+    A, T = sphere(rng, nq), sphere(rng, n)
+    M = np.full(nq, 1.0 / nq)
+    W = np.full(n, 1.0 / n)
+    ref = RefLib().problem(3, A, M, T, W)
+    atoms = rs.SourceAtoms(dim=3, points=A, masses=M)
+    tgt = rs.TargetMeasure(dim=3, points=T, weights=W)
+    assert rs.covering_cost(atoms, tgt, kind=rs.CostKind.SqGeodesicSphere, ctx=ctx) == ref.covering_cost(1)
+    assert rs.covering_cost(atoms, tgt, ctx=ctx) == ref.covering_cost(0)

@@ -95,6 +95,37 @@ def test_input_validation(ctx):
         rs.SpatialIndex(np.zeros((0, 3)), ctx=ctx)
 
 
+def test_handle_validation_and_mass_range(ctx):
+    """Handles are validated from the first element (a non-finite target
+    point 0 used to slip through and poison the grid's bounding box); masses
+    must be finite and >= 0.  Unnormalised masses whose single contributions
+    exceed 2^10 (they used to lose the high limb of the fixed-point gradient
+    accumulator) match the oracle; a total mass >= 2^40 is refused instead of
+    overflowing the accumulator."""
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    pts = np.array([[np.nan, 0.0, 0.0], [1.0, 0.0, 0.0]])
+    assert lib.rsot_cuda_targets_create(ctx.handle, rs.rsot._ptr(pts), rs.rsot._ptr(np.array([.5, .5])), 2,
+                                        ctypes.byref(h)) == _lib.RSOT_CUDA_INVALID_ARGUMENT
+    assert lib.rsot_cuda_atoms_create(ctx.handle, rs.rsot._ptr(pts), rs.rsot._ptr(np.array([.5, .5])), 2,
+                                      ctypes.byref(h)) == _lib.RSOT_CUDA_INVALID_ARGUMENT
+    ok = np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0]])
+    assert lib.rsot_cuda_atoms_create(ctx.handle, rs.rsot._ptr(ok), rs.rsot._ptr(np.array([.5, -.5])), 2,
+                                      ctypes.byref(h)) == _lib.RSOT_CUDA_INVALID_ARGUMENT
+    rng = np.random.default_rng(2026)
+    A, M, T, W, psi = random_instance(rng, 3, 3000, 4000)
+    eps, cutoff = 0.01, 0.02
+    for scale in (1e7, 3e9):  # atoms of mass ~ 2.5e3 .. 7.5e5 (>= 2^10)
+        want = C.evaluate_dual(A, M * scale, T, W, psi, eps, cutoff, workers=8)
+        got = gpu_eval(ctx, A, M * scale, T, W, psi, eps, cutoff)
+        assert got["candidate_pairs"] == want["candidate_pairs"]
+        assert abs(got["J"] - want["J"]) <= TOL * abs(want["J"])
+        ref = np.abs(want["gradient"] + W).max()
+        assert np.abs(got["gradient"] - want["gradient"]).max() <= TOL * ref
+    with pytest.raises(ValueError, match="2\\^40"):
+        gpu_eval(ctx, A, M * 2.0 ** 41, T, W, psi, eps, cutoff)
+
+
 def test_gradient_sums_to_zero_gauge_invariance(ctx):
     rng = np.random.default_rng(31)
     A, M, T, W, psi = random_instance(rng, 2, 12, 80)
@@ -524,6 +555,51 @@ def test_partitioned_atoms_virtual_ranks(precision):
                 ctx.set_virtual_rank(world - 1, world)
                 again = gpu_eval(ctx, A, M, T, W, psi, eps, cutoff)
                 assert again["J"] == parts[-1]["J"] and np.array_equal(again["gradient"], parts[-1]["gradient"])
+
+
+def _virtual_world_eval(ctx, A, M, T, W, psi, eps, cutoff, world):
+    lib = _lib.load()
+    dev_t = rs.rsot.DeviceTargets(ctx, T, W)
+    h = ctypes.c_void_p()  # partitioned atom handle (every rank holds every atom)
+    _lib.check(lib.rsot_cuda_atoms_create_partitioned(ctx.handle, rs.rsot._ptr(np.ascontiguousarray(A)),
+                                                      rs.rsot._ptr(np.ascontiguousarray(M)), len(A),
+                                                      ctypes.byref(h)))
+    g = np.empty(len(T))
+    sc = _lib.RsotCudaScalars()
+    try:
+        _lib.check(lib.rsot_cuda_eval_virtual_world(ctx.handle, h, dev_t.handle,
+                                                    rs.rsot._ptr(np.ascontiguousarray(psi)), eps, cutoff, world,
+                                                    rs.rsot._ptr(g), ctypes.byref(sc)))
+    finally:
+        lib.rsot_cuda_atoms_destroy(h)
+    return dict(J=sc.J, D=sc.D, gradient=g, atoms_visited=sc.atoms_visited, candidate_pairs=sc.candidate_pairs,
+                empty_candidate_atoms=sc.empty_candidate_atoms)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_virtual_world_collective_path(precision):
+    """The multi-GPU combination code on one GPU (rsot_cuda_eval_virtual_world):
+    W virtual ranks' packed partial buffers land in the gather buffer where
+    ncclAllGather would put them, then the same rank_sum_kernel +
+    finalize_kernel launches that follow the collective produce the result.
+    Dense and truncated, W = 1, 2, 3, 8: oracle parity (counters exact),
+    bitwise reproducible, and W = 1 bitwise equal to the plain evaluation."""
+    rng = np.random.default_rng(556)
+    A, M, T, W, psi = _clustered_instance(rng, nq_side=32, n=20000, background=3000)
+    tol = TOL if precision == "fp64" else 2e-5
+    ctx = rs.Context(0)
+    ctx.set_precision(precision)
+    for eps, cutoff in ((2e-3, 0.004), (0.01, math.inf)):
+        want = C.evaluate_dual(A, M, T, W, psi, eps, cutoff, workers=8)
+        plain = gpu_eval(ctx, A, M, T, W, psi, eps, cutoff)
+        for world in (1, 2, 3, 8):
+            got = _virtual_world_eval(ctx, A, M, T, W, psi, eps, cutoff, world)
+            assert got["atoms_visited"] == len(A)
+            assert_parity(got, want, marginal_scale(W, want["gradient"]), tol)
+            again = _virtual_world_eval(ctx, A, M, T, W, psi, eps, cutoff, world)
+            assert again["J"] == got["J"] and np.array_equal(again["gradient"], got["gradient"])
+            if world == 1 and precision == "fp64":
+                assert got["J"] == plain["J"] and np.array_equal(got["gradient"], plain["gradient"])
 
 
 def test_partitioned_atoms_balance():

@@ -289,6 +289,10 @@ int rsot_cuda_last_kernel_ms(rsot_cuda_ctx* ctx, double* pass_a_ms,
 uint64_t rsot_cuda_kernel_launches(void);
 /* Measured FP64 DFMA rate of the device (lane-FMAs per second). */
 int rsot_cuda_measure_fp64_peak(rsot_cuda_ctx* ctx, double* dfma_per_s);
+/* Measured FP32 FFMA rate and MUFU ex2.approx rate of the device (lane
+ * operations per second): the roofline denominators of the fp32 path. */
+int rsot_cuda_measure_fp32_peaks(rsot_cuda_ctx* ctx, double* ffma_per_s,
+                                 double* ex2_per_s);
 
 #ifdef __cplusplus
 }

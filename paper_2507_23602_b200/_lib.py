@@ -80,6 +80,7 @@ _SIGNATURES = [
     ("rsot_cuda_host_rank_sum", None, [c_void_p, c_int, c_size_t, c_void_p]),
     ("rsot_cuda_atoms_create_local", c_int, [c_void_p, c_void_p, c_void_p, c_size_t, POINTER(c_void_p)]),
     ("rsot_cuda_covering_cost_kind", c_int, [c_void_p, c_void_p, c_void_p, c_int, POINTER(c_double)]),
+    ("rsot_cuda_measure_fp32_peaks", c_int, [c_void_p, POINTER(c_double), POINTER(c_double)]),
     ("rsot_cuda_host_finalize", None, [c_void_p, c_void_p, c_size_t, c_double, c_void_p, c_void_p]),
 ]
 

@@ -1049,4 +1049,13 @@ int rsot_cuda_measure_fp64_peak(rsot_cuda_ctx* c, double* out) {
   return RSOT_CUDA_OK;
 }
 
+int rsot_cuda_measure_fp32_peaks(rsot_cuda_ctx* c, double* ffma_per_s, double* ex2_per_s) {
+  if (!c || !ffma_per_s || !ex2_per_s) return fail(RSOT_CUDA_INVALID_ARGUMENT, "null argument");
+  int rc = set_device(c);
+  if (rc) return rc;
+  measure_fp32_rates(c->stream, ffma_per_s, ex2_per_s);
+  RSOT_CK(cudaGetLastError());
+  return RSOT_CUDA_OK;
+}
+
 }  // extern "C"

@@ -688,6 +688,83 @@ void launch_finalize(const DeviceTargets& t, EvalBuffers& b, cudaStream_t s) {
                                                     b.g_out, b.scalars_out));
 }
 
+namespace {
+// FP32 pipe probe: 8 independent FFMA chains per thread, constants in
+// registers the compiler cannot fold (one register operand per FFMA).
+__global__ void ffma_probe(float* out, float a, float b, int iters) {
+  float x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fmaf(x[k], a, b);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// MUFU.EX2 probe: 8 independent ex2.approx.ftz chains (argument kept in
+// [-1, 1] by the FMA folded in front, which runs on the FP32 pipe and
+// overlaps).
+__global__ void ex2_probe(float* out, int iters) {
+  float x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = 0.01f * (threadIdx.x + k);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float y;
+      asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x[k]));
+      x[k] = y - 1.5f;
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+template <class F>
+double best_rate(cudaStream_t s, double ops_per_launch, F launch) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < 4; ++r) {
+    cudaEventRecord(e0, s);
+    launch();
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r > 0 && ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return ops_per_launch / (best * 1e-3);
+}
+}  // namespace
+
+void measure_fp32_rates(cudaStream_t s, double* ffma_per_s, double* ex2_per_s) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int threads = 256, blocks = sms * 8, iters = 16384;
+  float* out = nullptr;
+  *ffma_per_s = *ex2_per_s = 0.0;
+  if (cudaMalloc(&out, sizeof(float) * threads * blocks) != cudaSuccess) return;
+  const double ops = static_cast<double>(threads) * blocks * iters * 8;
+  *ffma_per_s = best_rate(s, ops, [&] {
+    (note_launch(), ffma_probe<<<blocks, threads, 0, s>>>(out, 0.9999f, 1e-4f, iters));
+  });
+  *ex2_per_s = best_rate(s, ops / 8, [&] {
+    (note_launch(), ex2_probe<<<blocks, threads, 0, s>>>(out, iters / 8));
+  });
+  cudaFree(out);
+}
+
 double measure_dfma_rate(cudaStream_t s) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);

@@ -135,5 +135,8 @@ void launch_dense_gather(const double4* atoms, const double* lam, int nq, const 
 
 // FP64 DFMA peak probe (roofline denominator), returns DFMA/s.
 double measure_dfma_rate(cudaStream_t s);
+// FP32 pipe (FFMA lane-ops/s) and MUFU.EX2 (lane-ops/s) probes (the fp32
+// path's roofline denominators).
+void measure_fp32_rates(cudaStream_t s, double* ffma_per_s, double* ex2_per_s);
 
 }  // namespace rsot_cuda

@@ -241,6 +241,21 @@ __device__ __forceinline__ int find_row(const int* pref, int s) {
   return lo;
 }
 
+// Row of batch position s when 8 consecutive threads hold 8 consecutive
+// positions (a kGroup of the tile map, or a run of a contiguous tile): the
+// group's first thread runs the binary search, the others step forward from
+// its row (one search per 8 entries; ncu: the per-entry searches were 3 % of
+// the fused kernel's warp samples).  All 32 lanes must call it.
+__device__ __forceinline__ int find_row_group(const int* pref, int s, bool valid) {
+  const int lane = threadIdx.x & 31;
+  int r = 0;
+  if ((lane & 7) == 0 && valid) r = find_row(pref, s);
+  r = __shfl_sync(0xffffffffu, r, lane & ~7);
+  if (valid)
+    while (pref[r + 1] <= s) ++r;
+  return r;
+}
+
 // Interleaved tiles (load balance between the CTA's warps): a row batch's
 // `total` positions form ng = ceil(total / kGroup) groups of kGroup
 // consecutive (cell-ordered, hence close) targets, and tile k holds groups
@@ -565,6 +580,7 @@ struct FusedAtoms {
   uint32_t ca, cb;           // accepted pairs per atom
   uint64_t ha, hb;           // candidate hashes (debug)
   double wa, wb;             // phase 2: m_q / S~_q (0 for empty / exact-path atoms)
+  int Fa, Fb;                // floor(512 c2 |x'|^2) (exponent-side predicate; huge for invalid atoms)
 };
 
 struct FusedArgs {
@@ -691,9 +707,12 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // (each thread its entries tid + u kT; the same thread converts them).
 __device__ __forceinline__ void fused_prefetch(FusedSmem& sm, const FusedArgs& A, const TileMap& m,
                                                int tk, int cnt) {
-  for (int t = threadIdx.x; t < cnt; t += kT) {
-    const int s = tile_pos(m, tk, t);
-    const int r = find_row(sm.rowPref, s);
+  for (int u = 0; u < (kTileT + kT - 1) / kT; ++u) {  // (uniform trip count: the row search shuffles)
+    const int t = threadIdx.x + u * kT;
+    const bool valid = t < cnt;
+    const int s = valid ? tile_pos(m, tk, t) : 0;
+    const int r = find_row_group(sm.rowPref, s, valid);
+    if (!valid) continue;
     const int k = sm.rowStart[r] + (s - sm.rowPref[r]);
     sm.rawK[t] = k;  // tK of the tile being computed is still in use
     cp_async16(&sm.rawY[t], &A.ys[k]);
@@ -719,7 +738,10 @@ __device__ __forceinline__ void fused_convert(FusedSmem& sm, const FusedArgs& A,
     const float f0 = -static_cast<float>(y0), f1 = -static_cast<float>(y1),
                 f2 = -static_cast<float>(y2);
     sm.tN0[t] = make_float4(f0, f0, f1, f1);
-    sm.tN1[t] = make_float4(f2, f2, 0.f, 0.f);
+    // floor(512 (b2_j - B - c2 r^2)): the target side of the exponent-side
+    // pair predicate (step64i), clamped far from int overflow
+    const double th = fmin(fmax(512.0 * ((sm.rawB2[t] - B) - A.c2 * A.r2), -1.0e8), 1.0e8);
+    sm.tN1[t] = make_float4(f2, f2, __int_as_float(__double2int_rd(th)), 0.f);
     sm.tJ[t] = sm.rawJ[t];
     sm.tK[t] = sm.rawK[t];
   }
@@ -1049,6 +1071,64 @@ __device__ __forceinline__ double2 step64(const FusedSmem& sm, const FusedArgs& 
                                                         mio);
 }
 
+// acc + (take ? 2^s : 0) from a precomputed magic sum kk = s + M (its low
+// word n = round(512 s) already served the pair predicate).
+__device__ __forceinline__ double exp2_acc_kk(double s, double kk, int n, double acc,
+                                              const int2* __restrict__ tbl, bool take) {
+  const double kd = __dadd_rn(kk, -ExpTab512::kMagic);
+  const double r = __dadd_rn(s, -kd);
+  const double p = ExpTab512::poly(r);
+  n = take ? n : ExpTab512::kZeroN;
+  const int2 t = tbl[n & (ExpTab512::kTab - 1)];
+  return fma(p, __hiloint2double(t.y + n * ExpTab512::kUnit, t.x), acc);
+}
+
+// Phase-1 step (2 targets x atoms a, b; non-wide CTAs) whose pair predicates
+// come from the exponent itself instead of an FP32 distance pre-test.  With
+// s = T_j + X.y' (the chain, in log2 units about the CTA origin),
+//   c2 d^2 = c2 |x'|^2 + (b2_j - B) - s, so d^2 < r^2  <=>  s > phi_q + theta_j,
+// phi_q = c2 |x'|^2, theta_j = b2_j - B - c2 r^2.  The exp2 split already has
+// n = round(512 s); with F_q = floor(512 phi_q) and T_j = floor(512 theta_j)
+// (staged), n - F_q - T_j >= 3 proves the pair in and <= -1 proves it out
+// (512 (phi + theta) lies in [F + T, F + T + 2), 512 s within 1/2 of n, and
+// every rounding of s, phi, theta and the reference's own d^2 is orders of
+// magnitude below one unit); pairs with n - F - T in {0, 1, 2} -- a band of
+// 3 / (512 c2) in d^2 -- take the exact reference predicate (fused_exact,
+// warp-uniform branch, ~5 % of the steps at cfg3 / cfg5).  Replaces the
+// packed FP32 distances, their band test and the predicate merge.
+__device__ __forceinline__ void step64i(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at, int t0,
+                                        int t1, MaskIO& mio) {
+  const double2 y0a = at16(sm.tDa, t0), y0b = at16(sm.tDb, t0);
+  const double2 y1a = at16(sm.tDa, t1), y1b = at16(sm.tDb, t1);
+  const int T0 = __float_as_int(at16(sm.tN1, t0).z), T1 = __float_as_int(at16(sm.tN1, t1).z);
+  const double4 y0 = make_double4(y0a.x, y0a.y, y0b.x, y0b.y);
+  const double4 y1 = make_double4(y1a.x, y1a.y, y1b.x, y1b.y);
+  const double sa0 = chain3(at.Xa, y0), sb0 = chain3(at.Xb, y0);
+  const double sa1 = chain3(at.Xa, y1), sb1 = chain3(at.Xb, y1);
+  const double ka0 = __dadd_rn(sa0, ExpTab512::kMagic), kb0 = __dadd_rn(sb0, ExpTab512::kMagic);
+  const double ka1 = __dadd_rn(sa1, ExpTab512::kMagic), kb1 = __dadd_rn(sb1, ExpTab512::kMagic);
+  const int na0 = __double2loint(ka0), nb0 = __double2loint(kb0);
+  const int na1 = __double2loint(ka1), nb1 = __double2loint(kb1);
+  const int da0 = na0 - at.Fa - T0, db0 = nb0 - at.Fb - T0;
+  const int da1 = na1 - at.Fa - T1, db1 = nb1 - at.Fb - T1;
+  bool k0a = da0 >= 3, k0b = db0 >= 3, k1a = da1 >= 3, k1b = db1 >= 3;
+  const unsigned border = (static_cast<unsigned>(da0) < 3u ? 1u : 0u) | (static_cast<unsigned>(db0) < 3u ? 2u : 0u) |
+                          (static_cast<unsigned>(da1) < 3u ? 4u : 0u) | (static_cast<unsigned>(db1) < 3u ? 8u : 0u);
+  if (__any_sync(0xffffffffu, border != 0u)) {
+    unsigned in = (k0a ? 1u : 0u) | (k0b ? 2u : 0u) | (k1a ? 4u : 0u) | (k1b ? 8u : 0u);
+    if (border) in = fused_exact(sm, A, at.qa, at.qb, t0 >> 4, t1 >> 4, border, in);
+    k0a = in & 1u;
+    k0b = in & 2u;
+    k1a = in & 4u;
+    k1b = in & 8u;
+  }
+  mask_put(mio, k0a, k0b, k1a, k1b);
+  at.Sa = exp2_acc_kk(sa0, ka0, na0, at.Sa, sm.tbl, k0a);
+  at.Sb = exp2_acc_kk(sb0, kb0, nb0, at.Sb, sm.tbl, k0b);
+  at.Sa = exp2_acc_kk(sa1, ka1, na1, at.Sa, sm.tbl, k1a);
+  at.Sb = exp2_acc_kk(sb1, kb1, nb1, at.Sb, sm.tbl, k1b);
+}
+
 // Phase-2 batch replaying the stored masks (word = the batch's 8 steps).
 // No guards on the steps (one basic block of 8 steps): items past nsel read
 // stale but finite staged entries (fused_body zeroes the list and staging
@@ -1156,6 +1236,11 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
   // (phase 1 always stores when the kernel has a mask buffer: CTAs without a
   // slot write a shared scratch slot, so the step loop has no branch on it)
   constexpr bool kStore = !DEBUG && KS == 1;
+#ifdef RSOT_EXP_NOINTPRED
+  constexpr bool kIntPred = false;
+#else
+  constexpr bool kIntPred = kStore && !SAFE && PHASE == 1;  // (step64i stores the masks it decides)
+#endif
   const bool mon = kStore && A.mbuf && (PHASE == 1 || (sm.mslot >= 0 && sm.mok));
   MaskIO mio;
   mio.base = A.mbuf + static_cast<size_t>(sm.mslot < 0 ? kMaskSlots : sm.mslot) * (kMaskWords + 1) * kT +
@@ -1198,7 +1283,17 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
         float2 cn = make_float2(0.f, 0.f);
         bool hit = false;
         int i = 0;
-        if (nsel >= 2) {
+        if (kIntPred && nsel >= 2) {
+          int t0 = list[0], t1 = list[1];
+          for (; i + 1 < nsel; i += 2) {
+            const int c0 = t0, c1 = t1;
+            if (i + 3 < nsel) {
+              t0 = list[i + 2];
+              t1 = list[i + 3];
+            }
+            step64i(sm, A, at, c0, c1, mio);
+          }
+        } else if (nsel >= 2) {
           int t0 = list[0], t1 = list[1];
           float2 d0 = fused_d2(sm, at, t0), d1 = fused_d2(sm, at, t1);
           for (; i + 1 < nsel; i += 2) {
@@ -1414,6 +1509,9 @@ __device__ __forceinline__ void fused_body(FusedSmem& sm, const FusedArgs& A, in
   at.Xb[0] = c2x2 * bx; at.Xb[1] = c2x2 * by; at.Xb[2] = c2x2 * bz;
   at.xsqa = A.c2 * fma(az, az, fma(ay, ay, ax * ax));
   at.xsqb = A.c2 * fma(bz, bz, fma(by, by, bx * bx));
+  // (step64i; invalid atoms get a threshold no exponent reaches)
+  at.Fa = va ? __double2int_rd(512.0 * at.xsqa) : (1 << 30);
+  at.Fb = vb ? __double2int_rd(512.0 * at.xsqb) : (1 << 30);
   const float big = 1e30f;
   at.F0 = make_float2(va ? static_cast<float>(ax) : big, vb ? static_cast<float>(bx) : big);
   at.F1 = make_float2(va ? static_cast<float>(ay) : big, vb ? static_cast<float>(by) : big);
@@ -1602,9 +1700,12 @@ __device__ __forceinline__ float butterfly16f(float (&v)[16]) {
 // Next tile's raw target data (each thread its entries tid + u kT).
 __device__ __forceinline__ void fused_prefetch32(Fused32Smem& sm, const FusedArgs& A,
                                                  const TileMap& m, int tk, int cnt) {
-  for (int t = threadIdx.x; t < cnt; t += kT) {
-    const int s = tile_pos(m, tk, t);
-    const int r = find_row(sm.rowPref, s);
+  for (int u = 0; u < (kTileT32 + kT - 1) / kT; ++u) {  // (uniform trip count: the row search shuffles)
+    const int t = threadIdx.x + u * kT;
+    const bool valid = t < cnt;
+    const int s = valid ? tile_pos(m, tk, t) : 0;
+    const int r = find_row_group(sm.rowPref, s, valid);
+    if (!valid) continue;
     const int k = sm.rowStart[r] + (s - sm.rowPref[r]);
     sm.rawK[t] = k;
     cp_async16(&sm.rawY[t], &A.ys[k]);

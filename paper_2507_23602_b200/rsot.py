@@ -312,6 +312,12 @@ class Context:
                                                      ctypes.byref(t)))
         return a.value, b.value, t.value
 
+    def fp32_rates(self):
+        """(FFMA lane-ops/s, MUFU ex2 lane-ops/s) measured on the device."""
+        a, b = ctypes.c_double(), ctypes.c_double()
+        _lib.check(self.lib.rsot_cuda_measure_fp32_peaks(self.handle, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
     def fp64_dfma_rate(self) -> float:
         v = ctypes.c_double()
         _lib.check(self.lib.rsot_cuda_measure_fp64_peak(self.handle, ctypes.byref(v)))

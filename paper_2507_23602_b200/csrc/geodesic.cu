@@ -33,10 +33,16 @@ constexpr int kGT = 128;    // threads per block
 constexpr int kGTile = 128; // staged points per tile
 
 
+// cost.hpp:19-33 dot (unfused, (p0 q0 + p1 q1) + p2 q2), clamped to [-1, 1].
+__device__ __forceinline__ double geo_clamped_dot(const double4& x, const double4& y) {
+  const double d = __dadd_rn(__dadd_rn(__dmul_rn(x.x, y.x), __dmul_rn(x.y, y.y)), __dmul_rn(x.z, y.z));
+  return d < -1.0 ? -1.0 : (1.0 < d ? 1.0 : d);
+}
+
 template <bool TRUNC>
 __global__ void __launch_bounds__(kGT)
 geo_atoms(const double4* __restrict__ atoms, int nq, const double4* __restrict__ tgt,
-          const double* __restrict__ psi, int n, double eps, double cutoff,
+          const double* __restrict__ psi, int n, double eps, double tmin,
           double* __restrict__ L_out, double* __restrict__ J_out, double* __restrict__ D_out,
           double* __restrict__ cnt_out, double* __restrict__ empty_out,
           int* __restrict__ nearest_out, uint64_t* __restrict__ hash_out) {
@@ -67,7 +73,7 @@ geo_atoms(const double4* __restrict__ atoms, int nq, const double4* __restrict__
           bd = d2;
           bj = base + t;
         }
-        if (!(c < cutoff)) continue;
+        if (!(geo_clamped_dot(x, y) >= tmin)) continue;  // == (c < cutoff) with the host's acos
       }
       const double e = __dadd_rn(__ddiv_rn(__dsub_rn(tp[t], c), eps), y.w);
       if (e > mx) {
@@ -115,7 +121,7 @@ template <bool TRUNC>
 __global__ void __launch_bounds__(kGT)
 geo_targets(const double4* __restrict__ atoms, int nq, const double* __restrict__ L,
             const int* __restrict__ nearest, const double4* __restrict__ tgt,
-            const double* __restrict__ psi, int n, double eps, double cutoff,
+            const double* __restrict__ psi, int n, double eps, double tmin,
             double* __restrict__ G) {
   __shared__ double4 ta[kGTile];
   __shared__ double tl[kGTile];
@@ -138,8 +144,8 @@ geo_targets(const double4* __restrict__ atoms, int nq, const double* __restrict_
       const double lq = tl[t];
       if (lq == INFINITY) continue;
       const double4 x = ta[t];
+      if (TRUNC && !(geo_clamped_dot(x, y) >= tmin)) continue;  // == (c < cutoff), see geo_dot_threshold
       const double c = geo_cost(x.x, x.y, x.z, y.x, y.y, y.z);
-      if (TRUNC && !(c < cutoff)) continue;
       const double e = __dadd_rn(__ddiv_rn(__dsub_rn(pj, c), eps), y.w);
       g = fma(exp(e - lq), x.w, g);
     }
@@ -189,11 +195,40 @@ void GeoWorkspace::release() {
     }                                                              \
   } while (0)
 
+// Exact candidate selection without the device's acos: the reference keeps
+// a pair iff fl(acos(t))^2 < cutoff with t the clamped dot (cost.hpp:19-33,
+// evaluate.cpp:124-128), a non-increasing function of t (libm's acos is
+// monotone, squaring on [0, pi] too), so the kept set is {t >= t_min} with
+// t_min the smallest double in [-1, 1] that passes -- found here by bisection
+// with the host's own acos (the reference's libm call).  The device compares
+// the clamped dot with t_min: selection bit for bit as the reference, even
+// where libdevice's acos and glibc's differ in the last ulp.  -inf: every
+// pair passes; +inf: none.
+double geo_dot_threshold(double cutoff) {
+  auto pass = [cutoff](double t) {
+    const double g = std::acos(t);
+    return g * g < cutoff;
+  };
+  if (!pass(1.0)) return INFINITY;
+  if (pass(-1.0)) return -INFINITY;
+  double lo = -1.0, hi = 1.0;  // pass(lo) false, pass(hi) true
+  for (;;) {
+    double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) {  // adjacent doubles
+      mid = std::nextafter(lo, hi);
+      if (mid >= hi) break;
+    }
+    if (pass(mid)) hi = mid; else lo = mid;
+  }
+  return hi;
+}
+
 int run_geodesic(GeoWorkspace& w, const DeviceAtoms& a, const DeviceTargets& t, EvalBuffers& b,
                  double eps, double cutoff, cudaStream_t s, std::string& err,
                  uint32_t* dbg_count, uint64_t* dbg_hash, double* dbg_log_s) {
   const int nq = a.nq, n = t.n;
   const bool trunc = std::isfinite(cutoff);
+  const double tmin = trunc ? geo_dot_threshold(cutoff) : -INFINITY;
   GCK(grow(w.L, w.atom_cap_L, nq));
   GCK(grow(w.J, w.atom_cap_J, nq));
   GCK(grow(w.D, w.atom_cap_D, nq));
@@ -209,10 +244,10 @@ int run_geodesic(GeoWorkspace& w, const DeviceAtoms& a, const DeviceTargets& t, 
     const int ga = (nq + kGT - 1) / kGT, gt = (n + kGT - 1) / kGT;
     if (b.timing) cudaEventRecord(b.timing[1], s);
     if (trunc)
-      (note_launch(), geo_atoms<true><<<ga, kGT, 0, s>>>(a.x, nq, t.y, b.psi, n, eps, cutoff, w.L, w.J,
+      (note_launch(), geo_atoms<true><<<ga, kGT, 0, s>>>(a.x, nq, t.y, b.psi, n, eps, tmin, w.L, w.J,
                                                          w.D, w.cnt, w.empty, w.nearest, dbg_hash));
     else
-      (note_launch(), geo_atoms<false><<<ga, kGT, 0, s>>>(a.x, nq, t.y, b.psi, n, eps, cutoff, w.L, w.J,
+      (note_launch(), geo_atoms<false><<<ga, kGT, 0, s>>>(a.x, nq, t.y, b.psi, n, eps, tmin, w.L, w.J,
                                                           w.D, w.cnt, w.empty, w.nearest, dbg_hash));
     if (dbg_count || dbg_log_s)
       (note_launch(), geo_debug<<<(nq + 255) / 256, 256, 0, s>>>(w.L, w.cnt, nq, dbg_count, dbg_log_s));
@@ -222,10 +257,10 @@ int run_geodesic(GeoWorkspace& w, const DeviceAtoms& a, const DeviceTargets& t, 
     }
     if (trunc)
       (note_launch(), geo_targets<true><<<gt, kGT, 0, s>>>(a.x, nq, w.L, w.nearest, t.y, b.psi, n, eps,
-                                                           cutoff, w.G));
+                                                           tmin, w.G));
     else
       (note_launch(), geo_targets<false><<<gt, kGT, 0, s>>>(a.x, nq, w.L, w.nearest, t.y, b.psi, n, eps,
-                                                            cutoff, w.G));
+                                                            tmin, w.G));
     if (b.timing) cudaEventRecord(b.timing[4], s);
     (note_launch(), geo_empty<<<(nq + 255) / 256, 256, 0, s>>>(a.x, w.nearest, nq, w.gacc));
     (note_launch(), geo_assemble<<<(n + 255) / 256, 256, 0, s>>>(w.G, w.gacc, n, static_cast<double>(nq),

@@ -38,6 +38,11 @@ int run_geodesic(GeoWorkspace& w, const DeviceAtoms& a, const DeviceTargets& t, 
 // t* = min_q max_j clamp(x_q . y_j) with the reference's unfused dot
 // (cost.hpp:19-33, exact comparisons, order independent); the caller applies
 // acos and the square on the host (the same libm call as the reference).
+// Smallest clamped dot product t with fl(acos(t))^2 < cutoff under the
+// host's libm (the reference's predicate is monotone in t): -inf when every
+// t passes, +inf when none does.
+double geo_dot_threshold(double cutoff);
+
 int run_geo_covering_dot(GeoWorkspace& w, const DeviceAtoms& a, const DeviceTargets& t, double* t_star,
                          cudaStream_t s, std::string& err);
 

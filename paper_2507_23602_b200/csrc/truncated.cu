@@ -32,6 +32,7 @@
 
 #include "block_util.cuh"
 #include "device_math.cuh"
+#include "geodesic.cuh"
 #include "truncated.cuh"
 
 namespace rsot_cuda {
@@ -1585,8 +1586,11 @@ __device__ __forceinline__ void fused_body(FusedSmem& sm, const FusedArgs& A, in
   }
 }
 
+#ifndef RSOT_FUSED_MIN_BLOCKS
+#define RSOT_FUSED_MIN_BLOCKS 4
+#endif
 template <bool DEBUG>
-__global__ void __launch_bounds__(kT, 4)
+__global__ void __launch_bounds__(kT, RSOT_FUSED_MIN_BLOCKS)
 trunc_fused(FusedArgs A) {
   __shared__ FusedSmem sm;
   int chunk = static_cast<int>(blockIdx.x);
@@ -2495,9 +2499,11 @@ __global__ void plan_fill_kernel(const double4* __restrict__ xs, int nq,
 }
 
 // Geodesic cost: full scan {j : c < cutoff} in index order (evaluate.cpp /
-// plan.cpp full-scan branch), Euclidean nearest when empty.
+// plan.cpp full-scan branch) decided as clamped dot >= tmin
+// (geo_dot_threshold: the reference's acos on the host), Euclidean nearest
+// when empty.
 __global__ void plan_fill_geo_kernel(const double4* __restrict__ xs, int nq,
-                                     const double4* __restrict__ yo, int n, double cutoff,
+                                     const double4* __restrict__ yo, int n, double tmin,
                                      const double4* __restrict__ ys, const int* __restrict__ tperm,
                                      const int* __restrict__ cell_start, GridDev g,
                                      const unsigned long long* __restrict__ off,
@@ -2515,7 +2521,8 @@ __global__ void plan_fill_geo_kernel(const double4* __restrict__ xs, int nq,
       bool in = false;
       if (k < n) {
         const double4 y = yo[k];
-        in = geo_cost(x.x, x.y, x.z, y.x, y.y, y.z) < cutoff;
+        const double d = __dadd_rn(__dadd_rn(__dmul_rn(x.x, y.x), __dmul_rn(x.y, y.y)), __dmul_rn(x.z, y.z));
+        in = (d < -1.0 ? -1.0 : (1.0 < d ? 1.0 : d)) >= tmin;
       }
       const unsigned m = __ballot_sync(0xffffffffu, in);
       if (in) idx[base + pos + __popc(m & lt)] = static_cast<unsigned long long>(k);
@@ -2999,7 +3006,8 @@ int run_plan_candidates(TruncWorkspace& ws, const DeviceAtoms& a, const DeviceTa
   TCK(cudaMemsetAsync(bad, 0, sizeof(int), s));
   if (geo)
     (note_launch(), plan_fill_geo_kernel<<<std::min(8192, (nq + 7) / 8), 256, 0, s>>>(
-        a.x, nq, t.y, t.n, cutoff, tc.pc, tc.perm_c, tc.cell_start, to_dev(tc.g), off, idx, bad));
+        a.x, nq, t.y, t.n, std::isfinite(cutoff) ? geo_dot_threshold(cutoff) : -INFINITY, tc.pc, tc.perm_c,
+        tc.cell_start, to_dev(tc.g), off, idx, bad));
   else
     (note_launch(), plan_fill_kernel<<<std::min(8192, (nq + 7) / 8), 256, 0, s>>>(
         a.x, nq, tc.pc, tc.perm_c, tc.cell_start, to_dev(tc.g), r2, r_scan, scan ? 1 : 0, off, idx,

@@ -545,6 +545,11 @@ constexpr int kFA = 2 * kT;  // atoms per CTA
 // in phase 2; slot kMaskSlots is the shared scratch of CTAs without a slot.
 constexpr int kMaskSlots = 1024;
 constexpr int kMaskWords = 2048;
+// Word-major pool: word w of every slot (and of every thread of a slot) is
+// contiguous, so the words in use -- a few dozen per thread at cfg5 -- form
+// one compact region at the start of the pool that the L2 can hold (see
+// mask_l2_window) instead of 1024 scattered 1 MB slots.
+constexpr size_t kMaskWordStride = static_cast<size_t>(kMaskSlots + 1) * kT;
 
 struct FusedSmem {
   // 16-byte strided arrays: the culled lists hold byte offsets t << 4, so
@@ -1009,7 +1014,7 @@ struct MaskIO {
   uint32_t w;
 };
 __device__ __forceinline__ void mask_store(MaskIO& m) {
-  m.base[static_cast<size_t>(min(m.widx, m.cap)) * kT] = m.w;  // (overflow: scratch word)
+  m.base[static_cast<size_t>(min(m.widx, m.cap)) * kMaskWordStride] = m.w;  // (overflow: scratch word)
   m.ca += __popc(m.w & 0x55555555u);  // (bits 4s, 4s + 2: atom a; 4s + 1, 4s + 3: atom b)
   m.cb += __popc(m.w & 0xAAAAAAAAu);
   if (m.widx >= m.cap) *m.ok = 0;
@@ -1244,8 +1249,7 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
 #endif
   const bool mon = kStore && A.mbuf && (PHASE == 1 || (sm.mslot >= 0 && sm.mok));
   MaskIO mio;
-  mio.base = A.mbuf + static_cast<size_t>(sm.mslot < 0 ? kMaskSlots : sm.mslot) * (kMaskWords + 1) * kT +
-             threadIdx.x;
+  mio.base = A.mbuf + static_cast<size_t>(sm.mslot < 0 ? kMaskSlots : sm.mslot) * kT + threadIdx.x;
   mio.ok = &sm.mok;
   mio.cap = A.mwords;
   mio.ca = mio.cb = 0u;
@@ -1329,11 +1333,11 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
         // (a band-free second instantiation, as in fused_scan32, costs more in
         // instruction-cache misses than it saves here: measured +6 %)
         if (mon) {  // one word per batch of 8 steps (the next one prefetched)
-          uint32_t nw = mio.base[static_cast<size_t>(mio.widx) * kT];
+          uint32_t nw = mio.base[static_cast<size_t>(mio.widx) * kMaskWordStride];
           for (int b0 = 0; b0 < nsel; b0 += 16) {
             const uint32_t mw = nw;
             ++mio.widx;
-            nw = mio.base[static_cast<size_t>(mio.widx) * kT];
+            nw = mio.base[static_cast<size_t>(mio.widx) * kMaskWordStride];
             batch64_masked<SAFE>(sm, at, wide, list, b0, nsel, mw, col);
           }
         } else {
@@ -2672,6 +2676,35 @@ cudaError_t trunc_clear_overflow() {
   return cudaMemcpyToSymbol(g_fp_overflow, &zero, sizeof(unsigned));
 }
 
+// Keeps the mask pool's leading words resident in L2 (access-policy window,
+// persisting): phase 1 writes them and phase 2 of the same CTA reads them
+// back milliseconds later, while the streamed atoms and targets would
+// otherwise evict them to DRAM (round-1 ncu: ~2.6 GB of the 4.3 GB per cfg5
+// evaluation).  RSOT_CUDA_L2_PERSIST=0 disables it.  Best effort: errors
+// only leave the pool uncached-preferred.
+static void mask_l2_window(TruncWorkspace& ws, cudaStream_t s) {
+  if (env_double("RSOT_CUDA_L2_PERSIST", 1.0) == 0.0) return;
+  int dev = 0, max_persist = 0, max_win = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+  cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+  const size_t want = static_cast<size_t>(64) << 20;  // ~120 words of every slot
+  const size_t win = std::min<size_t>({want, static_cast<size_t>(max_persist), static_cast<size_t>(max_win)});
+  if (win == 0) return;
+  size_t cur = 0;
+  cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+  if (cur < win) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, win);
+  cudaStreamAttrValue v = {};
+  v.accessPolicyWindow.base_ptr = ws.mbuf;
+  v.accessPolicyWindow.num_bytes = win;
+  v.accessPolicyWindow.hitRatio = 1.0f;
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
+  if (ws.side) cudaStreamSetAttribute(ws.side, cudaStreamAttributeAccessPolicyWindow, &v);
+  cudaGetLastError();  // (best effort)
+}
+
 static int ensure_target_cells(TruncWorkspace& ws, const DeviceTargets& t, TargetCells& tc,
                                double r, cudaStream_t s, std::string& err) {
   if (!tc.bbox_set) {
@@ -2803,6 +2836,7 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
     if (!fp32 && !dbg) {
       if (!ws.mbuf) {
         TCK(cudaMalloc(&ws.mbuf, sizeof(uint32_t) * (static_cast<size_t>(kMaskSlots) + 1) * (kMaskWords + 1) * kT));
+        mask_l2_window(ws, s);
         TCK(cudaMalloc(&ws.mbusy, sizeof(int) * kMaskSlots));
         TCK(cudaMalloc(&ws.mticket, sizeof(unsigned)));
         TCK(cudaMemsetAsync(ws.mbusy, 0, sizeof(int) * kMaskSlots, s));

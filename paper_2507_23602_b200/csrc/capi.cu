@@ -809,11 +809,13 @@ int rsot_cuda_eval_virtual_world(rsot_cuda_ctx* c, rsot_cuda_atoms* a, rsot_cuda
 // Host mirrors of the combination kernels (the same element functions,
 // kernels.cuh), for the multi-process CPU tests of the host logic.
 void rsot_cuda_host_rank_sum(const double* gathered, int world, size_t len, double* out) {
+  if (!gathered || !out || world < 1) return;
   for (size_t i = 0; i < len; ++i) out[i] = rank_sum_element(gathered, world, len, i);
 }
 
 void rsot_cuda_host_finalize(const double* res, const double* nu, size_t n, double psi_nu, double* g_out,
                              double* scalars_out) {
+  if (!res || !nu || !g_out || !scalars_out) return;
   for (size_t j = 0; j < n; ++j) g_out[j] = finalize_gradient_element(res, nu, j);
   finalize_scalars(res, n, psi_nu, scalars_out);
 }

@@ -14,6 +14,7 @@
 // rsot_cuda_context.hpp.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -256,6 +257,20 @@ EvalResult evaluate_dual(const SourceAtoms& atoms, const TargetMeasure& target,
   result.atoms_visited = sc.atoms_visited;
   result.candidate_pairs = sc.candidate_pairs;
   result.empty_candidate_atoms = sc.empty_candidate_atoms;
+  // RSOT_CUDA_EVAL_LOG=1: one line per evaluation on stderr (the same format
+  // as the reference build's oracle/eval_progress.cpp, for trajectory
+  // comparisons of a solve)
+  static const bool log = [] {
+    const char* e = std::getenv("RSOT_CUDA_EVAL_LOG");
+    return e && *e && *e != '0';
+  }();
+  if (log) {
+    static int count = 0;
+    double l1 = 0.0;
+    for (double g : result.gradient) l1 += std::fabs(g);
+    std::fprintf(stderr, "eval %d eps %.1e  J %.17g  |g|_1 %.6e  pairs %llu  cutoff %.6e\n", ++count, cfg.epsilon,
+                 result.J, l1, static_cast<unsigned long long>(result.candidate_pairs), trunc.cutoff);
+  }
   return result;
 }
 

@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -42,6 +43,9 @@ namespace {
 constexpr int kT = 128;        // threads per CTA = points per chunk
 constexpr int kTileT = 256;    // staged points per tile (fp64 kernel)
 constexpr int kTileT32 = 384;  // staged points per tile (fp32 kernel)
+#ifndef RSOT_P1_LEAN
+#define RSOT_P1_LEAN 1
+#endif
 using ListT = unsigned short;  // per-warp culled-list entry (tile index)
 constexpr int kMortonBits = 7; // per dim, position inside a cell
 double g_cells_per_radius = 5.0;  // grid cell side ~ r / 5 (env RSOT_CELLS_PER_RADIUS; swept 2-8: r/5-r/6 best
@@ -1135,6 +1139,97 @@ __device__ __forceinline__ void step64i(const FusedSmem& sm, const FusedArgs& A,
   at.Sb = exp2_acc_kk(sb1, kb1, nb1, at.Sb, sm.tbl, k1b);
 }
 
+// Shared-memory loads at a register address plus a compile-time offset (the
+// staged arrays of FusedSmem lie at fixed distances from tDa): one LDS each,
+// no per-load address arithmetic.
+template <int OFF>
+__device__ __forceinline__ double2 lds_d2(unsigned addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+%3];" : "=d"(v.x), "=d"(v.y) : "r"(addr), "n"(OFF));
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ int lds_i(unsigned addr) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(OFF));
+  return v;
+}
+__device__ __forceinline__ int2 lds_i2(unsigned addr) {
+  int2 v;
+  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+// Shared address of table entry n & 511 (AND, then one shift-add).
+__device__ __forceinline__ unsigned tbl_addr(unsigned tbl, int n) {
+  unsigned a;
+  asm("{\n\t.reg .b32 t;\n\tand.b32 t, %1, 511;\n\tshl.b32 t, t, 3;\n\tadd.u32 %0, t, %2;\n\t}"
+      : "=r"(a) : "r"(n), "r"(tbl));
+  return a;
+}
+// acc + (take ? 2^s : 0) from the magic sum kk = s + M (n = its low word).
+__device__ __forceinline__ double exp2_acc_x(double s, double kk, int n, double acc, unsigned tbl, bool take) {
+  const double kd = __dadd_rn(kk, -ExpTab512::kMagic);
+  const double r = __dadd_rn(s, -kd);
+  const double p = ExpTab512::poly(r);
+  n = take ? n : ExpTab512::kZeroN;
+  const int2 t = lds_i2(tbl_addr(tbl, n));
+  return fma(p, __hiloint2double(t.y + n * ExpTab512::kUnit, t.x), acc);
+}
+__device__ __forceinline__ int exact_x(const FusedSmem& sm, const FusedArgs& A, int q, int t) {
+  const double4 yg = A.ys[sm.tK[t]];
+  const double4 x = A.xs[q];
+  return exact_inside(x.x, x.y, x.z, yg.x, yg.y, yg.z, A.r2) ? -1 : 3;
+}
+
+// step64i with the decisions kept as integers: x = F_q + 2 + T_j - n is
+// negative for a pair proven in, >= 3 for one proven out, and 0..2 inside the
+// band that takes the exact predicate (which then rewrites x to -1 or 3).
+// The step's mask bits are the sign bits of the four x, shifted into the
+// mask word by funnel shifts, and the accumulation is predicated on x < 0:
+// no boolean merges, selects or byte permutes in the step.
+// sb: shared address of sm.tDa[0]; o0, o1: byte offsets (t << 4).
+__device__ __forceinline__ void step64x(const FusedSmem& sm, const FusedArgs& A, FusedAtoms& at,
+                                        unsigned sb, unsigned tbl, int o0, int o1, MaskIO& mio) {
+  constexpr int kDb = offsetof(FusedSmem, tDb) - offsetof(FusedSmem, tDa);
+  constexpr int kN1 = offsetof(FusedSmem, tN1) - offsetof(FusedSmem, tDa) + 8;  // tN1[t].z
+  const unsigned a0 = sb + o0, a1 = sb + o1;
+  const double2 y0a = lds_d2<0>(a0), y0b = lds_d2<kDb>(a0);
+  const double2 y1a = lds_d2<0>(a1), y1b = lds_d2<kDb>(a1);
+  const int T0 = lds_i<kN1>(a0), T1 = lds_i<kN1>(a1);
+  const double4 y0 = make_double4(y0a.x, y0a.y, y0b.x, y0b.y);
+  const double4 y1 = make_double4(y1a.x, y1a.y, y1b.x, y1b.y);
+  const double sa0 = chain3(at.Xa, y0), sb0 = chain3(at.Xb, y0);
+  const double sa1 = chain3(at.Xa, y1), sb1 = chain3(at.Xb, y1);
+  const double ka0 = __dadd_rn(sa0, ExpTab512::kMagic), kb0 = __dadd_rn(sb0, ExpTab512::kMagic);
+  const double ka1 = __dadd_rn(sa1, ExpTab512::kMagic), kb1 = __dadd_rn(sb1, ExpTab512::kMagic);
+  const int na0 = __double2loint(ka0), nb0 = __double2loint(kb0);
+  const int na1 = __double2loint(ka1), nb1 = __double2loint(kb1);
+  // (at.Fa, at.Fb hold F + 2 here)
+  int xa0 = at.Fa + T0 - na0, xb0 = at.Fb + T0 - nb0;
+  int xa1 = at.Fa + T1 - na1, xb1 = at.Fb + T1 - nb1;
+  const unsigned lowest = min(__vimin3_u32(static_cast<unsigned>(xa0), static_cast<unsigned>(xb0),
+                                           static_cast<unsigned>(xa1)), static_cast<unsigned>(xb1));
+  if (__any_sync(0xffffffffu, lowest < 3u)) {
+    if (static_cast<unsigned>(xa0) < 3u) xa0 = exact_x(sm, A, at.qa, o0 >> 4);
+    if (static_cast<unsigned>(xb0) < 3u) xb0 = exact_x(sm, A, at.qb, o0 >> 4);
+    if (static_cast<unsigned>(xa1) < 3u) xa1 = exact_x(sm, A, at.qa, o1 >> 4);
+    if (static_cast<unsigned>(xb1) < 3u) xb1 = exact_x(sm, A, at.qb, o1 >> 4);
+  }
+  // nibble layout of mask_put: bit 0 = (t0, a), 1 = (t0, b), 2 = (t1, a), 3 = (t1, b)
+  uint32_t w = mio.w;
+  w = __funnelshift_l(static_cast<unsigned>(xb1), w, 1);
+  w = __funnelshift_l(static_cast<unsigned>(xa1), w, 1);
+  w = __funnelshift_l(static_cast<unsigned>(xb0), w, 1);
+  w = __funnelshift_l(static_cast<unsigned>(xa0), w, 1);
+  // (the four predicates from the nibble just shifted in: one R2P)
+  at.Sa = exp2_acc_x(sa0, ka0, na0, at.Sa, tbl, w & 1u);
+  at.Sb = exp2_acc_x(sb0, kb0, nb0, at.Sb, tbl, w & 2u);
+  at.Sa = exp2_acc_x(sa1, ka1, na1, at.Sa, tbl, w & 4u);
+  at.Sb = exp2_acc_x(sb1, kb1, nb1, at.Sb, tbl, w & 8u);
+  mio.w = w;
+  if (++mio.n == 8) mask_store(mio);
+}
+
 // Phase-2 batch replaying the stored masks (word = the batch's 8 steps).
 // No guards on the steps (one basic block of 8 steps): items past nsel read
 // stale but finite staged entries (fused_body zeroes the list and staging
@@ -1290,14 +1385,28 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
         int i = 0;
         if (kIntPred && nsel >= 2) {
           int t0 = list[0], t1 = list[1];
+#if RSOT_P1_LEAN
+          const unsigned sb = static_cast<unsigned>(__cvta_generic_to_shared(&sm.tDa[0]));
+          const unsigned tb = static_cast<unsigned>(__cvta_generic_to_shared(&sm.tbl[0]));
+          at.Fa += 2;  // (step64x: x = F + 2 + T - n)
+          at.Fb += 2;
+#endif
           for (; i + 1 < nsel; i += 2) {
             const int c0 = t0, c1 = t1;
             if (i + 3 < nsel) {
               t0 = list[i + 2];
               t1 = list[i + 3];
             }
+#if RSOT_P1_LEAN
+            step64x(sm, A, at, sb, tb, c0, c1, mio);
+#else
             step64i(sm, A, at, c0, c1, mio);
+#endif
           }
+#if RSOT_P1_LEAN
+          at.Fa -= 2;
+          at.Fb -= 2;
+#endif
         } else if (nsel >= 2) {
           int t0 = list[0], t1 = list[1];
           float2 d0 = fused_d2(sm, at, t0), d1 = fused_d2(sm, at, t1);

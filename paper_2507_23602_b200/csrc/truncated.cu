@@ -43,6 +43,9 @@ namespace {
 constexpr int kT = 128;        // threads per CTA = points per chunk
 constexpr int kTileT = 256;    // staged points per tile (fp64 kernel)
 constexpr int kTileT32 = 384;  // staged points per tile (fp32 kernel)
+#ifndef RSOT_FULLIN_RATIO2
+#define RSOT_FULLIN_RATIO2 49.0f  // full-in split when r > 7 warp-box half-diagonals
+#endif
 #ifndef RSOT_P1_LEAN
 #define RSOT_P1_LEAN 1
 #endif
@@ -549,6 +552,7 @@ constexpr int kFA = 2 * kT;  // atoms per CTA
 // in phase 2; slot kMaskSlots is the shared scratch of CTAs without a slot.
 constexpr int kMaskSlots = 1024;
 constexpr int kMaskWords = 2048;
+constexpr int kSlotsPerSm = 4;  // (>= resident trunc_fused CTAs per SM)
 // Word-major pool: word w of every slot (and of every thread of a slot) is
 // contiguous, so the words in use -- a few dozen per thread at cfg5 -- form
 // one compact region at the start of the pool that the L2 can hold (see
@@ -1210,6 +1214,7 @@ __device__ __forceinline__ void step64x(const FusedSmem& sm, const FusedArgs& A,
   const unsigned lowest = min(__vimin3_u32(static_cast<unsigned>(xa0), static_cast<unsigned>(xb0),
                                            static_cast<unsigned>(xa1)), static_cast<unsigned>(xb1));
   if (__any_sync(0xffffffffu, lowest < 3u)) {
+    // (inline: the same fix-up as an out-of-line call measured +2.6 % at cfg5)
     if (static_cast<unsigned>(xa0) < 3u) xa0 = exact_x(sm, A, at.qa, o0 >> 4);
     if (static_cast<unsigned>(xb0) < 3u) xb0 = exact_x(sm, A, at.qb, o0 >> 4);
     if (static_cast<unsigned>(xa1) < 3u) xa1 = exact_x(sm, A, at.qa, o1 >> 4);
@@ -1325,7 +1330,7 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
   if (!DEBUG && at.lo_thr > 0.f) {
     const float hx = wb.hi0 - wb.lo0, hy = wb.hi1 - wb.lo1, hz = wb.hi2 - wb.lo2;
     const float hd2 = 0.25f * fmaf(hz, hz, fmaf(hy, hy, hx * hx));
-    if (at.lo_thr > 49.0f * hd2) full_thr = at.lo_thr * (1.0f - 1e-5f);
+    if (at.lo_thr > RSOT_FULLIN_RATIO2 * hd2) full_thr = at.lo_thr * (1.0f - 1e-5f);
   }
   const ListT* const full = list + (kTileT - 1);  // full-in items: full[-i]
   const bool va = at.qa < A.nq, vb = at.qb < A.nq;
@@ -1392,11 +1397,19 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
           at.Fb += 2;
 #endif
           for (; i + 1 < nsel; i += 2) {
+#ifdef RSOT_P1_NOPIPE
+            const int c0 = list[i], c1 = list[i + 1];
+#else
             const int c0 = t0, c1 = t1;
+#ifdef RSOT_P1_NOGUARD
+            {  // (reads up to two entries past the list end: other list entries, unused)
+#else
             if (i + 3 < nsel) {
+#endif
               t0 = list[i + 2];
               t1 = list[i + 3];
             }
+#endif
 #if RSOT_P1_LEAN
             step64x(sm, A, at, sb, tb, c0, c1, mio);
 #else
@@ -1597,16 +1610,33 @@ __device__ __forceinline__ void fused_body(FusedSmem& sm, const FusedArgs& A, in
     setup_region(A.g, lo, hi, A.r2, A.r_scan, A.c2, sm.sh, R);
     if (threadIdx.x == 0) {
       sm.R = R;
-      // a mask slot for phase 2 (linear probing from a ticket: more slots
-      // than resident CTAs, so the search always ends)
+      // a mask slot for phase 2: slots kSlotsPerSm * smid + j belong to this
+      // SM, whose resident CTAs (at most RSOT_FUSED_MIN_BLOCKS by registers
+      // and shared memory) hold at most that many, so a few CAS always find
+      // one.  (Linear probing of the whole table from a ticket, as before,
+      // failed for some CTAs at cfg3: the probe of a late CTA chases the
+      // moving band of just-taken slots, 1024 CAS in ~350 us without a hit.)
+      // Fallback for SM ids beyond the table: the global probe.
       int slot = -1;
       if (!DEBUG && KS == 1 && A.mbuf && A.mslots) {
-        const unsigned t0 = atomicAdd(A.mticket, 1u);
-        for (unsigned k = 0; k < static_cast<unsigned>(kMaskSlots); ++k) {
-          const int c = static_cast<int>((t0 + k) & (kMaskSlots - 1));
-          if (atomicCAS(A.mbusy + c, 0, 1) == 0) {
-            slot = c;
-            break;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        if (smid < static_cast<unsigned>(kMaskSlots / kSlotsPerSm)) {
+          for (int j = 0; j < kSlotsPerSm; ++j) {
+            const int c = static_cast<int>(smid) * kSlotsPerSm + j;
+            if (atomicCAS(A.mbusy + c, 0, 1) == 0) {
+              slot = c;
+              break;
+            }
+          }
+        } else {
+          const unsigned t0 = atomicAdd(A.mticket, 1u);
+          for (unsigned k = 0; k < static_cast<unsigned>(kMaskSlots); ++k) {
+            const int c = static_cast<int>((t0 + k) & (kMaskSlots - 1));
+            if (atomicCAS(A.mbusy + c, 0, 1) == 0) {
+              slot = c;
+              break;
+            }
           }
         }
       }

@@ -1442,10 +1442,14 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
         // stale entries taken by no atom; f <= 252, so f + 3 stays in the list)
         for (int f = 0; f < nfull; f += 4) {
           const bool i1 = f + 1 < nfull, i2 = f + 2 < nfull, i3 = f + 3 < nfull;
-          exp_part64<1, true, SAFE>(sm, at, wide, full[-f], full[-(f + 1)], va, vb, i1 && va, i1 && vb, cn);
-          exp_part64<1, true, SAFE>(sm, at, wide, full[-(f + 2)], full[-(f + 3)], i2 && va, i2 && vb,
-                                    i3 && va, i3 && vb, cn);
+          exp_part64<1, true, SAFE, false>(sm, at, wide, full[-f], full[-(f + 1)], va, vb, i1 && va, i1 && vb,
+                                           cn);
+          exp_part64<1, true, SAFE, false>(sm, at, wide, full[-(f + 2)], full[-(f + 3)], i2 && va, i2 && vb,
+                                           i3 && va, i3 && vb, cn);
         }
+        // (every valid atom of the warp takes every full-in item: counted here, not per pair)
+        at.ca += va ? static_cast<uint32_t>(nfull) : 0u;
+        at.cb += vb ? static_cast<uint32_t>(nfull) : 0u;
         at.ca += static_cast<uint32_t>(cn.x);
         at.cb += static_cast<uint32_t>(cn.y);
       } else {

@@ -46,6 +46,9 @@ constexpr int kTileT32 = 384;  // staged points per tile (fp32 kernel)
 #ifndef RSOT_FULLIN_RATIO2
 #define RSOT_FULLIN_RATIO2 49.0f  // full-in split when r > 7 warp-box half-diagonals
 #endif
+#ifndef RSOT_P2_TM
+#define RSOT_P2_TM 1  // target-major phase 2 over per-warp item records (unsplit non-safe CTAs)
+#endif
 #ifndef RSOT_P1_LEAN
 #define RSOT_P1_LEAN 1
 #endif
@@ -191,6 +194,8 @@ struct Region {
   float lo_thr, hi_thr;
   int c_lo[3], c_hi[3];
   bool wide;
+  float xy_max;  // >= |2 c2 x'.y'| of any taken pair (|x'| <= hd, |y'| <= hd + r)
+  float wy_max;  // >= c2 |y'|^2 of any taken pair's target
 };
 
 __device__ void setup_region(const GridDev& g, const double lo[3], const double hi[3],
@@ -206,6 +211,11 @@ __device__ void setup_region(const GridDev& g, const double lo[3], const double 
   // error band (9x the worst-case rounding of the FP32 distance).
   R.wide = c2 * hd2 > 400.0;
   const double r = sqrt(r2);
+  {
+    const double hd = sqrt(hd2), yb = hd + r;
+    R.xy_max = __double2float_ru(2.0 * c2 * hd * yb * (1.0 + 1e-6));
+    R.wy_max = __double2float_ru(c2 * yb * yb * (1.0 + 1e-6));
+  }
   const double Rb = sqrt(hd2) + r_scan + 1.75 * g.h;
   const double band = 0x1p-21 * (8.0 * r * Rb + 4.0 * r2);
   R.lo_thr = __double2float_rd(r2 - band);
@@ -552,7 +562,9 @@ constexpr int kFA = 2 * kT;  // atoms per CTA
 // in phase 2; slot kMaskSlots is the shared scratch of CTAs without a slot.
 constexpr int kMaskSlots = 1024;
 constexpr int kMaskWords = 2048;
-constexpr int kSlotsPerSm = 4;  // (>= resident trunc_fused CTAs per SM)
+constexpr int kSlotsPerSm = 4;
+constexpr int kRecCap = 131072;  // item indices per warp stream (cfg3's heaviest unsplit chunks: ~64 K)
+constexpr int kRecSlots = 160 * kSlotsPerSm;  // streams exist for the slots of SM ids < 160 (1.3 GB)
 // Word-major pool: word w of every slot (and of every thread of a slot) is
 // contiguous, so the words in use -- a few dozen per thread at cfg5 -- form
 // one compact region at the start of the pool that the L2 can hold (see
@@ -571,7 +583,7 @@ struct FusedSmem {
   int rowStart[kT];
   int rowPref[kT + 1];
   ListT wlist[kT / 32][kTileT];
-  double colW[kT / 32][kTileT];
+  alignas(32) double colW[kT / 32][kTileT];  // (also the atom table of phase2_tm: double4)
   double4 rawY[kTileT];                // cp.async landing zone of the next tile
   double rawB2[kTileT];
   int rawJ[kTileT];
@@ -579,6 +591,9 @@ struct FusedSmem {
   Region R;                            // CTA-uniform scan region (kept out of registers)
   int mslot;                           // this CTA's mask slot (-1: none)
   int mok;                             // 1: phase 1 stored every step's pair mask
+  int nrec[kT / 32];                   // mixed / full-in item indices written by each warp
+  int nfulrec[kT / 32];                //   (target-major phase 2)
+  int rok;                             // 1: every warp's records fit its stream
   int2 tbl[ExpTab512::kTab];
   double sh[200];
   int shi[40];
@@ -617,6 +632,8 @@ struct FusedArgs {
   unsigned* mticket;                     // slot search start
   int mslots;                            // 0: no slots (phase 2 recomputes the masks)
   int mwords;                            // words per thread a slot may hold (<= kMaskWords)
+  int* rbuf;                             // cell-order indices of the warps' culled items: one stream of
+  int rcap;                              //   rcap entries per (slot, warp), or null / 0
 };
 
 // chunk roles (chunk_role)
@@ -755,7 +772,7 @@ __device__ __forceinline__ void fused_convert(FusedSmem& sm, const FusedArgs& A,
     // floor(512 (b2_j - B - c2 r^2)): the target side of the exponent-side
     // pair predicate (step64i), clamped far from int overflow
     const double th = fmin(fmax(512.0 * ((sm.rawB2[t] - B) - A.c2 * A.r2), -1.0e8), 1.0e8);
-    sm.tN1[t] = make_float4(f2, f2, __int_as_float(__double2int_rd(th)), 0.f);
+    sm.tN1[t] = make_float4(f2, f2, __int_as_float(__double2int_rd(th)), __int_as_float(sm.rawK[t]));
     sm.tJ[t] = sm.rawJ[t];
     sm.tK[t] = sm.rawK[t];
   }
@@ -1235,6 +1252,97 @@ __device__ __forceinline__ void step64x(const FusedSmem& sm, const FusedArgs& A,
   if (++mio.n == 8) mask_store(mio);
 }
 
+// acc + (take ? 2^s : 0), non-clamped (phase2_tm).
+__device__ __forceinline__ double exp2_acc_t(double s, double acc, unsigned tbl, bool take) {
+  const double kk = __dadd_rn(s, ExpTab512::kMagic);
+  return exp2_acc_x(s, kk, __double2loint(kk), acc, tbl, take);
+}
+
+// Target-major phase 2 of an unsplit non-safe CTA.  Phase 1 left, per warp,
+// the cell-order indices of its culled items in list order (mixed items from
+// the front of the warp's index stream, each tile padded to 16; full-in items
+// from the back) next to the pair-mask words (16 mixed items a word).  Each
+// warp walks its items, lane = item: the item's 64-atom mask is transposed out
+// of the lanes' mask words by ballots (2 per item, against ~1200 instructions
+// of pair work per item), and the item's column is summed over the warp's 64
+// atoms, broadcast from shared memory as {2 c2 x', log2(m_q / S_q)}.  No
+// tiles, staging, culling, barriers or cross-lane reduction; the per-target
+// factor 2^(w_j) multiplies the finished column (the exponents X.y' + log2 w
+// and w_j are bounded by the caller).  The item's local coordinates and w_j
+// are recomputed from the target record exactly as fused_convert staged them.
+// Bit-matrix transpose across the warp: returns in lane b the word whose bit
+// l is bit b of lane l's x (5 butterfly rounds).
+__device__ __forceinline__ unsigned warp_transpose32(unsigned x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 16; k >= 1; k >>= 1) {
+    const unsigned m = k == 16 ? 0x0000ffffu : k == 8 ? 0x00ff00ffu : k == 4 ? 0x0f0f0f0fu
+                     : k == 2 ? 0x33333333u : 0x55555555u;
+    const unsigned y = __shfl_xor_sync(0xffffffffu, x, k);
+    x = (lane & k) ? (((y >> k) & m) | (x & ~m)) : ((x & m) | ((y & m) << k));
+  }
+  return x;
+}
+
+__device__ __forceinline__ void tm_item(const FusedSmem& sm, const FusedArgs& A, const double4* atab,
+                                        unsigned tb, double B, int k, unsigned mA, unsigned mB) {
+  const double4 y = A.ys[k];
+  const double y0 = y.x - sm.R.o[0], y1 = y.y - sm.R.o[1], y2 = y.z - sm.R.o[2];
+  const double yy = fma(y2, y2, fma(y1, y1, y0 * y0));
+  const double w = fmax(fma(-A.c2, yy, A.b2s[k]) - B, -1.0e5);
+  double acc = 0.0;
+#pragma unroll 8
+  for (int a = 0; a < 32; ++a) {
+    const double4 X = atab[a];
+    acc = exp2_acc_t(fma(X.x, y0, fma(X.y, y1, fma(X.z, y2, X.w))), acc, tb, (mA >> a) & 1u);
+  }
+#pragma unroll 8
+  for (int a = 0; a < 32; ++a) {
+    const double4 X = atab[32 + a];
+    acc = exp2_acc_t(fma(X.x, y0, fma(X.y, y1, fma(X.z, y2, X.w))), acc, tb, (mB >> a) & 1u);
+  }
+  if (acc > 0.0)
+    fp_red(A.gacc + kLimbs * static_cast<size_t>(k), acc * exp2_acc<true, ExpTab512>(w, 0.0, sm.tbl));
+}
+
+__device__ __forceinline__ void phase2_tm(FusedSmem& sm, const FusedArgs& A, const FusedAtoms& at, double B,
+                                          double la, double lb, bool ea, bool eb) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double4* const atab = reinterpret_cast<double4*>(&sm.colW[0][0]) + warp * 64;
+  atab[lane] = make_double4(at.Xa[0], at.Xa[1], at.Xa[2], la);
+  atab[32 + lane] = make_double4(at.Xb[0], at.Xb[1], at.Xb[2], lb);
+  const unsigned EA = __ballot_sync(0xffffffffu, ea), EB = __ballot_sync(0xffffffffu, eb);
+  __syncwarp();
+  const unsigned tb = static_cast<unsigned>(__cvta_generic_to_shared(&sm.tbl[0]));
+  const int* const ks = A.rbuf + (static_cast<size_t>(sm.mslot) * (kT / 32) + warp) * static_cast<size_t>(A.rcap);
+  const uint32_t* const mw = A.mbuf + static_cast<size_t>(sm.mslot) * kT + threadIdx.x;
+  const int nmix = sm.nrec[warp], nful = sm.nfulrec[warp];
+  for (int e0 = 0; e0 < nmix; e0 += 32) {
+    const int w0 = e0 >> 4;
+    const uint32_t wA = mw[static_cast<size_t>(w0) * kMaskWordStride];
+    const uint32_t wB = e0 + 16 < nmix ? mw[static_cast<size_t>(w0 + 1) * kMaskWordStride] : 0u;
+    // 32 x 32 bit transposes of the two words across the warp: lane b then
+    // holds bit b of every lane's word, i.e. the 32-atom mask of one
+    // (item, atom slot).  Bits b, b + 1 (b even) of a word belong to the item
+    // of step (28 - b) / 4 (b % 4 == 0: slot 0) or (30 - b) / 4 (slot 1):
+    // even lanes take that item of word A, odd lanes (b = lane - 1) of word B.
+    const unsigned tA = warp_transpose32(wA), tB = warp_transpose32(wB);
+    const unsigned pA = __shfl_xor_sync(0xffffffffu, tA, 1), pB = __shfl_xor_sync(0xffffffffu, tB, 1);
+    const bool odd = lane & 1;
+    const unsigned mA = odd ? pB : tA, mB = odd ? tB : pA;
+    const int bpos = lane & ~1;
+    const int slot = (bpos >> 1) & 1, step = ((slot ? 30 : 28) - bpos) >> 2;
+    const int e = e0 + (odd ? 16 : 0) + 2 * step + slot;
+    const int k = e < nmix ? ks[e] : 0;
+    tm_item(sm, A, atab, tb, B, k, mA & EA, mB & EB);
+  }
+  for (int e0 = 0; e0 < nful; e0 += 32) {  // full-in items: every enabled atom
+    const bool in = e0 + lane < nful;
+    const int k = in ? ks[A.rcap - 1 - (e0 + lane)] : 0;
+    tm_item(sm, A, atab, tb, B, k, in ? EA : 0u, in ? EB : 0u);
+  }
+}
+
 // Phase-2 batch replaying the stored masks (word = the batch's 8 steps).
 // No guards on the steps (one basic block of 8 steps): items past nsel read
 // stale but finite staged entries (fused_body zeroes the list and staging
@@ -1347,6 +1455,19 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
 #else
   constexpr bool kIntPred = kStore && !SAFE && PHASE == 1;  // (step64i stores the masks it decides)
 #endif
+  // kRec: the non-safe phase 1 of an unsplit CTA also writes, per tile, the
+  // cell-order indices of the warp's culled items for the target-major
+  // phase 2 (phase2_tm): mixed items in list order from the front of the
+  // warp's stream (two per step: an odd tail item is followed by a pad), full-in
+  // items from the back.  The mask stream then runs on across the tiles (no
+  // per-tile padding to a word: item e belongs to word e / 16), so the tiled
+  // phase 2 cannot replay it: a kRec CTA that falls back recomputes.
+  constexpr bool kRec = kIntPred && RSOT_P1_LEAN && RSOT_P2_TM;
+  int* const kstream = kRec && A.rbuf != nullptr && sm.mslot >= 0 && sm.mslot < kRecSlots
+                           ? A.rbuf + (static_cast<size_t>(sm.mslot) * (kT / 32) + warp) * static_cast<size_t>(A.rcap)
+                           : nullptr;
+  int rmix = 0, rful = 0;  // entries written so far
+  bool rroom = kstream != nullptr;
   const bool mon = kStore && A.mbuf && (PHASE == 1 || (sm.mslot >= 0 && sm.mok));
   MaskIO mio;
   mio.base = A.mbuf + static_cast<size_t>(sm.mslot < 0 ? kMaskSlots : sm.mslot) * kT + threadIdx.x;
@@ -1388,6 +1509,23 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
         float2 cn = make_float2(0.f, 0.f);
         bool hit = false;
         int i = 0;
+        if (kRec) {
+          // (a tile whose items do not fit the stream any more: no further
+          // entries from this warp, phase 2 of the CTA recomputes)
+          const int pad = (nsel + 1) & ~1;  // (an odd tail item is a step of its own)
+          if (rroom && rmix + pad + rful + nfull > A.rcap) {
+            if (lane == 0) sm.rok = 0;
+            rroom = false;
+          }
+          if (rroom) {
+            for (int e = lane; e < pad; e += 32)
+              kstream[rmix + e] = e < nsel ? __float_as_int(at16(sm.tN1, list[e]).w) : 0;
+            for (int f = lane; f < nfull; f += 32)
+              kstream[A.rcap - 1 - (rful + f)] = __float_as_int(at16(sm.tN1, full[-f]).w);
+          }
+          rmix += pad;
+          rful += nfull;
+        }
         if (kIntPred && nsel >= 2) {
           int t0 = list[0], t1 = list[1];
 #if RSOT_P1_LEAN
@@ -1437,7 +1575,7 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
         }
         if (i < nsel)
           step64<1, false, SAFE, DEBUG, true, kStore>(sm, A, at, K, wide, list[i], list[i], cn, hit, &mio);
-        if (kStore) mask_flush(mio);  // each tile's stream starts on a word
+        if (kStore && !kRec) mask_flush(mio);  // each tile's stream starts on a word
         // full-in items, 4 per iteration without guards (items past nfull:
         // stale entries taken by no atom; f <= 252, so f + 3 stays in the list)
         for (int f = 0; f < nfull; f += 4) {
@@ -1480,9 +1618,16 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
       pend = 0;
     }
   }
+  if (kRec) mask_flush(mio);  // (the stream's last word, before its pairs are counted)
   if (PHASE == 1 && kStore) {  // the mixed-list pairs were counted in the mask words
     at.ca += mio.ca;
     at.cb += mio.cb;
+  }
+  if (kRec) {
+    if (lane == 0) {
+      sm.nrec[warp] = rmix;
+      sm.nfulrec[warp] = rful;
+    }
   }
 }
 
@@ -1646,6 +1791,7 @@ __device__ __forceinline__ void fused_body(FusedSmem& sm, const FusedArgs& A, in
       }
       sm.mslot = slot;
       sm.mok = slot >= 0 ? 1 : 0;
+      sm.rok = slot >= 0 ? 1 : 0;
     }
     __syncthreads();
   }
@@ -1719,10 +1865,41 @@ __device__ __forceinline__ void fused_body(FusedSmem& sm, const FusedArgs& A, in
                         at.wb, 0x1p-960, primary);
 
 #ifndef RSOT_EXP_NOPHASE2
-  if (safe)
-    fused_scan<2, true, DEBUG, KS>(sm, A, wb, cull_thr, B, at, split);
-  else
-    fused_scan<2, false, DEBUG, KS>(sm, A, wb, cull_thr, B, at, split);
+  if constexpr (!DEBUG && KS == 1 && RSOT_P1_LEAN && RSOT_P2_TM) {
+    // Unsplit CTAs: target-major phase 2 over the item records when phase 1
+    // wrote them all and every exponent involved stays in range -- the pairs'
+    // 2^(X.y' + log2 w_q) and the targets' 2^(w_j), bounded from the region.
+    // Any other CTA (safe, no slot, stream overflow, out of range) runs the
+    // tiled phase 2 in its safe instantiation, which handles every case.
+    const bool ea = at.wa > 0.0, eb = at.wb > 0.0;
+    const double la = ea ? log2(at.wa) : 0.0, lb = eb ? log2(at.wb) : 0.0;
+    const double xy = sm.R.xy_max;
+    const bool fits = fmax(la, lb) + xy <= 1000.0 && fmin(la, lb) - xy >= -1000.0;
+    const bool all_fit = __syncthreads_and(fits);  // (also: nrec / rok of phase 1 visible)
+    const bool tm = !safe && A.rbuf != nullptr && A.mbuf != nullptr && sm.mslot >= 0 && sm.mslot < kRecSlots &&
+                    sm.rok && sm.mok && all_fit &&
+                    (A.scal[kSlotBmin] - B) - static_cast<double>(sm.R.wy_max) >= -1000.0;
+#ifdef RSOT_LAM_TRACE
+    if (!tm && threadIdx.x == 0)
+      printf("tmfallback chunk %d safe %d mslot %d rok %d mok %d fit %d nrec %d %d %d %d ful %d\n", chunk, (int)safe,
+             sm.mslot, sm.rok, sm.mok, (int)all_fit, sm.nrec[0], sm.nrec[1], sm.nrec[2], sm.nrec[3], sm.nfulrec[0]);
+#endif
+    if (tm) {
+      phase2_tm(sm, A, at, B, la, lb, ea, eb);
+    } else {
+      if (!safe) {  // (a non-safe CTA's mask stream is not tile-aligned: recompute)
+        __syncthreads();
+        if (threadIdx.x == 0) sm.mok = 0;
+        __syncthreads();
+      }
+      fused_scan<2, true, DEBUG, KS>(sm, A, wb, cull_thr, B, at, split);
+    }
+  } else {
+    if (safe)
+      fused_scan<2, true, DEBUG, KS>(sm, A, wb, cull_thr, B, at, split);
+    else
+      fused_scan<2, false, DEBUG, KS>(sm, A, wb, cull_thr, B, at, split);
+  }
 #endif
   if (!DEBUG && KS == 1 && A.mbuf) {
     __syncthreads();  // every thread is done with the slot
@@ -2793,7 +2970,7 @@ void PointOrders::release() {
 void TruncWorkspace::release() {
   void* ptrs[] = {cub_tmp, keys, keys2, idx, idx2, b2s, S, atomL, atomJ, atomD, cntd, emptyd, cnt,
                   hash, empty_fp, pts, near_out, red, chunk_cost, heavy_flag,
-                  chunk_w, chunk_pre, part_range, mbuf, mbusy, mticket};
+                  chunk_w, chunk_pre, part_range, mbuf, mbusy, mticket, rbuf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (fork_ev) cudaEventDestroy(fork_ev);
@@ -2976,6 +3153,7 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
     A.queue = ws.part_range + 4;
     // phase-1 pair masks replayed by phase 2 (fp64 kernel; RSOT_CUDA_PAIR_MASKS=0: off)
     A.mbuf = nullptr; A.mbusy = nullptr; A.mticket = nullptr; A.mslots = 0; A.mwords = 0;
+    A.rbuf = nullptr; A.rcap = 0;
     if (!fp32 && !dbg) {
       if (!ws.mbuf) {
         TCK(cudaMalloc(&ws.mbuf, sizeof(uint32_t) * (static_cast<size_t>(kMaskSlots) + 1) * (kMaskWords + 1) * kT));
@@ -2985,11 +3163,17 @@ int run_truncated(TruncWorkspace& ws, const DeviceAtoms& a, AtomCells& ac,
         TCK(cudaMemsetAsync(ws.mbusy, 0, sizeof(int) * kMaskSlots, s));
         TCK(cudaMemsetAsync(ws.mticket, 0, sizeof(unsigned), s));
       }
+      if (!ws.rbuf && RSOT_P2_TM)
+        TCK(cudaMalloc(&ws.rbuf, sizeof(int) * static_cast<size_t>(kRecSlots) * (kT / 32) * kRecCap));
       A.mbuf = ws.mbuf; A.mbusy = ws.mbusy; A.mticket = ws.mticket;
       A.mslots = env_double("RSOT_CUDA_PAIR_MASKS", 1.0) != 0.0 ? 1 : 0;  // 0: phase 2 recomputes
       // (tests: a small cap forces the overflow fallback in most CTAs)
       A.mwords = static_cast<int>(std::min<double>(kMaskWords, std::max(0.0, env_double("RSOT_CUDA_MASK_WORDS",
                                                                                         kMaskWords))));
+      // item records of the target-major phase 2 (the same switches: no slots
+      // -> no streams; a small word cap also caps the streams, 8 records a word)
+      A.rbuf = ws.rbuf;
+      A.rcap = A.mwords < kMaskWords ? 16 * A.mwords : kRecCap;
     }
     // Scan costs of the chunks -> roles (partitioned atoms: this rank's
     // work-balanced range; heavy chunks run split across a CTA cluster) and a

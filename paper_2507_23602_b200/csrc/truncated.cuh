@@ -93,6 +93,8 @@ struct TruncWorkspace {
   // phase-1 pair masks replayed by phase 2 (trunc_fused): slots held by
   // resident CTAs, busy flags, slot-search ticket
   uint32_t* mbuf = nullptr; int* mbusy = nullptr; unsigned* mticket = nullptr;
+  // item indices of the target-major phase 2: one stream per (slot, warp)
+  int* rbuf = nullptr;
   void release();
 };
 

@@ -623,11 +623,14 @@ def test_partitioned_atoms_balance():
 
 @pytest.mark.parametrize("cutoff", [0.004, 0.02])
 def test_pair_mask_replay_and_fallbacks(cutoff, monkeypatch):
-    """Phase 2 of the fp64 truncated kernel replays phase 1's pair masks from
-    per-CTA slots (truncated.cu MaskIO); CTAs whose masks overflow their slot
-    (forced here with RSOT_CUDA_MASK_WORDS) or that hold no slot
-    (RSOT_CUDA_PAIR_MASKS=0) recompute them.  All three paths must give
-    bitwise identical results, within 1e-10 of the oracle."""
+    """Phase 2 of the fp64 truncated kernel runs target-major over phase 1's
+    pair masks and item-index streams (truncated.cu phase2_tm); CTAs whose
+    masks or streams overflow (forced here with RSOT_CUDA_MASK_WORDS) or that
+    hold no slot (RSOT_CUDA_PAIR_MASKS=0) run the tiled phase 2 and recompute
+    the masks.  Phase 1 is common: J, D and the counters are bitwise identical
+    in all three modes; the gradients differ only in the summation order of a
+    target's column (<= 1e-13 of the marginal scale); every mode is
+    reproducible run to run and within 1e-10 of the oracle."""
     rng = np.random.default_rng(977)
     A = np.vstack([0.45 + 0.1 * rng.uniform(size=(4000, 3)), rng.uniform(size=(12000, 3))])
     T = np.vstack([0.4 + 0.2 * rng.uniform(size=(60000, 3)), rng.uniform(size=(20000, 3))])
@@ -645,9 +648,13 @@ def test_pair_mask_replay_and_fallbacks(cutoff, monkeypatch):
             monkeypatch.setenv(k, v)
         ctx = rs.Context(0)
         runs[mode] = gpu_eval(ctx, A, M, T, W, psi, eps, cutoff)
+        again = gpu_eval(ctx, A, M, T, W, psi, eps, cutoff)
+        assert again["J"] == runs[mode]["J"] and np.array_equal(again["gradient"], runs[mode]["gradient"]), mode
+    want = C.evaluate_dual(A, M, T, W, psi, eps, cutoff, workers=8)
+    scale = marginal_scale(W, want["gradient"])
     for mode in ("overflow", "recompute"):
         assert runs[mode]["J"] == runs["replay"]["J"] and runs[mode]["D"] == runs["replay"]["D"], mode
-        assert np.array_equal(runs[mode]["gradient"], runs["replay"]["gradient"]), mode
+        assert np.max(np.abs(runs[mode]["gradient"] - runs["replay"]["gradient"])) <= 1e-13 * scale, mode
         assert runs[mode]["candidate_pairs"] == runs["replay"]["candidate_pairs"], mode
-    want = C.evaluate_dual(A, M, T, W, psi, eps, cutoff, workers=8)
-    assert_parity(runs["replay"], want, marginal_scale(W, want["gradient"]), TOL)
+        assert_parity(runs[mode], want, scale, TOL)
+    assert_parity(runs["replay"], want, scale, TOL)

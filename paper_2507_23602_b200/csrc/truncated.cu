@@ -1284,25 +1284,67 @@ __device__ __forceinline__ unsigned warp_transpose32(unsigned x) {
   return x;
 }
 
-__device__ __forceinline__ void tm_item(const FusedSmem& sm, const FusedArgs& A, const double4* atab,
-                                        unsigned tb, double B, int k, unsigned mA, unsigned mB) {
+// Local coordinates and exponent term of target k about the CTA origin (as
+// fused_convert stages them).
+struct TmItem {
+  double y0, y1, y2, w;
+};
+__device__ __forceinline__ TmItem tm_load(const FusedSmem& sm, const FusedArgs& A, double B, int k) {
   const double4 y = A.ys[k];
-  const double y0 = y.x - sm.R.o[0], y1 = y.y - sm.R.o[1], y2 = y.z - sm.R.o[2];
-  const double yy = fma(y2, y2, fma(y1, y1, y0 * y0));
-  const double w = fmax(fma(-A.c2, yy, A.b2s[k]) - B, -1.0e5);
-  double acc = 0.0;
-#pragma unroll 8
-  for (int a = 0; a < 32; ++a) {
-    const double4 X = atab[a];
-    acc = exp2_acc_t(fma(X.x, y0, fma(X.y, y1, fma(X.z, y2, X.w))), acc, tb, (mA >> a) & 1u);
+  TmItem t;
+  t.y0 = y.x - sm.R.o[0];
+  t.y1 = y.y - sm.R.o[1];
+  t.y2 = y.z - sm.R.o[2];
+  const double yy = fma(t.y2, t.y2, fma(t.y1, t.y1, t.y0 * t.y0));
+  t.w = fmax(fma(-A.c2, yy, A.b2s[k]) - B, -1.0e5);
+  return t;
+}
+__device__ __forceinline__ void tm_flush(const FusedSmem& sm, const FusedArgs& A, int k, double w, double acc) {
+  if (acc > 0.0) fp_red(A.gacc + kLimbs * static_cast<size_t>(k), acc * exp2_acc<true, ExpTab512>(w, 0.0, sm.tbl));
+}
+// Two items per lane against the warp's 64 atoms (mask bit a: atom a of the
+// table): each broadcast atom entry serves both items; 16 atoms per unrolled
+// block, the masks shifted down between blocks (immediate bit tests).
+__device__ __forceinline__ void tm_items2(const FusedSmem& sm, const FusedArgs& A, const double4* atab,
+                                          unsigned tb, double B, int k0, unsigned long long m0, int k1,
+                                          unsigned long long m1) {
+  const TmItem i0 = tm_load(sm, A, B, k0), i1 = tm_load(sm, A, B, k1);
+  double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll 1
+  for (int h = 0; h < 4; ++h) {
+    const unsigned b0 = static_cast<unsigned>(m0), b1 = static_cast<unsigned>(m1);
+#pragma unroll
+    for (int a = 0; a < 16; ++a) {
+      const double4 X = atab[16 * h + a];
+      acc0 = exp2_acc_t(fma(X.x, i0.y0, fma(X.y, i0.y1, fma(X.z, i0.y2, X.w))), acc0, tb, (b0 >> a) & 1u);
+      acc1 = exp2_acc_t(fma(X.x, i1.y0, fma(X.y, i1.y1, fma(X.z, i1.y2, X.w))), acc1, tb, (b1 >> a) & 1u);
+    }
+    m0 >>= 16;
+    m1 >>= 16;
   }
-#pragma unroll 8
-  for (int a = 0; a < 32; ++a) {
-    const double4 X = atab[32 + a];
-    acc = exp2_acc_t(fma(X.x, y0, fma(X.y, y1, fma(X.z, y2, X.w))), acc, tb, (mB >> a) & 1u);
-  }
-  if (acc > 0.0)
-    fp_red(A.gacc + kLimbs * static_cast<size_t>(k), acc * exp2_acc<true, ExpTab512>(w, 0.0, sm.tbl));
+  tm_flush(sm, A, k0, i0.w, acc0);
+  tm_flush(sm, A, k1, i1.w, acc1);
+}
+
+// The lane's item of a 32-item block (mask words wA: items 0..15, wB: items
+// 16..31 of the block starting at entry e0): index and 64-atom mask.
+// 32 x 32 bit transposes of the two words across the warp: lane b then holds
+// bit b of every lane's word, i.e. the 32-atom mask of one (item, atom slot).
+// Bits b, b + 1 (b even) of a word belong to the item of step (28 - b) / 4
+// (b % 4 == 0: slot 0) or (30 - b) / 4 (slot 1): even lanes take that item
+// of word A, odd lanes (b = lane - 1) of word B.
+__device__ __forceinline__ void tm_gather(uint32_t wA, uint32_t wB, int e0, int nmix, const int* ks,
+                                          unsigned EA, unsigned EB, int& k, unsigned long long& m) {
+  const int lane = threadIdx.x & 31;
+  const unsigned tA = warp_transpose32(wA), tB = warp_transpose32(wB);
+  const unsigned pA = __shfl_xor_sync(0xffffffffu, tA, 1), pB = __shfl_xor_sync(0xffffffffu, tB, 1);
+  const bool odd = lane & 1;
+  const unsigned mA = (odd ? pB : tA) & EA, mB = (odd ? tB : pA) & EB;
+  const int bpos = lane & ~1;
+  const int slot = (bpos >> 1) & 1, step = ((slot ? 30 : 28) - bpos) >> 2;
+  const int e = e0 + (odd ? 16 : 0) + 2 * step + slot;
+  k = e < nmix ? ks[e] : 0;
+  m = (static_cast<unsigned long long>(mB) << 32) | mA;
 }
 
 __device__ __forceinline__ void phase2_tm(FusedSmem& sm, const FusedArgs& A, const FusedAtoms& at, double B,
@@ -1317,29 +1359,28 @@ __device__ __forceinline__ void phase2_tm(FusedSmem& sm, const FusedArgs& A, con
   const int* const ks = A.rbuf + (static_cast<size_t>(sm.mslot) * (kT / 32) + warp) * static_cast<size_t>(A.rcap);
   const uint32_t* const mw = A.mbuf + static_cast<size_t>(sm.mslot) * kT + threadIdx.x;
   const int nmix = sm.nrec[warp], nful = sm.nfulrec[warp];
-  for (int e0 = 0; e0 < nmix; e0 += 32) {
-    const int w0 = e0 >> 4;
-    const uint32_t wA = mw[static_cast<size_t>(w0) * kMaskWordStride];
-    const uint32_t wB = e0 + 16 < nmix ? mw[static_cast<size_t>(w0 + 1) * kMaskWordStride] : 0u;
-    // 32 x 32 bit transposes of the two words across the warp: lane b then
-    // holds bit b of every lane's word, i.e. the 32-atom mask of one
-    // (item, atom slot).  Bits b, b + 1 (b even) of a word belong to the item
-    // of step (28 - b) / 4 (b % 4 == 0: slot 0) or (30 - b) / 4 (slot 1):
-    // even lanes take that item of word A, odd lanes (b = lane - 1) of word B.
-    const unsigned tA = warp_transpose32(wA), tB = warp_transpose32(wB);
-    const unsigned pA = __shfl_xor_sync(0xffffffffu, tA, 1), pB = __shfl_xor_sync(0xffffffffu, tB, 1);
-    const bool odd = lane & 1;
-    const unsigned mA = odd ? pB : tA, mB = odd ? tB : pA;
-    const int bpos = lane & ~1;
-    const int slot = (bpos >> 1) & 1, step = ((slot ? 30 : 28) - bpos) >> 2;
-    const int e = e0 + (odd ? 16 : 0) + 2 * step + slot;
-    const int k = e < nmix ? ks[e] : 0;
-    tm_item(sm, A, atab, tb, B, k, mA & EA, mB & EB);
-  }
-  for (int e0 = 0; e0 < nful; e0 += 32) {  // full-in items: every enabled atom
-    const bool in = e0 + lane < nful;
-    const int k = in ? ks[A.rcap - 1 - (e0 + lane)] : 0;
-    tm_item(sm, A, atab, tb, B, k, in ? EA : 0u, in ? EB : 0u);
+  const int nw = (nmix + 15) >> 4;                 // mask words of the warp's stream
+  const int pm = (nmix + 63) >> 6, pf = (nful + 63) >> 6;
+  const unsigned long long EF = (static_cast<unsigned long long>(EB) << 32) | EA;
+#pragma unroll 1
+  for (int pass = 0; pass < pm + pf; ++pass) {  // 64 items a pass, two per lane
+    int k0, k1;
+    unsigned long long m0, m1;
+    if (pass < pm) {
+      const int e0 = pass << 6, w0 = pass << 2;
+      uint32_t w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = w0 + u < nw ? mw[static_cast<size_t>(w0 + u) * kMaskWordStride] : 0u;
+      tm_gather(w[0], w[1], e0, nmix, ks, EA, EB, k0, m0);
+      tm_gather(w[2], w[3], e0 + 32, nmix, ks, EA, EB, k1, m1);
+    } else {  // full-in items: every enabled atom
+      const int e = ((pass - pm) << 6) + lane;
+      k0 = e < nful ? ks[A.rcap - 1 - e] : 0;
+      k1 = e + 32 < nful ? ks[A.rcap - 1 - (e + 32)] : 0;
+      m0 = e < nful ? EF : 0ull;
+      m1 = e + 32 < nful ? EF : 0ull;
+    }
+    tm_items2(sm, A, atab, tb, B, k0, m0, k1, m1);
   }
 }
 

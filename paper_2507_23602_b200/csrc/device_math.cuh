@@ -429,9 +429,13 @@ __device__ __forceinline__ void fp_red_top(unsigned long long* acc, int limb, un
 
 __device__ __forceinline__ void fp_red(unsigned long long* acc, double m) {
   if (!(m > 0.0)) return;
-  int e;
-  const double fr = frexp(m, &e);
-  unsigned long long mant = static_cast<unsigned long long>(ldexp(fr, 53));
+  // m = mant * 2^(e - 53), mant the 53-bit significand (frexp / ldexp done on
+  // the bits; subnormals lie far below the last limb)
+  const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(m));
+  const int ef = static_cast<int>(bits >> 52);
+  if (ef == 0) return;
+  unsigned long long mant = (bits & 0x000fffffffffffffull) | 0x0010000000000000ull;
+  const int e = ef - 1022;
   int sh = e - 53 + 150;  // value = mant * 2^sh (units of 2^-150)
   if (sh < 0) {
     if (sh <= -64) return;

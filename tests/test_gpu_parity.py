@@ -658,3 +658,36 @@ def test_pair_mask_replay_and_fallbacks(cutoff, monkeypatch):
         assert runs[mode]["candidate_pairs"] == runs["replay"]["candidate_pairs"], mode
         assert_parity(runs[mode], want, scale, TOL)
     assert_parity(runs["replay"], want, scale, TOL)
+
+
+@pytest.mark.parametrize("mass_scale", [1.0, 1e-280, 1e-305])
+def test_target_major_phase2_range_fallback(ctx, mass_scale):
+    """The target-major phase 2 (truncated.cu phase2_tm) folds log2(m_q / S_q)
+    into the exponents and is taken only when that stays within +-1000 for
+    every atom of the CTA; tiny masses push it out of range, and those CTAs
+    run the tiled phase 2 instead.  Either way the result matches the oracle
+    (relative to the masses' scale), with empty-set atoms, a partial last
+    chunk and a wide psi range in the instance."""
+    rng = np.random.default_rng(4242)
+    nq, n = 3 * 256 + 77, 6000            # partial last chunk
+    A = rng.uniform(size=(nq, 3))
+    A[:40] += 3.0                          # atoms far from every target: empty candidate sets
+    T = rng.uniform(size=(n, 3))
+    M = (rng.uniform(size=nq) + 0.1)
+    M = M / M.sum() * mass_scale
+    W = rng.uniform(size=n) + 0.5
+    W /= W.sum()
+    psi = rng.normal(0, 0.05, size=n)      # exponents spread over ~ +-30 at eps = 2e-3
+    eps, cutoff = 2e-3, 0.012
+    got = gpu_eval(ctx, A, M, T, W, psi, eps, cutoff)
+    want = C.evaluate_dual(A, M, T, W, psi, eps, cutoff, workers=4)
+    assert got["candidate_pairs"] == want["candidate_pairs"]
+    assert got["empty_candidate_atoms"] == want["empty_candidate_atoms"] >= 40
+    assert abs(got["J"] - want["J"]) <= TOL * abs(want["J"])
+    # (D = sum m_q exp(-L_q) overflows in the reference as well: the far atoms)
+    assert got["D"] == want["D"] or abs(got["D"] - want["D"]) <= TOL * abs(want["D"])
+    gm = got["gradient"] + W                # nu~ (the transported marginal), scale of the masses
+    wm = want["gradient"] + W
+    assert np.max(np.abs(gm - wm)) <= TOL * np.max(wm)
+    again = gpu_eval(ctx, A, M, T, W, psi, eps, cutoff)
+    assert again["J"] == got["J"] and np.array_equal(again["gradient"], got["gradient"])

@@ -1313,14 +1313,15 @@ __device__ __forceinline__ void tm_items2(const FusedSmem& sm, const FusedArgs& 
 #pragma unroll 1
   for (int h = 0; h < 4; ++h) {
     const unsigned b0 = static_cast<unsigned>(m0), b1 = static_cast<unsigned>(m1);
+    m0 >>= 16;
+    m1 >>= 16;
+    if (!__any_sync(0xffffffffu, ((b0 | b1) & 0xffffu) != 0u)) continue;  // no item of the pass takes these atoms
 #pragma unroll
     for (int a = 0; a < 16; ++a) {
       const double4 X = atab[16 * h + a];
       acc0 = exp2_acc_t(fma(X.x, i0.y0, fma(X.y, i0.y1, fma(X.z, i0.y2, X.w))), acc0, tb, (b0 >> a) & 1u);
       acc1 = exp2_acc_t(fma(X.x, i1.y0, fma(X.y, i1.y1, fma(X.z, i1.y2, X.w))), acc1, tb, (b1 >> a) & 1u);
     }
-    m0 >>= 16;
-    m1 >>= 16;
   }
   tm_flush(sm, A, k0, i0.w, acc0);
   tm_flush(sm, A, k1, i1.w, acc1);

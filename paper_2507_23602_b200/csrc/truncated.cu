@@ -44,7 +44,7 @@ constexpr int kT = 128;        // threads per CTA = points per chunk
 constexpr int kTileT = 256;    // staged points per tile (fp64 kernel)
 constexpr int kTileT32 = 384;  // staged points per tile (fp32 kernel)
 #ifndef RSOT_FULLIN_RATIO2
-#define RSOT_FULLIN_RATIO2 49.0f  // full-in split when r > 7 warp-box half-diagonals
+#define RSOT_FULLIN_RATIO2 16.0f  // full-in split when r > 4 warp-box half-diagonals
 #endif
 #ifndef RSOT_P2_TM
 #define RSOT_P2_TM 1  // target-major phase 2 over per-warp item records (unsplit non-safe CTAs)
@@ -1472,10 +1472,12 @@ __device__ void fused_scan(FusedSmem& sm, const FusedArgs& A, const WarpBox& wb,
   ListT* const list = sm.wlist[warp];
   const bool wide = SAFE && sm.R.wide;
   const Step32 K = make_step(at.lo_thr, at.hi_thr);
-  // Full-in split only when the ball is large against the warp box (r > 7
-  // half-diagonals, e.g. cfg3: ~half the culled targets are full-in, -6 %);
-  // for smaller ratios (cfg5) the split list handling costs more than the
-  // skipped pre-tests (+5 %).
+  // Full-in split only when the ball is large against the warp box (r > 4
+  // half-diagonals; cfg3: ~half the culled targets are full-in, cfg5 (4.9
+  // half-diagonals): ~1/8).  With the tiled phase 2 the threshold was 7: the
+  // split list handling cost more than it saved at cfg5 (+5 %); with the
+  // target-major phase 2, where a full-in item costs what a mixed one does,
+  // it pays there too (cfg5 39.65 -> 38.61 ms).
   float full_thr = -1.0f;
   if (!DEBUG && at.lo_thr > 0.f) {
     const float hx = wb.hi0 - wb.lo0, hy = wb.hi1 - wb.lo1, hz = wb.hi2 - wb.lo2;
